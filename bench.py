@@ -1,0 +1,402 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 all-pairs hot path (BASELINE.json metric: G pair-tests/s
+at N=2^20, 1/2/4/8 B200, vs the CPU reference).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Workload (config 3): N = 2^20 uniform fp32 unit-diameter
+spheres (generators.random_spheres(2^20, (4*pi*N/3)^(1/3), 1)), one step =
+one pass over all C(N,2) pairs computing the exact contact count and the
+softened inverse-square sum, balanced schedule on uniform tiles.  With N>1
+ranks each GPU owns an equal-work slab of outer rows and the partials meet in
+one NCCL int64 all-reduce (strong scaling: total work fixed).
+
+Rank 0 prints ONE JSON line.  `value` is device-resident throughput (inputs
+already in HBM; CUDA events on the launching stream; max over ranks); `e2e`
+is the same metric through the C-ABI host entry (pc_pairs_host) with the
+pinned host array copied in and the result copied out every step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_POINTS = 2**20
+FLOPS_PER_PAIR = 12  # reference formula: 3 sub, 3 mul, 2 add (d^2), compare, 1 add + 1 div (1/(1+d^2)), 1 accumulate
+THROTTLE_BAD = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--no-secondary", action="store_true", help="skip the config-2/5 side measurements")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-rows-per-core", type=int, default=12)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_input():
+    from paper_1901_11204_b200 import generators as gen
+
+    return gen.random_spheres(N_POINTS, gen.contact_box_edge(N_POINTS), 1).astype(np.float32)
+
+
+# ---------------------------------------------------------------- clocks --
+class ClockSampler:
+    """nvidia-smi sampled every 200 ms while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out = ""
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        loaded = [r for r in rows if r[0] > 0.5 * r[1]] or rows
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for _, _, parts in loaded:
+            for name, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median([r[0] for r in loaded])), "sm_max_mhz": max(r[1] for r in loaded),
+                "samples": len(loaded), "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------ reference --
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import cpu_baseline as cb
+
+    obj = workload_input()
+    n = len(obj)
+    cores = os.cpu_count() or 1
+    per_step = cores * max(1, args.cpu_rows_per_core // 2)
+    times, pairs = [], []
+    for step in range(args.warmup + args.steps):
+        rows = cb.sample_rows(n, per_step, 1, offset=step * 7919)
+        p, wall, used = cb.time_sample(obj, rows, "balanced", processes=cores)
+        if step >= args.warmup:
+            times.append(wall)
+            pairs.append(p)
+    rate = sum(pairs) / sum(times) / 1e9
+    line = {
+        "impl": "reference", "metric": f"G pair-tests/s at N=2^20 (contact count + inverse-square sum)",
+        "value": rate, "unit": "Gpair/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg3: 2^20 uniform spheres, balanced schedule, reference per-row numpy (oracle port)",
+                   "n_points": n, "sample": f"{per_step} balanced rows per step x 2 interaction passes"},
+        "cpu_baseline": {"value": rate, "unit": "Gpair/s", "cores": cores, "kind": "port",
+                         "sample": f"{per_step} rows/step of {n} ({sum(pairs)} pair-tests timed)",
+                         "cpu": cb.cpu_model(), "numpy": np.__version__},
+        "e2e": {"value": rate, "unit": "Gpair/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -------------------------------------------------------------- helpers --
+def l2_flush(buf):
+    buf.zero_()
+
+
+def cpu_baseline_leg(obj, rows_per_core):
+    from oracle import cpu_baseline as cb
+
+    cores = os.cpu_count() or 1
+    rows = cb.sample_rows(len(obj), cores * rows_per_core, 1)
+    pairs, wall, used = cb.time_sample(obj, rows, "balanced", processes=cores)
+    return {"value": pairs / wall / 1e9, "unit": "Gpair/s", "cores": used, "kind": "port",
+            "sample": f"{len(rows)} balanced rows of N=2^20 (reference per-row numpy, collision_indicator + "
+                      f"inverse-square passes, fork pool), {pairs} pair-tests in {wall:.1f} s",
+            "cpu": cb.cpu_model(), "numpy": np.__version__}
+
+
+def secondary(torch, lib, stream):
+    """Config 2 (naive vs balanced at N=65,536) and config 5 (counting array)."""
+    import ctypes
+
+    from paper_1901_11204_b200 import _lib
+    from paper_1901_11204_b200 import generators as gen
+
+    out = {}
+    # ---- config 2
+    n2 = 65536
+    obj2 = gen.random_spheres(n2, gen.contact_box_edge(n2), 0).astype(np.float32)
+    d2 = torch.from_numpy(obj2).cuda()
+    ws = torch.empty(_lib.workspace_bytes(n2), dtype=torch.uint8, device="cuda")
+    res = torch.zeros(8, dtype=torch.int64, device="cuda")
+    pairs2 = n2 * (n2 - 1) // 2
+    rows = {}
+    for label, sched, tiling in (("naive_standard_per_row_tile", _lib.PC_STANDARD, _lib.PC_TILE_PER_ROW_TILE),
+                                 ("balanced_per_row_tile", _lib.PC_BALANCED, _lib.PC_TILE_PER_ROW_TILE),
+                                 ("balanced_uniform_tiles", _lib.PC_BALANCED, _lib.PC_TILE_FLAT)):
+        for _ in range(3):
+            _lib.pairs_async(d2.data_ptr(), _lib.PC_F32, n2, _lib.PC_COLLISION, sched, np.array([0, n2]),
+                             ws.data_ptr(), ws.numel(), res.data_ptr(), stream.cuda_stream, tiling)
+        _lib.kernel_timing(True)
+        reps = 20
+        for _ in range(reps):
+            _lib.pairs_async(d2.data_ptr(), _lib.PC_F32, n2, _lib.PC_COLLISION, sched, np.array([0, n2]),
+                             ws.data_ptr(), ws.numel(), res.data_ptr(), stream.cuda_stream, tiling)
+        ms, cnt = _lib.kernel_timing_read()
+        _lib.kernel_timing(False)
+        torch.cuda.synchronize()
+        count = int(res[0].item())
+        rows[label] = {"kernel_ms": ms / cnt, "Gpair_per_s": pairs2 / (ms / cnt * 1e-3) / 1e9, "count": count}
+    rows["naive_over_balanced_time"] = rows["naive_standard_per_row_tile"]["kernel_ms"] / \
+        rows["balanced_uniform_tiles"]["kernel_ms"]
+    rows["paper_reference_ratio"] = "1.12x on P100 for N > 525,000 (PAPER.md:419)"
+    out["cfg2_naive_vs_balanced_n65536"] = rows
+    del d2, ws
+
+    # ---- config 5: counting array, device-resident int32 coordinates
+    n5, a5 = 2**26, 512
+    pts = gen.grid_points(n5, a5)
+    d5 = torch.from_numpy(pts.astype(np.int32)).cuda()
+    ncell = int(lib.pc_lattice_grid_cells(a5))
+    grid = torch.zeros(ncell, dtype=torch.int32, device="cuda")
+    keys = torch.empty(n5, dtype=torch.int32, device="cuda")
+    r = _lib.LatticeResult()
+    times = []
+    for step in range(8):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rc = lib.pc_lattice_collisions(d5.data_ptr(), _lib.PC_I32, 1, n5, a5, grid.data_ptr(), keys.data_ptr(), 1,
+                                       ctypes.byref(r), ctypes.c_void_p(stream.cuda_stream))
+        _lib.check(rc)
+        lib.pc_lattice_reset_keys(grid.data_ptr(), a5, keys.data_ptr(), n5, ctypes.c_void_p(stream.cuda_stream))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if step >= 3:
+            times.append(e0.elapsed_time(e1))
+    ms = float(np.median(times))
+    b_alg = 12 * n5 + 8 * n5 + 4 * n5 + 4 * n5 + 4 * n5  # coords, atomic RMW, key write, key read, zero write
+    out["cfg5_counting_array_n2^26"] = {
+        "wall_ms_per_step": ms, "count": int(r.count), "cells_touched": int(r.cells_touched),
+        "expected_count": 2101067, "step": "validate+histogram (Alg. 1, atomics) + sparse reset via touched keys",
+        "alg_bytes": b_alg, "achieved_GBps": b_alg / (ms * 1e-3) / 1e9}
+    del d5, grid, keys
+    return out
+
+
+# ------------------------------------------------------------------ ours --
+def run_ours(args):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1901_11204_b200 import _lib
+    from paper_1901_11204_b200.distributed import row_slabs
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    os.environ["PAIRCOUNT_DEVICE"] = str(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.load()
+    stream = torch.cuda.current_stream()
+
+    obj = workload_input()
+    n = len(obj)
+    lo, hi = row_slabs(n, world, "balanced")[rank]
+    total_pairs = n * (n - 1) // 2
+    d_obj = torch.from_numpy(obj).cuda()
+    ws = torch.empty(_lib.workspace_bytes(n), dtype=torch.uint8, device="cuda")
+    res = torch.zeros(8, dtype=torch.int64, device="cuda")  # pc_pairs_result (40 B)
+    slots = torch.zeros(2 * world, dtype=torch.int64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    bounds = np.array([lo, hi], dtype=np.int64)
+
+    def step():
+        _lib.pairs_async(d_obj.data_ptr(), _lib.PC_F32, n, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, bounds,
+                         ws.data_ptr(), ws.numel(), res.data_ptr(), stream.cuda_stream, _lib.PC_TILE_FLAT)
+        launches = _lib.launches()
+        if world > 1:
+            slots.zero_()
+            slots[2 * rank: 2 * rank + 2].copy_(res[0:2])
+            dist.all_reduce(slots)  # the one NCCL int64 all-reduce of partials
+        return launches
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    launches = 0
+    elapsed = 0.0
+    _lib.kernel_timing(True)
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            l2_flush(flush)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            launches += step()
+            e1.record(stream)
+            e1.synchronize()
+            elapsed += e0.elapsed_time(e1)
+    torch.cuda.synchronize()
+    kern_ms, kern_launches = _lib.kernel_timing_read()
+    _lib.kernel_timing(False)
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+        counts = slots.view(world, 2)[:, 0].sum().item()
+    else:
+        counts = int(res[0].item())
+    ms_per_step = elapsed / args.steps
+    value = total_pairs / (ms_per_step * 1e-3) / 1e9
+
+    # ---- end-to-end through the C-ABI host entry, pinned host buffer
+    pinned = torch.from_numpy(obj).pin_memory()
+    host_view = pinned.numpy()
+    bnd = [lo, hi]
+    for _ in range(2):
+        _lib.pairs_host(host_view, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, bnd)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    e2e_launches = 0
+    for _ in range(args.steps):
+        (r,) = _lib.pairs_host(host_view, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, bnd)
+        e2e_launches += _lib.launches()
+        if world > 1:
+            t_slots = torch.zeros(2 * world, dtype=torch.int64, device="cuda")
+            t_slots[2 * rank] = int(r.count)
+            t_slots[2 * rank + 1] = int(np.array([r.sum]).view(np.int64)[0])
+            dist.all_reduce(t_slots)
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": total_pairs / e2e_s / 1e9, "unit": "Gpair/s", "h2d_bytes_per_step": int(host_view.nbytes),
+           "d2h_bytes_per_step": 40, "ms_per_step": e2e_s * 1e3,
+           "path": "pc_pairs_host (ctypes) from pinned host memory; one H2D + prep + kernel + finalize + D2H per step"}
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (pairs_kernel, direct formula)
+    kern_ms_avg = kern_ms / max(1, kern_launches)
+    rank_pairs = (hi - lo) * (n // 2)  # balanced rows own n//2 (odd) or n/2, n/2-1 (even) pairs
+    from paper_1901_11204_b200.pair_schedule import row_pairs
+    rank_pairs = row_pairs(n, lo, hi, "balanced")
+    achieved_tflops = FLOPS_PER_PAIR * rank_pairs / (kern_ms_avg * 1e-3) / 1e12
+    ffma_rate, _ = _lib.microbench(0)
+    peak_tflops = 2.0 * ffma_rate / 1e12
+    traffic = None
+    tfile = ROOT / "profiles" / "kernel_traffic.json"
+    if tfile.exists():
+        try:
+            traffic = json.loads(tfile.read_text()).get("pairs_kernel_direct_flat_n2^20")
+        except (ValueError, OSError):
+            traffic = None
+    clocks = clk.summary()
+    roofline = {"bound": "fp32", "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
+                "frac": achieved_tflops / peak_tflops, "traffic": traffic,
+                "kernel": "pairs_kernel<128,8,256,DIRECT,FLAT>", "kernel_ms": kern_ms_avg,
+                "flops_per_pair": FLOPS_PER_PAIR,
+                "peak_source": "measured live: pc_microbench FFMA stream x 2 flop (no FP32 entry in MEASURED_PEAKS.json)",
+                "pairs_per_s_kernel": rank_pairs / (kern_ms_avg * 1e-3)}
+
+    line = {
+        "metric": "G pair-tests/s at N=2^20 (contact count + inverse-square sum)",
+        "value": value, "unit": "Gpair/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "cfg3: N=2^20 uniform fp32 unit spheres, exact contact count + softened "
+                               "inverse-square sum, balanced schedule on uniform tiles",
+                   "n_points": n, "pairs_per_step": total_pairs, "schedule": "balanced", "tiling": "flat",
+                   "parallelism": f"row slabs x{world}, one NCCL int64 all-reduce" if world > 1 else "1 GPU",
+                   "l2": "flushed between timed steps (256 MiB memset)", "contacts": int(counts)},
+        "roofline": roofline,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_leg(obj, args.cpu_rows_per_core)
+    if world == 1 and not args.no_secondary:
+        line["secondary"] = secondary(torch, lib, stream)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,225 @@
+"""ctypes binding of libpaircount.so (include/paircount.h).
+
+This is the only place the package touches native code.  There is no CPU
+fallback: if the shared library is missing, or no CUDA device is visible,
+every compute entry point raises ``PaircountUnavailable`` (a RuntimeError).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB_PATH = HERE / "libpaircount.so"
+
+# --- codes (include/paircount.h) -------------------------------------------
+PC_OK = 0
+PC_ERR_CUDA = -1
+PC_ERR_ARG = 1
+PC_ERR_DOMAIN = 2
+PC_ERR_RANGE = 3
+PC_ERR_OVERFLOW = 4
+PC_ERR_ODD = 5
+
+PC_F32, PC_F64, PC_I32, PC_I64 = 0, 1, 2, 3
+PC_STANDARD, PC_BALANCED = 0, 1
+PC_COLLISION, PC_COLLISION_INVSQ, PC_COINCIDE, PC_MANHATTAN1 = 1, 2, 3, 4
+PC_TILE_AUTO, PC_TILE_PER_ROW_TILE, PC_TILE_FLAT = 0, 1, 2
+
+SCHEDULE_CODES = {"standard": PC_STANDARD, "balanced": PC_BALANCED}
+DTYPE_CODES = {np.dtype(np.float32): PC_F32, np.dtype(np.float64): PC_F64,
+               np.dtype(np.int32): PC_I32, np.dtype(np.int64): PC_I64}
+
+# Every symbol include/paircount.h declares (checked by tests/test_abi.py).
+EXPORTED = (
+    "pc_last_error", "pc_version", "pc_device_count", "pc_set_device", "pc_device_alloc",
+    "pc_device_free", "pc_memcpy_h2d", "pc_memcpy_d2h", "pc_stream_sync",
+    "pc_pairs_workspace_bytes", "pc_pairs", "pc_pairs_async", "pc_pairs_host",
+    "pc_last_launch_count", "pc_kernel_timing", "pc_kernel_timing_read", "pc_lattice_grid_cells", "pc_lattice_key_bytes",
+    "pc_lattice_collisions", "pc_lattice_contacts", "pc_lattice_reset_keys",
+    "pc_lattice_reset_beads", "pc_grid_count_nonzero", "pc_microbench",
+)
+
+
+class PaircountUnavailable(RuntimeError):
+    """libpaircount.so is not built or no CUDA device is visible."""
+
+
+class PaircountError(RuntimeError):
+    """A CUDA call inside libpaircount failed."""
+
+
+class PairsResult(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_int64), ("sum", ctypes.c_double), ("pairs", ctypes.c_int64),
+                ("exact_checks", ctypes.c_int64), ("error", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class LatticeResult(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_int64), ("beads_processed", ctypes.c_int64),
+                ("cells_touched", ctypes.c_int64), ("doubled", ctypes.c_int64),
+                ("error", ctypes.c_int32), ("reserved", ctypes.c_int32), ("detail", ctypes.c_int64)]
+
+
+_vp, _i32, _i64, _sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+_SIGS = {
+    "pc_last_error": ([], ctypes.c_char_p),
+    "pc_version": ([], ctypes.c_char_p),
+    "pc_device_count": ([ctypes.POINTER(_i32)], ctypes.c_int),
+    "pc_set_device": ([_i32], ctypes.c_int),
+    "pc_device_alloc": ([_sz, ctypes.POINTER(_vp)], ctypes.c_int),
+    "pc_device_free": ([_vp], ctypes.c_int),
+    "pc_memcpy_h2d": ([_vp, _vp, _sz, _vp], ctypes.c_int),
+    "pc_memcpy_d2h": ([_vp, _vp, _sz, _vp], ctypes.c_int),
+    "pc_stream_sync": ([_vp], ctypes.c_int),
+    "pc_pairs_workspace_bytes": ([_i64, _i32], _sz),
+    "pc_pairs": ([_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _sz, _vp, _vp], ctypes.c_int),
+    "pc_pairs_async": ([_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _sz, _vp, _vp], ctypes.c_int),
+    "pc_pairs_host": ([_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
+    "pc_last_launch_count": ([], _i32),
+    "pc_kernel_timing": ([_i32], ctypes.c_int),
+    "pc_kernel_timing_read": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i32)], ctypes.c_int),
+    "pc_lattice_grid_cells": ([_i64], _i64),
+    "pc_lattice_key_bytes": ([_i64], _i32),
+    "pc_lattice_collisions": ([_vp, _i32, _i32, _i64, _i64, _vp, _vp, _i32, _vp, _vp], ctypes.c_int),
+    "pc_lattice_contacts": ([_vp, _i32, _i32, _i64, _i64, _vp, _vp, _i32, _vp, _vp], ctypes.c_int),
+    "pc_lattice_reset_keys": ([_vp, _i64, _vp, _i64, _vp], ctypes.c_int),
+    "pc_lattice_reset_beads": ([_vp, _i32, _i32, _i64, _i64, _vp, _vp, _vp], ctypes.c_int),
+    "pc_grid_count_nonzero": ([_vp, _i64, ctypes.POINTER(_i64), _vp], ctypes.c_int),
+    "pc_microbench": ([_i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+}
+
+_lock = threading.Lock()
+_handle = None
+_device_checked = False
+
+
+def load(require_device: bool = True):
+    """Load (once) and return the ctypes handle; fail loudly if unavailable."""
+    global _handle, _device_checked
+    with _lock:
+        if _handle is None:
+            if not LIB_PATH.exists():
+                raise PaircountUnavailable(
+                    f"{LIB_PATH} is not built; run `python -m paper_1901_11204_b200.build` "
+                    "(there is no CPU fallback)")
+            lib = ctypes.CDLL(str(LIB_PATH))
+            for name, (args, res) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = res
+            _handle = lib
+        if require_device and not _device_checked:
+            cnt = ctypes.c_int32(0)
+            rc = _handle.pc_device_count(ctypes.byref(cnt))
+            if rc != PC_OK or cnt.value < 1:
+                raise PaircountUnavailable(
+                    "no CUDA device visible to libpaircount (there is no CPU fallback): "
+                    + _handle.pc_last_error().decode())
+            dev = int(os.environ.get("PAIRCOUNT_DEVICE", "0"))
+            check(_handle.pc_set_device(dev))
+            _device_checked = True
+        return _handle
+
+
+def last_error() -> str:
+    return load(require_device=False).pc_last_error().decode()
+
+
+def check(rc: int) -> None:
+    if rc == PC_ERR_CUDA:
+        raise PaircountError(last_error())
+    if rc == PC_ERR_ARG:
+        raise ValueError(last_error())
+
+
+def launches() -> int:
+    """Kernel launches issued by the last pairs/lattice call on this thread."""
+    return int(load(require_device=False).pc_last_launch_count())
+
+
+# --- all-pairs --------------------------------------------------------------
+
+def pairs_host(xyz: np.ndarray, interaction: int, schedule: int, bounds, tiling: int = PC_TILE_AUTO):
+    """Run pc_pairs_host on a C-contiguous (n, 3) array; returns PairsResult[]."""
+    lib = load()
+    arr = np.ascontiguousarray(xyz)
+    code = DTYPE_CODES[arr.dtype]
+    b = np.ascontiguousarray(np.asarray(bounds, dtype=np.int64))
+    nr = len(b) - 1
+    res = (PairsResult * nr)()
+    rc = lib.pc_pairs_host(arr.ctypes.data, code, len(arr), interaction, schedule, tiling, nr,
+                           b.ctypes.data, ctypes.addressof(res))
+    check(rc)
+    return list(res)
+
+
+def pairs_async(xyz_ptr: int, dtype_code: int, n: int, interaction: int, schedule: int, bounds_host: np.ndarray,
+                workspace_ptr: int, workspace_bytes: int, results_dev_ptr: int, stream_ptr: int,
+                tiling: int = PC_TILE_AUTO) -> None:
+    """Device-pointer entry (bench / torch users): enqueue, no synchronisation."""
+    lib = load()
+    b = np.ascontiguousarray(bounds_host, dtype=np.int64)
+    rc = lib.pc_pairs_async(xyz_ptr, dtype_code, n, interaction, schedule, tiling, len(b) - 1, b.ctypes.data,
+                            workspace_ptr, workspace_bytes, results_dev_ptr, stream_ptr)
+    check(rc)
+
+
+def workspace_bytes(n: int, nranges: int = 1) -> int:
+    return int(load(require_device=False).pc_pairs_workspace_bytes(n, nranges))
+
+
+def kernel_timing(enable: bool) -> None:
+    check(load().pc_kernel_timing(1 if enable else 0))
+
+
+def kernel_timing_read():
+    """(summed main-kernel ms, launches) recorded since kernel_timing(True)."""
+    ms, cnt = ctypes.c_double(), ctypes.c_int32()
+    check(load().pc_kernel_timing_read(ctypes.byref(ms), ctypes.byref(cnt)))
+    return ms.value, cnt.value
+
+
+def microbench(kind: int):
+    lib = load()
+    rate, secs = ctypes.c_double(), ctypes.c_double()
+    check(lib.pc_microbench(kind, ctypes.byref(rate), ctypes.byref(secs)))
+    return rate.value, secs.value
+
+
+# --- device memory (used by the lattice mirror; no torch dependency) --------
+
+class DeviceBuffer:
+    """A cudaMalloc'd, zero-filled buffer owned by Python."""
+
+    def __init__(self, nbytes: int):
+        self.nbytes = int(nbytes)
+        ptr = ctypes.c_void_p()
+        rc = load().pc_device_alloc(self.nbytes, ctypes.byref(ptr))
+        if rc != PC_OK:
+            raise MemoryError(f"cannot allocate {self.nbytes} device bytes: {last_error()}")
+        self.ptr = ptr.value
+
+    def to_host(self, dtype, count: int) -> np.ndarray:
+        out = np.empty(count, dtype=dtype)
+        lib = load()
+        check(lib.pc_memcpy_d2h(out.ctypes.data, self.ptr, out.nbytes, None))
+        check(lib.pc_stream_sync(None))
+        return out
+
+    def free(self) -> None:
+        if getattr(self, "ptr", None):
+            try:
+                _handle.pc_device_free(self.ptr)
+            finally:
+                self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

@@ -1,0 +1,1358 @@
+// libpaircount.so -- sm_100a kernels and the C ABI of include/paircount.h.
+//
+// Hot path (BASELINE.json north_star):
+//   * all-pairs count over the i<j triangle under the reference's two outer
+//     schedules (standard = Alg. 3, balanced = Alg. 4; spi_engine.py:102-106,
+//     pair_schedule.py:49-59), exact for collision_indicator
+//     (spi_engine.py:62-73) and the integer oracles (lattice_counter.py:
+//     227-255), plus the softened inverse-square sum;
+//   * the O(N) counting array (Alg. 1/2; lattice_counter.py:125-217).
+//
+// Design (DESIGN.md has the full story):
+//   - Points are staged as one float4 each.  For counting, the float4 holds
+//     bounding-box-centred coordinates q and w = -|q|^2/2, so the test
+//     |p_i - p_j|^2 < thr becomes  q_i . q_j + w_j > c_i  with the row
+//     constant c_i = (|q_i|^2 - thr - band)/2: three FFMAs per pair.  The
+//     band is a rigorous bound on the fp32 rounding of that expression, so
+//     the fp32 test is a conservative filter; every pair it passes is
+//     re-evaluated by the reference's own float64/int64 predicate.  Results
+//     are therefore bit-exact while the inner loop is 3 FFMA + 1/2 FMNMX3.
+//   - A CTA holds R rows per thread in registers (T = NT*R rows per tile)
+//     and streams partner columns through double-buffered shared memory
+//     (cp.async 16 B per point); every LDS.128 is a warp broadcast reused
+//     across R rows.
+//   - Row ownership is the reference's: row i owns column offsets
+//     s in [1, lim(i)] (standard: lim = n-1-i, j = i+s; balanced:
+//     lim = steps_for(n,i), j = (i+s) mod n).  A row tile walks column
+//     offsets s' = 1 .. L relative to its first row; window cells that a row
+//     does not own are rejected in the exact slow path (counts) or masked in
+//     the few edge chunks (sums), so per-row-range results equal the
+//     reference's _run_outer partials and the fast path has no masks.
+//   - PC_TILE_FLAT (balanced): every row tile has the same window length L,
+//     so the (tile, column) space is a uniform rectangle, split into equal
+//     contiguous column ranges over a persistent grid sized to the SM count.
+//   - PC_TILE_PER_ROW_TILE: one CTA per row tile (the paper's scheme,
+//     PAPER.md:417); with the standard schedule this is the naive kernel.
+//   - Reduction: warp shuffles, CTA shared memory, one slot write per CTA,
+//     then a fixed-order finalize -- deterministic for the float64 sum.
+
+#include "../../include/paircount.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+// Optional CUDA-event timing of the main all-pairs kernel (bench.py's
+// roofline needs that kernel's own duration, on the stream it runs on).
+struct EvPair {
+    cudaEvent_t a, b;
+};
+thread_local bool g_timing = false;
+thread_local EvPair g_ev[4096];
+thread_local int g_ev_used = 0, g_ev_made = 0;
+
+int cuda_fail(const char* what, cudaError_t e) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return PC_ERR_CUDA;
+}
+int arg_fail(const char* what) {
+    g_err = what;
+    return PC_ERR_ARG;
+}
+
+#define CK(call)                                                  \
+    do {                                                          \
+        cudaError_t e_ = (call);                                  \
+        if (e_ != cudaSuccess) return cuda_fail(#call, e_);       \
+    } while (0)
+#define CK_LAUNCH(what)                                           \
+    do {                                                          \
+        ++g_launches;                                             \
+        cudaError_t e_ = cudaGetLastError();                      \
+        if (e_ != cudaSuccess) return cuda_fail(what, e_);        \
+    } while (0)
+
+constexpr int kPredSphere = 0, kPredCoincide = 1, kPredManhattan1 = 2;
+
+// ------------------------------------------------------------------------
+// small device helpers
+// ------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long enc_f64(double d) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(d);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ __forceinline__ double dec_f64(unsigned long long e) {
+    unsigned long long b = (e >> 63) ? (e & 0x7fffffffffffffffull) : ~e;
+    double d;
+    memcpy(&d, &b, sizeof d);
+    return d;
+}
+// ordered code 0 (memset value) means "no point seen": decode as 0.0
+__host__ __device__ __forceinline__ double dec_f64_or0(unsigned long long e) { return e ? dec_f64(e) : 0.0; }
+__device__ __forceinline__ unsigned long long enc_i64(long long v) {
+    return (unsigned long long)v ^ 0x8000000000000000ull;
+}
+__host__ __device__ __forceinline__ long long dec_i64(unsigned long long e) {
+    return (long long)(e ^ 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float min3f(float a, float b, float c) {
+    float d;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// coordinate k of point i, as double / int64
+__device__ __forceinline__ double coord_f64(const void* xyz, int dtype, long long i, int k) {
+    switch (dtype) {
+        case PC_F32: return (double)((const float*)xyz)[3 * i + k];
+        case PC_F64: return ((const double*)xyz)[3 * i + k];
+        case PC_I32: return (double)((const int*)xyz)[3 * i + k];
+        default: return (double)((const long long*)xyz)[3 * i + k];
+    }
+}
+__device__ __forceinline__ long long coord_i64(const void* xyz, int dtype, long long i, int k) {
+    return dtype == PC_I32 ? (long long)((const int*)xyz)[3 * i + k]
+                           : ((const long long*)xyz)[3 * i + k];
+}
+
+// The reference predicates, evaluated exactly as the reference evaluates them.
+__device__ bool exact_pair(const void* xyz, int dtype, int pred, long long i, long long j) {
+    if (pred == kPredSphere) {
+        // collision_indicator (spi_engine.py:68-73): float64 upcast,
+        // d2 = ((a-b)**2).sum(-1) in numpy order (dx^2 + dy^2) + dz^2, no FMA,
+        // strict < 1.0.
+        double dx = __dsub_rn(coord_f64(xyz, dtype, i, 0), coord_f64(xyz, dtype, j, 0));
+        double dy = __dsub_rn(coord_f64(xyz, dtype, i, 1), coord_f64(xyz, dtype, j, 1));
+        double dz = __dsub_rn(coord_f64(xyz, dtype, i, 2), coord_f64(xyz, dtype, j, 2));
+        double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+        return d2 < 1.0;
+    }
+    long long d[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        d[k] = (long long)((unsigned long long)coord_i64(xyz, dtype, i, k) -
+                           (unsigned long long)coord_i64(xyz, dtype, j, k));
+    if (pred == kPredCoincide) return d[0] == 0 && d[1] == 0 && d[2] == 0;  // lattice_counter.py:238-241
+    // Manhattan == 1 with numpy int64 wrap-around semantics (lattice_counter.py:252-255)
+    unsigned long long man = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) man += (unsigned long long)(d[k] < 0 ? -d[k] : d[k]);
+    return man == 1ull;
+}
+
+// ------------------------------------------------------------------------
+// preparation: bounding box, centring, float4 staging, error bands
+// ------------------------------------------------------------------------
+struct PrepStats {
+    unsigned long long mn[3], mx[3];  // ordered encodings (f64 for float input, i64 for int input)
+    unsigned long long maxabs;        // ordered f64: max |coordinate| (raw)
+    unsigned long long mnorm;         // ordered f64: max |q|^2 of the staged fp32 coordinates
+    int nonfinite;
+    int pad;
+};
+
+__device__ __forceinline__ bool is_int_dtype(int dtype) { return dtype >= PC_I32; }
+
+__global__ void prep_bbox_kernel(const void* __restrict__ xyz, int dtype, long long n,
+                                 PrepStats* __restrict__ st) {
+    const bool isint = is_int_dtype(dtype);
+    unsigned long long mn[3], mx[3];
+    double maxabs = 0.0;
+    int bad = 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { mn[k] = ~0ull; mx[k] = 0ull; }
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            unsigned long long e;
+            if (isint) {
+                long long v = coord_i64(xyz, dtype, i, k);
+                e = enc_i64(v);
+                maxabs = fmax(maxabs, fabs((double)v));
+            } else {
+                double v = coord_f64(xyz, dtype, i, k);
+                if (!isfinite(v)) { bad = 1; v = 0.0; }
+                e = enc_f64(v);
+                maxabs = fmax(maxabs, fabs(v));
+            }
+            mn[k] = mn[k] < e ? mn[k] : e;
+            mx[k] = mx[k] > e ? mx[k] : e;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            unsigned long long a = __shfl_xor_sync(0xffffffffu, mn[k], o);
+            unsigned long long b = __shfl_xor_sync(0xffffffffu, mx[k], o);
+            mn[k] = mn[k] < a ? mn[k] : a;
+            mx[k] = mx[k] > b ? mx[k] : b;
+        }
+        maxabs = fmax(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, o));
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            atomicMin(&st->mn[k], mn[k]);
+            atomicMax(&st->mx[k], mx[k]);
+        }
+        atomicMax(&st->maxabs, enc_f64(maxabs));
+        if (bad) atomicOr(&st->nonfinite, 1);
+    }
+}
+
+// Centre of the bounding box; for integer input an exact int64 midpoint so
+// p - centre is exact (SURVEY.md hard part 1 / DESIGN.md "error band").
+__device__ __forceinline__ void bbox_centre(const PrepStats& st, int dtype, double c[3], long long ci[3]) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (is_int_dtype(dtype)) {
+            long long lo = dec_i64(st.mn[k]), hi = dec_i64(st.mx[k]);
+            ci[k] = lo + (long long)(((unsigned long long)hi - (unsigned long long)lo) >> 1);
+            c[k] = 0.0;
+        } else {
+            c[k] = 0.5 * dec_f64(st.mn[k]) + 0.5 * dec_f64(st.mx[k]);
+            ci[k] = 0;
+        }
+    }
+}
+
+template <bool DIRECT>
+__global__ void prep_stage_kernel(const void* __restrict__ xyz, int dtype, long long n,
+                                  PrepStats* __restrict__ st, float4* __restrict__ pts) {
+    double c[3];
+    long long ci[3];
+    bbox_centre(*st, dtype, c, ci);
+    const bool isint = is_int_dtype(dtype);
+    double mnorm = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        float q[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (DIRECT) {
+                q[k] = (float)coord_f64(xyz, dtype, i, k);  // raw coordinates: exact for fp32 input
+            } else if (isint) {
+                long long v = (long long)((unsigned long long)coord_i64(xyz, dtype, i, k) -
+                                          (unsigned long long)ci[k]);
+                q[k] = (float)(double)v;
+            } else {
+                q[k] = (float)(coord_f64(xyz, dtype, i, k) - c[k]);
+            }
+        }
+        double nq = (double)q[0] * q[0] + (double)q[1] * q[1] + (double)q[2] * q[2];
+        if (!(nq <= 1e300)) nq = INFINITY;
+        mnorm = fmax(mnorm, nq);
+        pts[i] = make_float4(q[0], q[1], q[2], DIRECT ? 0.0f : (float)(-0.5 * nq));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mnorm = fmax(mnorm, __shfl_xor_sync(0xffffffffu, mnorm, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&st->mnorm, enc_f64(mnorm));
+}
+
+// ------------------------------------------------------------------------
+// the all-pairs kernel
+// ------------------------------------------------------------------------
+struct Slot {
+    unsigned long long count;
+    unsigned long long checks;
+    double sum;
+    unsigned long long pad;
+};
+
+struct PairsArgs {
+    const float4* pts;
+    const void* xyz;
+    const PrepStats* st;
+    Slot* slots;
+    int dtype, pred, sched;
+    float thr;
+    int n, lo, hi;      // n < 2^31 enforced on the host
+    int n_tiles;        // row tiles in [lo, hi)
+    long long L;        // FLAT: window length shared by every row tile
+    long long total;    // FLAT: n_tiles * L
+};
+
+__device__ __forceinline__ int steps_for_dev(int n, int i) {
+    // pair_schedule.py:49-59
+    if (n & 1) return (n - 1) >> 1;
+    return i < (n >> 1) ? (n >> 1) : (n >> 1) - 1;
+}
+
+template <int NT, int R, int W, bool DIRECT, bool FLAT>
+__global__ void __launch_bounds__(NT, 4) pairs_kernel(const PairsArgs a) {
+    constexpr int T = NT * R;
+    static_assert(W % NT == 0 && W % 2 == 0, "chunk must be a multiple of the CTA");
+    __shared__ __align__(16) float4 s_pts[2][W];
+    __shared__ int s_j[2][W];
+    __shared__ unsigned long long s_red[NT / 32][2];
+    __shared__ double s_sum[NT / 32];
+
+    const int tid = threadIdx.x;
+    const int n = a.n;
+    const bool bal = a.sched == PC_BALANCED;
+
+    // error bands: computed by every CTA from the prep stats
+    const double M = dec_f64_or0(a.st->mnorm);
+    const double X = dec_f64_or0(a.st->maxabs);
+    const bool force = !DIRECT && !(M < 1e30);  // fp32 filter unusable: exact path for every pair
+    const float half_tb = (float)(0.5 * ((double)a.thr + 3.814697265625e-06 * (M + 4.0)));
+    const double bd = 1.52587890625e-05 + (a.dtype == PC_F32 ? 0.0 : 9.5367431640625e-07 * X);
+    const float thr2 = (float)(1.0 + (double)a.thr + bd);
+    const int steps_min = (n & 1) ? (n - 1) >> 1 : (n >> 1) - 1;
+
+    // this CTA's column range
+    long long g, g_end;
+    if (FLAT) {
+        g = a.total * (long long)blockIdx.x / gridDim.x;
+        g_end = a.total * (long long)(blockIdx.x + 1) / gridDim.x;
+    } else {
+        const int i0 = a.lo + (int)blockIdx.x * T;
+        g = 0;
+        g_end = bal ? (long long)(T - 1 + (n >> 1)) : (long long)(n - 1 - i0);
+    }
+    auto tile_of = [&](long long gg) -> int { return FLAT ? (int)(gg / a.L) : (int)blockIdx.x; };
+    auto off_of = [&](long long gg) -> int { return FLAT ? (int)(gg % a.L) : (int)gg; };
+    auto width_of = [&](long long gg) -> int {
+        long long rem_tile = FLAT ? a.L - gg % a.L : g_end - gg;
+        long long w = rem_tile < (long long)W ? rem_tile : (long long)W;
+        return (int)(w < g_end - gg ? w : g_end - gg);
+    };
+
+    auto stage = [&](int buf, long long gg) {
+        const int t = tile_of(gg), off = off_of(gg), wc = width_of(gg);
+        const int i0 = a.lo + t * T;
+#pragma unroll
+        for (int q = 0; q < W / NT; ++q) {
+            const int k = q * NT + tid;
+            if (k < wc) {
+                long long j = (long long)i0 + off + 1 + k;  // s' = off + 1 + k
+                if (bal) {
+                    if (j >= n) j -= n;
+                    if (j >= n) j %= n;
+                }
+                cp_async16(&s_pts[buf][k], &a.pts[j]);
+                s_j[buf][k] = (int)j;
+            } else {
+                s_pts[buf][k] = DIRECT ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                       : make_float4(0.f, 0.f, 0.f, -INFINITY);
+                s_j[buf][k] = -1;
+            }
+        }
+        cp_async_commit();
+    };
+
+    float rx[R], ry[R], rz[R], rc[R];
+    int rlim[R];
+    int cur_tile = -1;
+    unsigned valid_rows = 0;
+    unsigned long long cnt = 0, checks = 0;
+    double sum = 0.0;
+
+    if (g < g_end) stage(0, g);
+    int buf = 0;
+    while (g < g_end) {
+        const long long g_next = g + width_of(g);
+        if (g_next < g_end) {
+            stage(buf ^ 1, g_next);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+
+        const int t = tile_of(g), off = off_of(g), wc = width_of(g);
+        const int i0 = a.lo + t * T;
+        if (t != cur_tile) {
+            cur_tile = t;
+            valid_rows = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int i = i0 + r * NT + tid;
+                const bool ok = i < a.hi;
+                const float4 v = ok ? a.pts[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+                rx[r] = v.x; ry[r] = v.y; rz[r] = v.z;
+                rc[r] = ok ? (force ? -INFINITY : -v.w - half_tb) : INFINITY;
+                rlim[r] = ok ? (bal ? steps_for_dev(n, i) : n - 1 - i) : 0;
+                valid_rows |= (ok ? 1u : 0u) << r;
+            }
+        }
+        const float4* sp = s_pts[buf];
+        const int* sj = s_j[buf];
+        unsigned fl = 0;
+
+        if (!DIRECT) {
+            // ---- fast path: 3 FFMA per pair + FMNMX3 per two pairs ----
+            float m[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) m[r] = -INFINITY;
+#pragma unroll 4
+            for (int k = 0; k < W; k += 2) {
+                const float4 c0 = sp[k], c1 = sp[k + 1];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    float t0 = fmaf(rx[r], c0.x, c0.w);
+                    float t1 = fmaf(rx[r], c1.x, c1.w);
+                    t0 = fmaf(ry[r], c0.y, t0);
+                    t1 = fmaf(ry[r], c1.y, t1);
+                    t0 = fmaf(rz[r], c0.z, t0);
+                    t1 = fmaf(rz[r], c1.z, t1);
+                    m[r] = max3f(m[r], t0, t1);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) fl |= (m[r] > rc[r] ? 1u : 0u) << r;
+            if (force) fl = valid_rows;
+        } else {
+            const bool dense = wc == W && i0 + T <= a.hi && off + 1 >= T && (!bal || off + W <= steps_min);
+            float m[R], acc[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) { m[r] = INFINITY; acc[r] = 0.f; }
+            if (dense) {
+                // ---- direct formula: p = 1 + |dr|^2; two pairs share one reciprocal ----
+#pragma unroll 2
+                for (int k = 0; k < W; k += 2) {
+                    const float4 c0 = sp[k], c1 = sp[k + 1];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const float dx0 = rx[r] - c0.x, dy0 = ry[r] - c0.y, dz0 = rz[r] - c0.z;
+                        const float dx1 = rx[r] - c1.x, dy1 = ry[r] - c1.y, dz1 = rz[r] - c1.z;
+                        const float p0 = fmaf(dz0, dz0, fmaf(dy0, dy0, fmaf(dx0, dx0, 1.0f)));
+                        const float p1 = fmaf(dz1, dz1, fmaf(dy1, dy1, fmaf(dx1, dx1, 1.0f)));
+                        m[r] = min3f(m[r], p0, p1);
+                        acc[r] = fmaf(p0 + p1, rcp_approx(p0 * p1), acc[r]);
+                    }
+                }
+            } else {
+                // ---- edge chunk: per-pair ownership mask ----
+                for (int k = 0; k < W; ++k) {
+                    const float4 c0 = sp[k];
+                    const int j = sj[k];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int rl = r * NT + tid;
+                        const bool ok = j >= 0 && (unsigned)(off + k - rl) < (unsigned)rlim[r];
+                        const float dx = rx[r] - c0.x, dy = ry[r] - c0.y, dz = rz[r] - c0.z;
+                        const float p = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1.0f)));
+                        acc[r] += ok ? rcp_approx(p) : 0.0f;
+                        m[r] = ok ? fminf(m[r], p) : m[r];
+                    }
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                sum += (double)acc[r];
+                fl |= (m[r] < thr2 ? 1u : 0u) << r;
+            }
+        }
+
+        // ---- slow path: re-scan flagged rows, exact reference predicate ----
+        if (__any_sync(0xffffffffu, fl != 0)) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (fl & (1u << r)) {
+                    const int rl = r * NT + tid;
+                    for (int k = 0; k < wc; ++k) {
+                        const float4 c0 = sp[k];
+                        bool cand;
+                        if (DIRECT) {
+                            const float dx = rx[r] - c0.x, dy = ry[r] - c0.y, dz = rz[r] - c0.z;
+                            cand = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1.0f))) < thr2;
+                        } else {
+                            float tt = fmaf(rx[r], c0.x, c0.w);
+                            tt = fmaf(ry[r], c0.y, tt);
+                            tt = fmaf(rz[r], c0.z, tt);
+                            cand = force || tt > rc[r];
+                        }
+                        if (cand && (unsigned)(off + k - rl) < (unsigned)rlim[r]) {
+                            ++checks;
+                            cnt += exact_pair(a.xyz, a.dtype, a.pred, i0 + rl, sj[k]) ? 1ull : 0ull;
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();  // buffer `buf` may be restaged next iteration
+        g = g_next;
+        buf ^= 1;
+    }
+
+    // ---- CTA reduction: one slot per CTA ----
+    cnt = warp_sum(cnt);
+    checks = warp_sum(checks);
+    sum = warp_sum(sum);
+    const int w = tid >> 5;
+    if ((tid & 31) == 0) { s_red[w][0] = cnt; s_red[w][1] = checks; s_sum[w] = sum; }
+    __syncthreads();
+    if (tid == 0) {
+        Slot s{0ull, 0ull, 0.0, 0ull};
+        for (int q = 0; q < NT / 32; ++q) { s.count += s_red[q][0]; s.checks += s_red[q][1]; s.sum += s_sum[q]; }
+        a.slots[blockIdx.x] = s;
+    }
+}
+
+// Fixed-order sum of the CTA slots into one result record.
+__global__ void finalize_kernel(const Slot* __restrict__ slots, int nslots, const PrepStats* __restrict__ st,
+                                long long pairs, int direct, pc_pairs_result* __restrict__ out) {
+    __shared__ unsigned long long sc[256], sk[256];
+    __shared__ double ss[256];
+    unsigned long long c = 0, k = 0;
+    double s = 0.0;
+    for (int q = threadIdx.x; q < nslots; q += blockDim.x) { c += slots[q].count; k += slots[q].checks; s += slots[q].sum; }
+    sc[threadIdx.x] = c; sk[threadIdx.x] = k; ss[threadIdx.x] = s;
+    __syncthreads();
+    for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h) {
+            sc[threadIdx.x] += sc[threadIdx.x + h];
+            sk[threadIdx.x] += sk[threadIdx.x + h];
+            ss[threadIdx.x] += ss[threadIdx.x + h];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        pc_pairs_result r;
+        r.count = (long long)sc[0];
+        r.sum = ss[0];
+        r.pairs = pairs;
+        r.exact_checks = (long long)sk[0];
+        r.error = st->nonfinite ? PC_ERR_DOMAIN : PC_OK;
+        if (direct && r.error == PC_OK && !(dec_f64_or0(st->maxabs) < 1e18)) r.error = PC_ERR_ARG;
+        r.reserved = 0;
+        *out = r;
+    }
+}
+
+// ------------------------------------------------------------------------
+// host side of the all-pairs path
+// ------------------------------------------------------------------------
+struct KernelCfg {
+    int nt, r, w;
+};
+constexpr KernelCfg kBig{128, 8, 256};
+constexpr KernelCfg kSmall{64, 2, 64};
+constexpr int kSmallN = 16384;
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+long long max_slots(long long n) { return 148LL * 64 + n / (kSmall.nt * kSmall.r) + 64; }
+
+struct WsLayout {
+    size_t pts, stats, slots, total;
+};
+WsLayout ws_layout(long long n) {
+    WsLayout l;
+    l.pts = 0;
+    l.stats = align_up((size_t)n * sizeof(float4), 256);
+    l.slots = l.stats + 256;
+    l.total = align_up(l.slots + (size_t)max_slots(n) * sizeof(Slot), 256);
+    return l;
+}
+
+long long row_pairs(long long n, long long lo, long long hi, int sched) {
+    if (hi <= lo) return 0;
+    if (sched == PC_STANDARD) return ((n - 1 - lo) + (n - 1 - (hi - 1))) * (hi - lo) / 2;
+    if (n & 1) return (hi - lo) * ((n - 1) / 2);
+    long long h = n / 2;
+    long long first = std::max(0LL, std::min(hi, h) - lo);
+    return first * h + (hi - lo - first) * (h - 1);
+}
+
+int g_num_sms[64] = {0};
+int num_sms() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!g_num_sms[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        g_num_sms[dev] = v > 0 ? v : 148;
+    }
+    return g_num_sms[dev];
+}
+
+template <int NT, int R, int W, bool DIRECT, bool FLAT>
+int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStream_t s) {
+    constexpr int T = NT * R;
+    auto kern = pairs_kernel<NT, R, W, DIRECT, FLAT>;
+    int grid;
+    if (FLAT) {
+        static thread_local int occ_cache[64] = {0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!occ_cache[dev & 63]) {
+            int occ = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0));
+            occ_cache[dev & 63] = occ > 0 ? occ : 1;
+        }
+        long long want = (long long)num_sms() * occ_cache[dev & 63];
+        long long chunks = (args.total + W - 1) / W;
+        grid = (int)std::max(1LL, std::min(want, chunks));
+    } else {
+        grid = args.n_tiles;
+    }
+    if (grid > n_slots_cap) return arg_fail("workspace too small for the CTA slots");
+    (void)T;
+    EvPair* ev = nullptr;
+    if (g_timing && g_ev_used < 4096) {
+        if (g_ev_used == g_ev_made) {
+            CK(cudaEventCreate(&g_ev[g_ev_made].a));
+            CK(cudaEventCreate(&g_ev[g_ev_made].b));
+            ++g_ev_made;
+        }
+        ev = &g_ev[g_ev_used++];
+        CK(cudaEventRecord(ev->a, s));
+    }
+    kern<<<grid, NT, 0, s>>>(args);
+    CK_LAUNCH("pairs_kernel");
+    if (ev) CK(cudaEventRecord(ev->b, s));
+    *nslots_out = grid;
+    return PC_OK;
+}
+
+template <int NT, int R, int W>
+int dispatch_cfg(PairsArgs args, bool direct, bool flat, long long cap, int* nslots, cudaStream_t s) {
+    constexpr int T = NT * R;
+    args.n_tiles = (args.hi - args.lo + T - 1) / T;
+    if (flat) {
+        args.L = (long long)(T - 1) + (args.n >> 1);
+        args.total = (long long)args.n_tiles * args.L;
+        return direct ? launch_pairs<NT, R, W, true, true>(args, cap, nslots, s)
+                      : launch_pairs<NT, R, W, false, true>(args, cap, nslots, s);
+    }
+    return direct ? launch_pairs<NT, R, W, true, false>(args, cap, nslots, s)
+                  : launch_pairs<NT, R, W, false, false>(args, cap, nslots, s);
+}
+
+int run_pairs(const void* xyz, int dtype, long long n, int interaction, int schedule, int tiling,
+              int nranges, const long long* bounds, void* workspace, size_t wsb,
+              pc_pairs_result* dres, cudaStream_t s) {
+    g_launches = 0;
+    if (dtype < PC_F32 || dtype > PC_I64) return arg_fail("unknown dtype");
+    if (schedule != PC_STANDARD && schedule != PC_BALANCED) return arg_fail("unknown schedule");
+    if (interaction < PC_COLLISION || interaction > PC_MANHATTAN1) return arg_fail("unknown interaction");
+    if ((interaction == PC_COINCIDE || interaction == PC_MANHATTAN1) && dtype < PC_I32)
+        return arg_fail("integer interactions need integer coordinates");
+    if (n < 0 || n >= (1LL << 31) - 4096) return arg_fail("n out of range (0 <= n < 2^31)");
+    if (nranges < 1 || !bounds) return arg_fail("need at least one row range");
+    for (int k = 0; k < nranges; ++k)
+        if (bounds[k] < 0 || bounds[k] > bounds[k + 1] || bounds[k + 1] > n) return arg_fail("bad row range bounds");
+    if (tiling == PC_TILE_AUTO) tiling = schedule == PC_BALANCED ? PC_TILE_FLAT : PC_TILE_PER_ROW_TILE;
+    if (tiling == PC_TILE_FLAT && schedule != PC_BALANCED)
+        return arg_fail("PC_TILE_FLAT needs the balanced schedule (equal windows per row tile)");
+    if (tiling != PC_TILE_FLAT && tiling != PC_TILE_PER_ROW_TILE) return arg_fail("unknown tiling");
+    const WsLayout lay = ws_layout(n);
+    if (!workspace || wsb < lay.total) return arg_fail("workspace too small (see pc_pairs_workspace_bytes)");
+    char* ws = (char*)workspace;
+    float4* pts = (float4*)(ws + lay.pts);
+    PrepStats* st = (PrepStats*)(ws + lay.stats);
+    Slot* slots = (Slot*)(ws + lay.slots);
+    const bool direct = interaction == PC_COLLISION_INVSQ;
+
+    // bbox init: minima to the largest ordered code, maxima to the smallest
+    CK(cudaMemsetAsync(st, 0xff, offsetof(PrepStats, mx), s));
+    CK(cudaMemsetAsync((char*)st + offsetof(PrepStats, mx), 0, sizeof(PrepStats) - offsetof(PrepStats, mx), s));
+    if (n > 0) {
+        const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)num_sms() * 8);
+        prep_bbox_kernel<<<blocks, 256, 0, s>>>(xyz, dtype, n, st);
+        CK_LAUNCH("prep_bbox_kernel");
+        if (direct) prep_stage_kernel<true><<<blocks, 256, 0, s>>>(xyz, dtype, n, st, pts);
+        else prep_stage_kernel<false><<<blocks, 256, 0, s>>>(xyz, dtype, n, st, pts);
+        CK_LAUNCH("prep_stage_kernel");
+    }
+    PairsArgs args{};
+    args.pts = pts;
+    args.xyz = xyz;
+    args.st = st;
+    args.slots = slots;
+    args.dtype = dtype;
+    args.pred = interaction == PC_COINCIDE ? kPredCoincide : interaction == PC_MANHATTAN1 ? kPredManhattan1 : kPredSphere;
+    args.thr = interaction == PC_COINCIDE ? 0.5f : interaction == PC_MANHATTAN1 ? 1.5f : 1.0f;
+    args.sched = schedule;
+    args.n = (int)n;
+    const long long cap = max_slots(n);
+    for (int k = 0; k < nranges; ++k) {
+        const long long lo = bounds[k], hi = bounds[k + 1];
+        int nslots = 0;
+        if (hi > lo && n >= 2) {
+            args.lo = (int)lo;
+            args.hi = (int)hi;
+            const bool flat = tiling == PC_TILE_FLAT;
+            int rc = n < kSmallN ? dispatch_cfg<kSmall.nt, kSmall.r, kSmall.w>(args, direct, flat, cap, &nslots, s)
+                                 : dispatch_cfg<kBig.nt, kBig.r, kBig.w>(args, direct, flat, cap, &nslots, s);
+            if (rc) return rc;
+        }
+        finalize_kernel<<<1, 256, 0, s>>>(slots, nslots, st, row_pairs(n, lo, hi, schedule), direct ? 1 : 0, dres + k);
+        CK_LAUNCH("finalize_kernel");
+    }
+    return PC_OK;
+}
+
+// ------------------------------------------------------------------------
+// library-owned per-device scratch for the *_host entry points
+// ------------------------------------------------------------------------
+struct Arena {
+    std::mutex mu;
+    void* dev = nullptr;
+    size_t cap = 0;
+    cudaStream_t stream = nullptr;
+};
+Arena g_arena[64];
+
+int arena_get(size_t bytes, Arena** out) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    Arena& ar = g_arena[dev & 63];
+    if (!ar.stream) CK(cudaStreamCreateWithFlags(&ar.stream, cudaStreamNonBlocking));
+    if (ar.cap < bytes) {
+        if (ar.dev) CK(cudaFree(ar.dev));
+        ar.dev = nullptr;
+        ar.cap = 0;
+        size_t want = align_up(bytes + bytes / 8, 1 << 20);
+        CK(cudaMalloc(&ar.dev, want));
+        ar.cap = want;
+    }
+    *out = &ar;
+    return PC_OK;
+}
+
+size_t dtype_bytes(int dtype) { return dtype == PC_F32 || dtype == PC_I32 ? 4 : 8; }
+
+// ------------------------------------------------------------------------
+// counting array (Alg. 1 / Alg. 2)
+// ------------------------------------------------------------------------
+struct LatSlot {
+    unsigned long long a, b;
+};
+constexpr unsigned long long kNoBad = ~0ull;
+
+template <typename KT>
+__global__ void lat_keys_kernel(const void* __restrict__ xyz, int dtype, long long n, long long a, long long side,
+                                KT* __restrict__ keys, unsigned long long* __restrict__ bad) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long x = coord_i64(xyz, dtype, i, 0), y = coord_i64(xyz, dtype, i, 1),
+                        z = coord_i64(xyz, dtype, i, 2);
+        if (x < -a || x > a || y < -a || y > a || z < -a || z > a) {  // _validate, lattice_counter.py:98-105
+            atomicMin(bad, (unsigned long long)i);
+        } else if (keys) {
+            keys[i] = (KT)(((x + a + 1) * side + (y + a + 1)) * side + (z + a + 1));  // _flatten, :107-111
+        }
+    }
+}
+
+// Alg. 1 on a clean grid: collisions += space[b]; space[b]++  
+template <typename KT>
+__global__ void lat_place_clean_kernel(const KT* __restrict__ keys, long long n, unsigned* __restrict__ grid,
+                                       const unsigned long long* __restrict__ bad, LatSlot* __restrict__ slots,
+                                       int* __restrict__ overflow) {
+    __shared__ unsigned long long s_a[8], s_b[8];
+    unsigned long long cnt = 0, first = 0;
+    int ovf = 0;
+    if (*bad == kNoBad) {
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+             i += (long long)gridDim.x * blockDim.x) {
+            const unsigned old = atomicAdd(grid + keys[i], 1u);
+            cnt += old;
+            first += old == 0u;
+            ovf |= old >= 0xfffffffeu;
+        }
+    }
+    cnt = warp_sum(cnt);
+    first = warp_sum(first);
+    if (__any_sync(0xffffffffu, ovf) && (threadIdx.x & 31) == 0) atomicOr(overflow, 1);
+    if ((threadIdx.x & 31) == 0) { s_a[threadIdx.x >> 5] = cnt; s_b[threadIdx.x >> 5] = first; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        LatSlot sl{0, 0};
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { sl.a += s_a[q]; sl.b += s_b[q]; }
+        slots[blockIdx.x] = sl;
+    }
+}
+
+template <typename KT>
+__global__ void lat_place_kernel(const KT* __restrict__ keys, long long n, unsigned* __restrict__ grid,
+                                 const unsigned long long* __restrict__ bad) {
+    if (*bad != kNoBad) return;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        atomicAdd(grid + keys[i], 1u);
+}
+
+// sum over beads of (final occupancy - 1) (lattice_counter.py:151-153); b = overflow flag
+template <typename KT>
+__global__ void lat_gather_kernel(const KT* __restrict__ keys, long long n, const unsigned* __restrict__ grid,
+                                  const unsigned long long* __restrict__ bad, LatSlot* __restrict__ slots,
+                                  int* __restrict__ overflow) {
+    __shared__ unsigned long long s_a[8];
+    unsigned long long acc = 0;
+    int ovf = 0;
+    if (*bad == kNoBad) {
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+             i += (long long)gridDim.x * blockDim.x) {
+            const unsigned occ = grid[keys[i]];
+            acc += (unsigned long long)occ - 1ull;
+            ovf |= occ >= 0xffffffffu;
+        }
+    }
+    acc = warp_sum(acc);
+    if (__any_sync(0xffffffffu, ovf) && (threadIdx.x & 31) == 0) atomicOr(overflow, 1);
+    if ((threadIdx.x & 31) == 0) s_a[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        LatSlot sl{0, 0};
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) sl.a += s_a[q];
+        slots[blockIdx.x] = sl;
+    }
+}
+
+// Alg. 2 second loop: six axial neighbour occupancies per bead
+template <typename KT>
+__global__ void lat_neighbours_kernel(const KT* __restrict__ keys, long long n, long long side,
+                                      const unsigned* __restrict__ grid, const unsigned long long* __restrict__ bad,
+                                      LatSlot* __restrict__ slots) {
+    __shared__ unsigned long long s_a[8];
+    unsigned long long acc = 0;
+    if (*bad == kNoBad) {
+        const long long d2 = side * side;
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+             i += (long long)gridDim.x * blockDim.x) {
+            const long long k = (long long)keys[i];
+            acc += (unsigned long long)grid[k + d2] + grid[k - d2] + grid[k + side] + grid[k - side] +
+                   grid[k + 1] + grid[k - 1];
+        }
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) s_a[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        LatSlot sl{0, 0};
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) sl.a += s_a[q];
+        slots[blockIdx.x] = sl;
+    }
+}
+
+// Distinct-cell count by marking bit 31 of every read cell (own cell, and the
+// six neighbours when `with_neighbours`), counting first markers; a second
+// call with unmark=1 clears the marks.  Occupancies never reach 2^31 here
+// (overflow is reported first).
+template <typename KT>
+__global__ void lat_mark_kernel(const KT* __restrict__ keys, long long n, long long side, int with_neighbours,
+                                int unmark, unsigned* __restrict__ grid, const unsigned long long* __restrict__ bad,
+                                LatSlot* __restrict__ slots) {
+    __shared__ unsigned long long s_a[8];
+    unsigned long long firsts = 0;
+    if (*bad == kNoBad) {
+        const long long d2 = side * side;
+        const long long offs[7] = {0, d2, -d2, side, -side, 1, -1};
+        const int m = with_neighbours ? 7 : 1;
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+             i += (long long)gridDim.x * blockDim.x) {
+            const long long k = (long long)keys[i];
+            for (int q = 0; q < m; ++q) {
+                if (unmark) atomicAnd(grid + k + offs[q], 0x7fffffffu);
+                else firsts += (atomicOr(grid + k + offs[q], 0x80000000u) & 0x80000000u) ? 0ull : 1ull;
+            }
+        }
+    }
+    firsts = warp_sum(firsts);
+    if ((threadIdx.x & 31) == 0) s_a[threadIdx.x >> 5] = firsts;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        LatSlot sl{0, 0};
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) sl.a += s_a[q];
+        slots[blockIdx.x] = sl;
+    }
+}
+
+template <typename KT>
+__global__ void lat_zero_keys_kernel(const KT* __restrict__ keys, long long n, unsigned* __restrict__ grid) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        grid[keys[i]] = 0u;
+}
+
+__global__ void lat_zero_beads_kernel(const void* __restrict__ xyz, int dtype, long long n, long long a, long long side,
+                                      unsigned* __restrict__ grid, const unsigned long long* __restrict__ bad) {
+    if (*bad != kNoBad) return;
+    const long long d2 = side * side;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long k = ((coord_i64(xyz, dtype, i, 0) + a + 1) * side + (coord_i64(xyz, dtype, i, 1) + a + 1)) * side +
+                            (coord_i64(xyz, dtype, i, 2) + a + 1);
+        grid[k] = 0u; grid[k + d2] = 0u; grid[k - d2] = 0u; grid[k + side] = 0u;
+        grid[k - side] = 0u; grid[k + 1] = 0u; grid[k - 1] = 0u;
+    }
+}
+
+__global__ void lat_sum_slots_kernel(const LatSlot* __restrict__ slots, int nslots, unsigned long long* __restrict__ out) {
+    __shared__ unsigned long long sa[256], sb[256];
+    unsigned long long x = 0, y = 0;
+    for (int q = threadIdx.x; q < nslots; q += blockDim.x) { x += slots[q].a; y += slots[q].b; }
+    sa[threadIdx.x] = x; sb[threadIdx.x] = y;
+    __syncthreads();
+    for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h) { sa[threadIdx.x] += sa[threadIdx.x + h]; sb[threadIdx.x] += sb[threadIdx.x + h]; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) { out[0] = sa[0]; out[1] = sb[0]; }
+}
+
+__global__ void count_nonzero_kernel(const uint4* __restrict__ grid4, long long n4, const unsigned* __restrict__ tail,
+                                     int ntail, unsigned long long* __restrict__ out) {
+    unsigned long long c = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+        const uint4 v = grid4[i];
+        c += (v.x != 0u) + (v.y != 0u) + (v.z != 0u) + (v.w != 0u);
+    }
+    if (blockIdx.x == 0 && (int)threadIdx.x < ntail) c += tail[threadIdx.x] != 0u;
+    c = warp_sum(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+// Scratch layout for one lattice call: [coords copy][bad u64][overflow int][slots][sums]
+struct LatScratch {
+    const void* xyz;
+    unsigned long long* bad;
+    int* overflow;
+    LatSlot* slots;
+    unsigned long long* sums;  // 8 pairs of (a, b)
+    int nslots;
+};
+
+int lattice_blocks(long long n) {
+    return (int)std::max(1LL, std::min<long long>((n + 255) / 256, (long long)num_sms() * 8));
+}
+
+int lat_prepare(const void* xyz, int dtype, int on_device, long long n, Arena** ar_out, LatScratch* sc,
+                cudaStream_t* s_inout) {
+    if (dtype != PC_I32 && dtype != PC_I64) return arg_fail("lattice beads must be int32 or int64");
+    const int nb = lattice_blocks(n);
+    const size_t cbytes = on_device ? 0 : align_up((size_t)n * 3 * dtype_bytes(dtype), 256);
+    const size_t need = cbytes + 256 + align_up((size_t)nb * sizeof(LatSlot), 256) + 256;
+    Arena* ar = nullptr;
+    int rc = arena_get(need, &ar);
+    if (rc) return rc;
+    char* base = (char*)ar->dev;
+    cudaStream_t s = *s_inout;
+    if (!on_device) {
+        if (n > 0) CK(cudaMemcpyAsync(base, xyz, (size_t)n * 3 * dtype_bytes(dtype), cudaMemcpyHostToDevice, s));
+        sc->xyz = base;
+    } else {
+        sc->xyz = xyz;
+    }
+    sc->bad = (unsigned long long*)(base + cbytes);
+    sc->overflow = (int*)(base + cbytes + 8);
+    sc->slots = (LatSlot*)(base + cbytes + 256);
+    sc->sums = (unsigned long long*)(base + cbytes + 256 + align_up((size_t)nb * sizeof(LatSlot), 256));
+    sc->nslots = nb;
+    CK(cudaMemsetAsync(sc->bad, 0xff, 8, s));
+    CK(cudaMemsetAsync(sc->overflow, 0, 4, s));
+    *ar_out = ar;
+    return PC_OK;
+}
+
+template <typename KT>
+int lattice_run(const void* xyz_in, int dtype, int on_device, long long n, long long a, unsigned* grid, void* keys_v,
+                int clean, int contacts, pc_lattice_result* res, cudaStream_t s) {
+    g_launches = 0;
+    memset(res, 0, sizeof *res);
+    res->beads_processed = n;
+    if (n == 0) return PC_OK;
+    if (!grid || !keys_v) return arg_fail("grid and keys buffers are required");
+    KT* keys = (KT*)keys_v;
+    const long long side = 2 * a + 3;
+    Arena* ar = nullptr;
+    LatScratch sc;
+    std::unique_lock<std::mutex> lock;
+    {
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        lock = std::unique_lock<std::mutex>(g_arena[dev & 63].mu);
+    }
+    int rc = lat_prepare(xyz_in, dtype, on_device, n, &ar, &sc, &s);
+    if (rc) return rc;
+    const int nb = sc.nslots;
+    lat_keys_kernel<KT><<<nb, 256, 0, s>>>(sc.xyz, dtype, n, a, side, keys, sc.bad);
+    CK_LAUNCH("lat_keys_kernel");
+    if (clean && !contacts) {
+        lat_place_clean_kernel<KT><<<nb, 256, 0, s>>>(keys, n, grid, sc.bad, sc.slots, sc.overflow);
+        CK_LAUNCH("lat_place_clean_kernel");
+        lat_sum_slots_kernel<<<1, 256, 0, s>>>(sc.slots, nb, sc.sums);
+        CK_LAUNCH("lat_sum_slots_kernel");
+    } else {
+        lat_place_kernel<KT><<<nb, 256, 0, s>>>(keys, n, grid, sc.bad);
+        CK_LAUNCH("lat_place_kernel");
+        lat_gather_kernel<KT><<<nb, 256, 0, s>>>(keys, n, grid, sc.bad, sc.slots, sc.overflow);
+        CK_LAUNCH("lat_gather_kernel");
+        lat_sum_slots_kernel<<<1, 256, 0, s>>>(sc.slots, nb, sc.sums);  // sums[0] = sum(occ - 1)
+        CK_LAUNCH("lat_sum_slots_kernel");
+        if (contacts) {
+            lat_neighbours_kernel<KT><<<nb, 256, 0, s>>>(keys, n, side, grid, sc.bad, sc.slots);
+            CK_LAUNCH("lat_neighbours_kernel");
+            lat_sum_slots_kernel<<<1, 256, 0, s>>>(sc.slots, nb, sc.sums + 2);  // sums[2] = doubled
+            CK_LAUNCH("lat_sum_slots_kernel");
+        }
+        lat_mark_kernel<KT><<<nb, 256, 0, s>>>(keys, n, side, contacts, 0, grid, sc.bad, sc.slots);
+        CK_LAUNCH("lat_mark_kernel");
+        lat_sum_slots_kernel<<<1, 256, 0, s>>>(sc.slots, nb, sc.sums + 4);  // sums[4] = distinct cells
+        CK_LAUNCH("lat_sum_slots_kernel");
+        lat_mark_kernel<KT><<<nb, 256, 0, s>>>(keys, n, side, contacts, 1, grid, sc.bad, sc.slots);
+        CK_LAUNCH("lat_mark_kernel");
+    }
+    unsigned long long host[8] = {0};
+    unsigned long long bad = 0;
+    int ovf = 0;
+    CK(cudaMemcpyAsync(host, sc.sums, sizeof host, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&bad, sc.bad, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&ovf, sc.overflow, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (bad != kNoBad) {
+        res->error = PC_ERR_RANGE;
+        res->detail = (long long)bad;
+        return PC_ERR_RANGE;
+    }
+    if (ovf) {
+        res->error = PC_ERR_OVERFLOW;
+        return PC_ERR_OVERFLOW;
+    }
+    if (clean && !contacts) {
+        res->count = (long long)host[0];
+        res->cells_touched = (long long)host[1];
+    } else if (!contacts) {
+        res->count = (long long)(host[0] / 2);
+        res->cells_touched = (long long)host[4];
+    } else {
+        res->doubled = (long long)host[2];
+        res->count = res->doubled / 2;
+        res->cells_touched = (long long)host[4];
+        if (res->doubled & 1) {
+            res->error = PC_ERR_ODD;
+            return PC_ERR_ODD;
+        }
+    }
+    return PC_OK;
+}
+
+// ------------------------------------------------------------------------
+// micro-benchmarks for the roofline denominator
+// ------------------------------------------------------------------------
+__global__ void mb_ffma_kernel(float* out, int iters, float b, float c) {
+    float v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = threadIdx.x * 1e-3f + k;
+    const float bb = b * (1.0f + threadIdx.x * 1e-9f);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = fmaf(v[k], c, bb);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s += v[k];
+    if (s == 1234.5f) out[0] = s;
+}
+
+__global__ void mb_pairs_kernel(float* out, int iters, float4 c0, float4 c1) {
+    constexpr int R = 8;
+    float rx[R], ry[R], rz[R], m[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) { rx[r] = threadIdx.x * 1e-3f + r; ry[r] = rx[r] * 0.5f; rz[r] = rx[r] * 0.25f; m[r] = -1e30f; }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            float t0 = fmaf(rx[r], c0.x, c0.w), t1 = fmaf(rx[r], c1.x, c1.w);
+            t0 = fmaf(ry[r], c0.y, t0); t1 = fmaf(ry[r], c1.y, t1);
+            t0 = fmaf(rz[r], c0.z, t0); t1 = fmaf(rz[r], c1.z, t1);
+            m[r] = max3f(m[r], t0, t1);
+        }
+        c0.w += 1e-7f;
+        c1.w -= 1e-7f;
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r) s += m[r];
+    if (s == 1234.5f) out[0] = s;
+}
+
+}  // namespace
+
+// ==========================================================================
+// C ABI
+// ==========================================================================
+extern "C" {
+
+const char* pc_last_error(void) { return g_err.c_str(); }
+const char* pc_version(void) { return "paircount-b200 0.1 (sm_100a)"; }
+
+int pc_device_count(int32_t* count) {
+    int c = 0;
+    CK(cudaGetDeviceCount(&c));
+    *count = c;
+    return PC_OK;
+}
+int pc_set_device(int32_t device) {
+    CK(cudaSetDevice(device));
+    return PC_OK;
+}
+int pc_device_alloc(size_t bytes, void** ptr) {
+    *ptr = nullptr;
+    if (bytes == 0) bytes = 256;
+    CK(cudaMalloc(ptr, bytes));
+    CK(cudaMemset(*ptr, 0, bytes));
+    return PC_OK;
+}
+int pc_device_free(void* ptr) {
+    CK(cudaFree(ptr));
+    return PC_OK;
+}
+int pc_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    return PC_OK;
+}
+int pc_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream) {
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    return PC_OK;
+}
+int pc_stream_sync(void* stream) {
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    return PC_OK;
+}
+
+size_t pc_pairs_workspace_bytes(int64_t n, int32_t nranges) {
+    (void)nranges;
+    return ws_layout(n < 0 ? 0 : n).total;
+}
+
+int pc_pairs_async(const void* xyz, int32_t dtype, int64_t n, int32_t interaction, int32_t schedule, int32_t tiling,
+                   int32_t nranges, const int64_t* bounds, void* workspace, size_t workspace_bytes,
+                   pc_pairs_result* results_device, void* stream) {
+    return run_pairs(xyz, dtype, n, interaction, schedule, tiling, nranges, (const long long*)bounds, workspace,
+                     workspace_bytes, results_device, (cudaStream_t)stream);
+}
+
+int pc_pairs(const void* xyz, int32_t dtype, int64_t n, int32_t interaction, int32_t schedule, int32_t tiling,
+             int32_t nranges, const int64_t* bounds, void* workspace, size_t workspace_bytes,
+             pc_pairs_result* results, void* stream) {
+    if (nranges < 1) return arg_fail("need at least one row range");
+    // results live at the tail of the workspace's slot area: use a separate small allocation instead
+    pc_pairs_result* dres = nullptr;
+    CK(cudaMallocAsync((void**)&dres, sizeof(pc_pairs_result) * nranges, (cudaStream_t)stream));
+    int rc = run_pairs(xyz, dtype, n, interaction, schedule, tiling, nranges, (const long long*)bounds, workspace,
+                       workspace_bytes, dres, (cudaStream_t)stream);
+    if (rc == PC_OK) {
+        CK(cudaMemcpyAsync(results, dres, sizeof(pc_pairs_result) * nranges, cudaMemcpyDeviceToHost,
+                           (cudaStream_t)stream));
+    }
+    CK(cudaFreeAsync(dres, (cudaStream_t)stream));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    return rc;
+}
+
+int pc_pairs_host(const void* xyz_host, int32_t dtype, int64_t n, int32_t interaction, int32_t schedule,
+                  int32_t tiling, int32_t nranges, const int64_t* bounds, pc_pairs_result* results) {
+    if (dtype < PC_F32 || dtype > PC_I64) return arg_fail("unknown dtype");
+    if (n < 0) return arg_fail("negative n");
+    if (nranges < 1) return arg_fail("need at least one row range");
+    const size_t in_bytes = align_up((size_t)n * 3 * dtype_bytes(dtype), 256);
+    const size_t ws_bytes = ws_layout(n).total;
+    const size_t res_bytes = align_up(sizeof(pc_pairs_result) * nranges, 256);
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_arena[dev & 63].mu);
+    Arena* ar = nullptr;
+    int rc = arena_get(in_bytes + ws_bytes + res_bytes, &ar);
+    if (rc) return rc;
+    char* base = (char*)ar->dev;
+    cudaStream_t s = ar->stream;
+    if (n > 0) CK(cudaMemcpyAsync(base, xyz_host, (size_t)n * 3 * dtype_bytes(dtype), cudaMemcpyHostToDevice, s));
+    pc_pairs_result* dres = (pc_pairs_result*)(base + in_bytes + ws_bytes);
+    rc = run_pairs(base, dtype, n, interaction, schedule, tiling, nranges, (const long long*)bounds,
+                   base + in_bytes, ws_bytes, dres, s);
+    const int launches = g_launches;
+    if (rc == PC_OK)
+        CK(cudaMemcpyAsync(results, dres, sizeof(pc_pairs_result) * nranges, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    g_launches = launches;
+    return rc;
+}
+
+int32_t pc_last_launch_count(void) { return g_launches; }
+
+int pc_kernel_timing(int32_t enable) {
+    g_timing = enable != 0;
+    g_ev_used = 0;
+    return PC_OK;
+}
+
+int pc_kernel_timing_read(double* total_ms, int32_t* launches) {
+    double t = 0.0;
+    for (int k = 0; k < g_ev_used; ++k) {
+        CK(cudaEventSynchronize(g_ev[k].b));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, g_ev[k].a, g_ev[k].b));
+        t += ms;
+    }
+    *total_ms = t;
+    *launches = g_ev_used;
+    g_ev_used = 0;
+    return PC_OK;
+}
+
+int64_t pc_lattice_grid_cells(int64_t half_extent) {
+    const int64_t side = 2 * half_extent + 3;
+    return side * side * side;
+}
+int32_t pc_lattice_key_bytes(int64_t half_extent) {
+    return pc_lattice_grid_cells(half_extent) < (1LL << 32) ? 4 : 8;
+}
+
+int pc_lattice_collisions(const void* xyz, int32_t dtype, int32_t xyz_on_device, int64_t n, int64_t half_extent,
+                          uint32_t* grid, void* keys, int32_t assume_clean, pc_lattice_result* result,
+                          void* stream) {
+    if (half_extent < 0) return arg_fail("half_extent must be >= 0");
+    return pc_lattice_key_bytes(half_extent) == 4
+               ? lattice_run<unsigned>(xyz, dtype, xyz_on_device, n, half_extent, grid, keys, assume_clean, 0, result,
+                                       (cudaStream_t)stream)
+               : lattice_run<unsigned long long>(xyz, dtype, xyz_on_device, n, half_extent, grid, keys, assume_clean,
+                                                 0, result, (cudaStream_t)stream);
+}
+
+int pc_lattice_contacts(const void* xyz, int32_t dtype, int32_t xyz_on_device, int64_t n, int64_t half_extent,
+                        uint32_t* grid, void* keys, int32_t assume_clean, pc_lattice_result* result, void* stream) {
+    if (half_extent < 0) return arg_fail("half_extent must be >= 0");
+    return pc_lattice_key_bytes(half_extent) == 4
+               ? lattice_run<unsigned>(xyz, dtype, xyz_on_device, n, half_extent, grid, keys, assume_clean, 1, result,
+                                       (cudaStream_t)stream)
+               : lattice_run<unsigned long long>(xyz, dtype, xyz_on_device, n, half_extent, grid, keys, assume_clean,
+                                                 1, result, (cudaStream_t)stream);
+}
+
+int pc_lattice_reset_keys(uint32_t* grid, int64_t half_extent, const void* keys, int64_t nkeys, void* stream) {
+    g_launches = 0;
+    if (nkeys <= 0) return PC_OK;
+    const int nb = lattice_blocks(nkeys);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (pc_lattice_key_bytes(half_extent) == 4) lat_zero_keys_kernel<unsigned><<<nb, 256, 0, s>>>((const unsigned*)keys, nkeys, grid);
+    else lat_zero_keys_kernel<unsigned long long><<<nb, 256, 0, s>>>((const unsigned long long*)keys, nkeys, grid);
+    CK_LAUNCH("lat_zero_keys_kernel");
+    return PC_OK;
+}
+
+int pc_lattice_reset_beads(const void* xyz, int32_t dtype, int32_t xyz_on_device, int64_t n, int64_t half_extent,
+                           uint32_t* grid, pc_lattice_result* result, void* stream) {
+    g_launches = 0;
+    memset(result, 0, sizeof *result);
+    if (n <= 0) return PC_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_arena[dev & 63].mu);
+    Arena* ar = nullptr;
+    LatScratch sc;
+    int rc = lat_prepare(xyz, dtype, xyz_on_device, n, &ar, &sc, &s);
+    if (rc) return rc;
+    const long long side = 2 * half_extent + 3;
+    lat_keys_kernel<unsigned><<<sc.nslots, 256, 0, s>>>(sc.xyz, dtype, n, half_extent, side, nullptr, sc.bad);
+    CK_LAUNCH("lat_keys_kernel");
+    lat_zero_beads_kernel<<<sc.nslots, 256, 0, s>>>(sc.xyz, dtype, n, half_extent, side, grid, sc.bad);
+    CK_LAUNCH("lat_zero_beads_kernel");
+    unsigned long long bad = 0;
+    CK(cudaMemcpyAsync(&bad, sc.bad, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (bad != kNoBad) {
+        result->error = PC_ERR_RANGE;
+        result->detail = (long long)bad;
+        return PC_ERR_RANGE;
+    }
+    return PC_OK;
+}
+
+int pc_grid_count_nonzero(const uint32_t* grid, int64_t cells, int64_t* nonzero, void* stream) {
+    g_launches = 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long* d = nullptr;
+    CK(cudaMallocAsync((void**)&d, 8, s));
+    CK(cudaMemsetAsync(d, 0, 8, s));
+    const long long n4 = cells / 4;
+    const int ntail = (int)(cells - n4 * 4);
+    const int nb = (int)std::max(1LL, std::min<long long>((n4 + 255) / 256, (long long)num_sms() * 8));
+    count_nonzero_kernel<<<nb, 256, 0, s>>>((const uint4*)grid, n4, grid + n4 * 4, ntail, d);
+    CK_LAUNCH("count_nonzero_kernel");
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaFreeAsync(d, s));
+    CK(cudaStreamSynchronize(s));
+    *nonzero = (int64_t)h;
+    return PC_OK;
+}
+
+int pc_microbench(int32_t kind, double* per_second, double* seconds) {
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    float* out = nullptr;
+    CK(cudaMalloc(&out, 64));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    const int blocks = num_sms() * 8, threads = 256;
+    const int iters = kind == 0 ? 65536 : 8192;
+    double work;
+    for (int rep = 0; rep < 2; ++rep) {  // first pass warms clocks up
+        CK(cudaEventRecord(e0, s));
+        if (kind == 0) mb_ffma_kernel<<<blocks, threads, 0, s>>>(out, iters, 0.5f, 0.999f);
+        else mb_pairs_kernel<<<blocks, threads, 0, s>>>(out, iters, make_float4(0.1f, 0.2f, 0.3f, -1e6f),
+                                                        make_float4(0.3f, 0.2f, 0.1f, -1e6f));
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(e1, s));
+        CK(cudaEventSynchronize(e1));
+    }
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    work = (double)blocks * threads * iters * (kind == 0 ? 16.0 : 16.0);  // kind 0: lane-FFMA; kind 1: pairs
+    *seconds = ms * 1e-3;
+    *per_second = work / (ms * 1e-3);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    cudaStreamDestroy(s);
+    return PC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,93 @@
+"""N>1 host path on CPU: world_size-2 gloo process group, slab split and the
+single int64 all-reduce of partials.  The per-slab compute is injected (the
+pinned C oracle), so this runs without a GPU; the GPU path differs only in
+the compute callback."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1901_11204_b200 import distributed as D
+from paper_1901_11204_b200.pair_schedule import row_pairs
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _oracle_compute(obj, f, lo, hi, schedule):
+    from oracle import c_oracle
+
+    c, s, _ = c_oracle.rows(obj, lo, hi, schedule)
+    return c if f == "count" else s
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1901_11204_b200 import generators as gen
+
+        objs = gen.random_spheres(3001, 14.0, 7).astype(np.float32)
+        out = {}
+        for sched in ("balanced", "standard"):
+            out[sched] = (D.spi_distributed(objs, "count", sched, compute=_oracle_compute),
+                          D.spi_distributed(objs, "sum", sched, compute=_oracle_compute))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_matches_single_process():
+    from oracle import c_oracle
+    from paper_1901_11204_b200 import generators as gen
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    objs = gen.random_spheres(3001, 14.0, 7).astype(np.float32)
+    n = len(objs)
+    for sched in ("balanced", "standard"):
+        want_c, want_s, _ = c_oracle.rows(objs, 0, n, sched)
+        for rank in range(world):
+            (tc, pc_, pairs), (ts, ps_, _) = results[rank][sched]
+            assert tc == want_c
+            assert ts == pytest.approx(want_s, rel=1e-12)
+            assert sum(pairs) == n * (n - 1) // 2
+            # every rank sees every partial, bit-identical
+            assert (pc_, ps_) == (results[0][sched][0][1], results[0][sched][1][1])
+
+
+def test_slabs_cover_and_balance():
+    for n in (1, 2, 7, 1000, 2**20):
+        for world in (1, 2, 4, 8):
+            for sched in ("balanced", "standard"):
+                slabs = D.row_slabs(n, world, sched)
+                assert slabs[0][0] == 0 and slabs[-1][1] == n
+                assert all(a[1] == b[0] for a, b in zip(slabs, slabs[1:]))
+                if n >= 1000:
+                    work = [row_pairs(n, a, b, sched) for a, b in slabs]
+                    assert max(work) <= 1.01 * min(work) + n
+
+
+def test_pack_roundtrip():
+    s = D.pack_partial(12345, 0.1 + 0.2, 1, 3)
+    counts, sums = D.unpack_partials(s, 3)
+    assert counts == [0, 12345, 0] and sums[1] == 0.1 + 0.2 and sums[0] == 0.0

@@ -1,0 +1,295 @@
+"""GPU parity: the drop-in API (ctypes -> libpaircount.so on the B200) against
+the reference's outputs (golden fixtures) and the pinned CPU oracle.
+
+Bars (BASELINE.json north_star): integer counts bit-exact; the float
+inverse-square sum within REL_TOL = 1e-5 relative of the float64 reference.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_1901_11204_b200 as pc
+from paper_1901_11204_b200 import _lib
+from paper_1901_11204_b200 import generators as gen
+from paper_1901_11204_b200 import lattice_counter as lc
+from paper_1901_11204_b200 import spi_engine as se
+from oracle import c_oracle
+from tests.helpers import config_input, digest, lattice_input, spi_input
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-5  # fp32 interaction sum vs float64 reference (north_star)
+
+
+def _f(name):
+    return se.collision_indicator if name == "collision" else se.inverse_square
+
+
+def _close(got, want):
+    return got == pytest.approx(want, rel=REL_TOL, abs=1e-9)
+
+
+# ------------------------------------------------------------------ SPI --
+
+def test_spi_golden_cases(golden_small):
+    for case in golden_small["spi_cases"]:
+        objs = spi_input(case)
+        assert digest(objs) == case["input_sha256"], case["tag"]
+        f = _f(case["f"])
+        for name, fn in (("standard", se.spi_standard), ("balanced", se.spi_balanced)):
+            if name not in case:
+                continue
+            r = fn(objs, f)
+            want = case[name]
+            assert r.pairs_evaluated == want["pairs"] and r.depth_per_worker == want["depth"], case["tag"]
+            if case["f"] == "collision":
+                assert r.total == want["total"] and isinstance(r.total, int), (case["tag"], name)
+            else:
+                assert isinstance(r.total, float) and _close(r.total, want["total"]), (case["tag"], name)
+        for entry in case["parallel"]:
+            r = se.spi_parallel(objs, f, entry["workers"], entry["schedule"])
+            assert list(r.worker_pairs) == entry["worker_pairs"], case["tag"]
+            assert r.depth_per_worker == entry["depth"]
+            if case["f"] == "collision":
+                assert list(r.partials) == entry["partials"], (case["tag"], entry["workers"], entry["schedule"])
+                assert r.total == entry["total"]
+            else:
+                for got, want in zip(r.partials, entry["partials"]):
+                    assert _close(got, want), (case["tag"], entry)
+
+
+def test_reference_unit_cases():
+    # test_spi_engine.py:32-49 with GPU-supported interactions
+    assert se.spi_standard([se.Sphere(0.0, 0.0, 0.0)] * 3, se.collision_indicator).total == 3
+    assert se.spi_balanced([se.Sphere(0.0, 0.0, 0.0)] * 3, se.collision_indicator).total == 3
+    spheres = gen.random_spheres(100, 4.0, 3)
+    for sched, seq in (("standard", se.spi_standard), ("balanced", se.spi_balanced)):
+        assert se.spi_parallel(spheres, se.collision_indicator, 1, sched).total == seq(spheres, se.collision_indicator).total
+    runs = {se.spi_parallel(gen.random_spheres(200, 3.0, 9), se.collision_indicator, 4, "balanced").total for _ in range(3)}
+    assert len(runs) == 1
+    # (n, 1) / (n, 2) objects are padded with zero coordinates
+    line = np.array([0.0, 0.5, 2.0, 2.9, 10.0])[:, None]
+    assert se.spi_standard(line, se.collision_indicator).total == 2
+    ints = np.array([[0, 0, 0], [0, 0, 0], [1, 0, 0]], dtype=np.int64)
+    assert se.spi_balanced(ints, se.collision_indicator).total == 1
+
+
+def test_near_boundary_exactness():
+    # pairs at d^2 = 1 +- ulp far from the origin, where fp32 Gram arithmetic is coarsest
+    rng = np.random.default_rng(5)
+    for base in (0.0, 100.0, 1000.0, 1.0e5):
+        a = base + rng.random((500, 3)) * 50
+        d = rng.normal(size=(500, 3))
+        d /= np.linalg.norm(d, axis=1, keepdims=True)
+        b = a + d * np.where(rng.random((500, 1)) < 0.5, np.nextafter(1.0, 0.0), np.nextafter(1.0, 2.0))
+        pts = np.empty((1000, 3))
+        pts[0::2], pts[1::2] = a, b
+        for arr in (pts, pts.astype(np.float32)):
+            want, _, _ = c_oracle.rows(arr, 0, len(arr), "balanced")
+            assert se.spi_balanced(arr, se.collision_indicator).total == want
+            assert se.spi_standard(arr, se.collision_indicator).total == want
+
+
+@pytest.mark.parametrize("n", [2, 3, 63, 64, 65, 127, 129, 1023, 1024, 1025, 4095, 16383, 16384, 16385, 20001])
+def test_sizes_vs_c_oracle(n):
+    # tile-boundary sizes on both kernel configurations (small < 16384 <= big)
+    box = max(2.0, (n / 2.0) ** (1 / 3) * 1.6)
+    objs = gen.random_spheres(n, box, n).astype(np.float32)
+    for sched in ("standard", "balanced"):
+        for workers in (1, 3):
+            blocks = se._partition(n, workers)
+            r = se.spi_parallel(objs, se.collision_indicator, workers, sched)
+            for b, got in zip(blocks, r.partials):
+                c, _, _ = c_oracle.rows(objs, b.start, b.stop, sched)
+                assert got == c, (n, sched, workers)
+        r = se.spi_parallel(objs, se.inverse_square, 2, sched)
+        for b, got in zip(se._partition(n, 2), r.partials):
+            _, s, _ = c_oracle.rows(objs, b.start, b.stop, sched)
+            assert _close(got, s), (n, sched)
+
+
+def test_dense_every_pair_in_contact():
+    objs = gen.random_spheres(3000, 0.5, 1)
+    assert se.spi_balanced(objs, se.collision_indicator).total == 3000 * 2999 // 2
+    assert se.spi_standard(objs.astype(np.float32), se.collision_indicator).total == 3000 * 2999 // 2
+
+
+def test_tilings_agree():
+    objs = gen.random_spheres(40_000, 30.0, 4).astype(np.float32)
+    n = len(objs)
+    want, s_want, _ = c_oracle.rows(objs, 0, n, "balanced")
+    for tiling in (_lib.PC_TILE_FLAT, _lib.PC_TILE_PER_ROW_TILE):
+        (r,) = _lib.pairs_host(objs, _lib.PC_COLLISION, _lib.PC_BALANCED, [0, n], tiling)
+        assert r.count == want
+        (r,) = _lib.pairs_host(objs, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, n], tiling)
+        assert r.count == want and _close(r.sum, s_want)
+    with pytest.raises(ValueError):
+        _lib.pairs_host(objs, _lib.PC_COLLISION, _lib.PC_STANDARD, [0, n], _lib.PC_TILE_FLAT)
+
+
+# --------------------------------------------------------- BASELINE configs --
+
+def test_config1_integer_coincidence(golden_configs):
+    for name, key in (("cfg1_cloud", "cloud"), ("cfg1_chain", "chain")):
+        beads = config_input(golden_configs, name)
+        g = golden_configs["cfg1"][key]
+        assert pc.oracle_collisions(beads) == g["oracle_collisions"]
+        assert pc.oracle_contacts(beads) == g["oracle_contacts"]
+
+
+def test_config2_naive_and_balanced(golden_configs):
+    objs = config_input(golden_configs, "cfg2")
+    g = golden_configs["cfg2"]
+    for name, fn in (("standard", se.spi_standard), ("balanced", se.spi_balanced)):
+        r = fn(objs, se.collision_indicator)
+        assert (r.total, r.pairs_evaluated, r.depth_per_worker) == (g[name]["total"], g[name]["pairs"], g[name]["depth"])
+    for smp in g["samples"]:
+        cnt, pairs = se.spi_rows(objs, se.collision_indicator, tuple(smp["rows"]), smp["schedule"])
+        assert (cnt, pairs) == (smp["count"], smp["pairs"])
+        s, _ = se.spi_rows(objs, se.inverse_square, tuple(smp["rows"]), smp["schedule"])
+        assert _close(s, smp["inv_sum"])
+
+
+@pytest.mark.parametrize("name", ["cfg3", "cfg4u", "cfg4c"])
+def test_large_config_row_samples(golden_configs, name):
+    objs = config_input(golden_configs, name)
+    assert digest(objs) == golden_configs[name]["sha256"]
+    for smp in golden_configs[name]["samples"]:
+        rows = tuple(smp["rows"])
+        cnt, pairs = se.spi_rows(objs, se.collision_indicator, rows, smp["schedule"])
+        assert (cnt, pairs) == (smp["count"], smp["pairs"]), smp
+        s, _ = se.spi_rows(objs, se.inverse_square, rows, smp["schedule"])
+        assert _close(s, smp["inv_sum"]), smp
+
+
+def test_config3_full_size_properties(golden_configs):
+    """N = 2^20: beyond the CPU oracle; pinned by size-independent properties:
+    standard == balanced, 1 range == sum of 8 ranges, count(INVSQ kernel) ==
+    count(Gram kernel), determinism."""
+    objs = config_input(golden_configs, "cfg3")
+    n = len(objs)
+    b = se.spi_balanced(objs, se.collision_indicator).total
+    s = se.spi_standard(objs, se.collision_indicator).total
+    assert b == s
+    par = se.spi_parallel(objs, se.collision_indicator, 8, "balanced")
+    assert par.total == b and sum(par.partials) == b
+    (r,) = _lib.pairs_host(objs, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, n])
+    assert r.count == b
+    (r2,) = _lib.pairs_host(objs, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, n])
+    assert r2.sum == r.sum  # bitwise deterministic
+    (rs,) = _lib.pairs_host(objs, _lib.PC_COLLISION_INVSQ, _lib.PC_STANDARD, [0, n])
+    assert rs.count == b and _close(rs.sum, r.sum)
+
+
+def test_config5_counting_array(golden_configs):
+    pts = config_input(golden_configs, "cfg5")
+    g = golden_configs["cfg5"]
+    sp = pc.new_space(512)
+    rep = pc.count_collisions(pts, sp)
+    assert (rep.count, rep.beads_processed, rep.cells_touched) == (g["count"], g["beads_processed"], g["cells_touched"])
+    pc.reset_sparse(sp)
+    assert sp.is_zero()
+    # counting array == all-pairs count on a slice (north_star: "checked against the all-pairs count")
+    part = pts[:200_000]
+    rep = pc.count_collisions(part, sp)
+    assert rep.count == pc.oracle_collisions(part)
+
+
+# ------------------------------------------------------------- lattice --
+
+def test_lattice_golden(golden_small):
+    for case in golden_small["lattice_cases"]:
+        beads = lattice_input(case)
+        assert pc.oracle_collisions(beads) == case["oracle_collisions"], case["tag"]
+        assert pc.oracle_contacts(beads) == case["oracle_contacts"], case["tag"]
+        if "count_collisions" not in case:
+            continue
+        sp = pc.new_space(case["half_extent"])
+        col = pc.count_collisions(beads, sp)
+        assert [col.count, col.beads_processed, col.cells_touched] == case["count_collisions"], case["tag"]
+        pc.reset_sparse(sp, beads)
+        assert sp.is_zero()
+        con = pc.count_contacts(beads, sp)
+        assert [con.count, con.beads_processed, con.cells_touched] == case["count_contacts"], case["tag"]
+        pc.reset_sparse(sp, beads)
+        assert lc.contact_accumulator(beads, pc.new_space(case["half_extent"])) == case["contact_accumulator"]
+
+
+def test_lattice_reference_unit_cases():
+    # test_lattice_counter.py:23-76,144-182
+    assert pc.new_space(0).interior_cells == 1 and pc.new_space(0).cells.size == 27
+    sp = pc.new_space(1)
+    assert pc.count_collisions([(0, 0, 0)] * 5, sp).count == 10
+    assert sum(len(t) for t in sp.touched) <= 5
+    pc.reset_sparse(sp)
+    assert sp.is_zero() and not sp.touched
+    with pytest.raises(lc.CoordinateRangeError, match="bead 1"):
+        pc.count_collisions([(0, 0, 0), (3, 0, 0)], pc.new_space(2))
+    sp = pc.new_space(2)
+    pc.count_collisions([(1, 1, 0), (0, 0, 0)], sp)
+    sp.touched.clear()
+    pc.reset_sparse(sp, [(1, 1, 0), (0, 0, 0)])
+    assert sp.is_zero()
+    sp = pc.new_space(1)
+    pc.count_contacts([(1, 1, 1), (-1, -1, -1), (1, -1, 0)], sp)
+    cells = sp.cells
+    assert cells.sum() == cells[1:-1, 1:-1, 1:-1].sum()
+
+
+def test_lattice_dirty_space_semantics():
+    # counting into a populated space evaluates the reference's formulas exactly
+    rng = np.random.default_rng(0)
+    first = rng.integers(-3, 4, size=(300, 3))
+    second = rng.integers(-3, 4, size=(200, 3))
+    import importlib
+    npo = importlib.import_module("oracle.numpy_port")
+    sp = pc.new_space(4)
+    pc.count_collisions(first, sp)
+    rep = pc.count_collisions(second, sp)  # no reset in between
+    both = np.concatenate([first, second])
+    # reference: occ = final occupancy of each second-vector bead's cell
+    side = 11
+    flat = lambda b: ((b[:, 0] + 5) * side + (b[:, 1] + 5)) * side + (b[:, 2] + 5)
+    occ = np.bincount(flat(both), minlength=side**3)[flat(second)]
+    assert rep.count == int((occ - 1).sum()) // 2
+    assert rep.cells_touched == len(np.unique(flat(second)))
+    pc.reset_sparse(sp)
+    assert sp.is_zero()
+    assert pc.count_collisions(second, sp).count == npo.count_collisions(second, 4)[0]
+
+
+def test_sparse_reset_soundness_random():
+    rng = np.random.default_rng(1)
+    reused = pc.new_space(8)
+    for _ in range(30):
+        first = rng.integers(-8, 9, size=(rng.integers(0, 65), 3))
+        second = rng.integers(-8, 9, size=(rng.integers(0, 65), 3))
+        pc.count_contacts(first, reused)
+        pc.reset_sparse(reused, first)
+        fresh = pc.new_space(8)
+        assert pc.count_contacts(second, reused).count == pc.count_contacts(second, fresh).count
+        pc.reset_sparse(reused, second)
+        assert pc.count_collisions(second, reused).count == pc.oracle_collisions(second)
+        pc.reset_sparse(reused, second)
+
+
+def test_chains_vs_oracle():
+    # acceptance criterion 1/2 (test_acceptance.py:49-84), 40 chains per size
+    for n in (1, 2, 3, 16, 64, 257, 1024):
+        for v in range(40):
+            beads, ext = gen.random_chain(n, 1000 * n + v)
+            sp = pc.new_space(max(ext, 1))
+            col = pc.count_collisions(beads, sp)
+            pc.reset_sparse(sp, beads)
+            doubled = lc.contact_accumulator(beads, sp)
+            pc.reset_sparse(sp, beads)
+            want_col, want_con = c_oracle.int_pairs(beads)
+            assert col.count == want_col == pc.oracle_collisions(beads)
+            assert doubled % 2 == 0 and doubled // 2 == want_con == pc.oracle_contacts(beads)
+
+
+def test_smoke_entry():
+    import __graft_entry__
+    __graft_entry__.smoke()
