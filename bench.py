@@ -47,7 +47,8 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-secondary", action="store_true", help="skip the config-2/5 side measurements")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-rows-per-core", type=int, default=12)
+    p.add_argument("--cpu-rows-per-core", type=int, default=160)
+    p.add_argument("--ref-rows-per-core", type=int, default=32, help="reference arm: rows per core per step")
     return p.parse_args()
 
 
@@ -130,7 +131,7 @@ def run_reference(args):
     obj = workload_input()
     n = len(obj)
     cores = os.cpu_count() or 1
-    per_step = cores * max(1, args.cpu_rows_per_core // 2)
+    per_step = cores * max(1, args.ref_rows_per_core)
     times, pairs = [], []
     for step in range(args.warmup + args.steps):
         rows = cb.sample_rows(n, per_step, 1, offset=step * 7919)

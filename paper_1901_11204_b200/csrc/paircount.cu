@@ -317,217 +317,7 @@ __device__ __forceinline__ int steps_for_dev(int n, int i) {
     return i < (n >> 1) ? (n >> 1) : (n >> 1) - 1;
 }
 
-template <int NT, int R, int W, bool DIRECT, bool FLAT>
-__global__ void __launch_bounds__(NT, 4) pairs_kernel(const PairsArgs a) {
-    constexpr int T = NT * R;
-    static_assert(W % NT == 0 && W % 2 == 0, "chunk must be a multiple of the CTA");
-    __shared__ __align__(16) float4 s_pts[2][W];
-    __shared__ int s_j[2][W];
-    __shared__ unsigned long long s_red[NT / 32][2];
-    __shared__ double s_sum[NT / 32];
-
-    const int tid = threadIdx.x;
-    const int n = a.n;
-    const bool bal = a.sched == PC_BALANCED;
-
-    // error bands: computed by every CTA from the prep stats
-    const double M = dec_f64_or0(a.st->mnorm);
-    const double X = dec_f64_or0(a.st->maxabs);
-    const bool force = !DIRECT && !(M < 1e30);  // fp32 filter unusable: exact path for every pair
-    const float half_tb = (float)(0.5 * ((double)a.thr + 3.814697265625e-06 * (M + 4.0)));
-    const double bd = 1.52587890625e-05 + (a.dtype == PC_F32 ? 0.0 : 9.5367431640625e-07 * X);
-    const float thr2 = (float)(1.0 + (double)a.thr + bd);
-    const int steps_min = (n & 1) ? (n - 1) >> 1 : (n >> 1) - 1;
-
-    // this CTA's column range
-    long long g, g_end;
-    if (FLAT) {
-        g = a.total * (long long)blockIdx.x / gridDim.x;
-        g_end = a.total * (long long)(blockIdx.x + 1) / gridDim.x;
-    } else {
-        const int i0 = a.lo + (int)blockIdx.x * T;
-        g = 0;
-        g_end = bal ? (long long)(T - 1 + (n >> 1)) : (long long)(n - 1 - i0);
-    }
-    auto tile_of = [&](long long gg) -> int { return FLAT ? (int)(gg / a.L) : (int)blockIdx.x; };
-    auto off_of = [&](long long gg) -> int { return FLAT ? (int)(gg % a.L) : (int)gg; };
-    auto width_of = [&](long long gg) -> int {
-        long long rem_tile = FLAT ? a.L - gg % a.L : g_end - gg;
-        long long w = rem_tile < (long long)W ? rem_tile : (long long)W;
-        return (int)(w < g_end - gg ? w : g_end - gg);
-    };
-
-    auto stage = [&](int buf, long long gg) {
-        const int t = tile_of(gg), off = off_of(gg), wc = width_of(gg);
-        const int i0 = a.lo + t * T;
-#pragma unroll
-        for (int q = 0; q < W / NT; ++q) {
-            const int k = q * NT + tid;
-            if (k < wc) {
-                long long j = (long long)i0 + off + 1 + k;  // s' = off + 1 + k
-                if (bal) {
-                    if (j >= n) j -= n;
-                    if (j >= n) j %= n;
-                }
-                cp_async16(&s_pts[buf][k], &a.pts[j]);
-                s_j[buf][k] = (int)j;
-            } else {
-                s_pts[buf][k] = DIRECT ? make_float4(0.f, 0.f, 0.f, 0.f)
-                                       : make_float4(0.f, 0.f, 0.f, -INFINITY);
-                s_j[buf][k] = -1;
-            }
-        }
-        cp_async_commit();
-    };
-
-    float rx[R], ry[R], rz[R], rc[R];
-    int rlim[R];
-    int cur_tile = -1;
-    unsigned valid_rows = 0;
-    unsigned long long cnt = 0, checks = 0;
-    double sum = 0.0;
-
-    if (g < g_end) stage(0, g);
-    int buf = 0;
-    while (g < g_end) {
-        const long long g_next = g + width_of(g);
-        if (g_next < g_end) {
-            stage(buf ^ 1, g_next);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
-
-        const int t = tile_of(g), off = off_of(g), wc = width_of(g);
-        const int i0 = a.lo + t * T;
-        if (t != cur_tile) {
-            cur_tile = t;
-            valid_rows = 0;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int i = i0 + r * NT + tid;
-                const bool ok = i < a.hi;
-                const float4 v = ok ? a.pts[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-                rx[r] = v.x; ry[r] = v.y; rz[r] = v.z;
-                rc[r] = ok ? (force ? -INFINITY : -v.w - half_tb) : INFINITY;
-                rlim[r] = ok ? (bal ? steps_for_dev(n, i) : n - 1 - i) : 0;
-                valid_rows |= (ok ? 1u : 0u) << r;
-            }
-        }
-        const float4* sp = s_pts[buf];
-        const int* sj = s_j[buf];
-        unsigned fl = 0;
-
-        if (!DIRECT) {
-            // ---- fast path: 3 FFMA per pair + FMNMX3 per two pairs ----
-            float m[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) m[r] = -INFINITY;
-#pragma unroll 4
-            for (int k = 0; k < W; k += 2) {
-                const float4 c0 = sp[k], c1 = sp[k + 1];
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    float t0 = fmaf(rx[r], c0.x, c0.w);
-                    float t1 = fmaf(rx[r], c1.x, c1.w);
-                    t0 = fmaf(ry[r], c0.y, t0);
-                    t1 = fmaf(ry[r], c1.y, t1);
-                    t0 = fmaf(rz[r], c0.z, t0);
-                    t1 = fmaf(rz[r], c1.z, t1);
-                    m[r] = max3f(m[r], t0, t1);
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < R; ++r) fl |= (m[r] > rc[r] ? 1u : 0u) << r;
-            if (force) fl = valid_rows;
-        } else {
-            const bool dense = wc == W && i0 + T <= a.hi && off + 1 >= T && (!bal || off + W <= steps_min);
-            float m[R], acc[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) { m[r] = INFINITY; acc[r] = 0.f; }
-            if (dense) {
-                // ---- direct formula: p = 1 + |dr|^2; two pairs share one reciprocal ----
-#pragma unroll 2
-                for (int k = 0; k < W; k += 2) {
-                    const float4 c0 = sp[k], c1 = sp[k + 1];
-#pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        const float dx0 = rx[r] - c0.x, dy0 = ry[r] - c0.y, dz0 = rz[r] - c0.z;
-                        const float dx1 = rx[r] - c1.x, dy1 = ry[r] - c1.y, dz1 = rz[r] - c1.z;
-                        const float p0 = fmaf(dz0, dz0, fmaf(dy0, dy0, fmaf(dx0, dx0, 1.0f)));
-                        const float p1 = fmaf(dz1, dz1, fmaf(dy1, dy1, fmaf(dx1, dx1, 1.0f)));
-                        m[r] = min3f(m[r], p0, p1);
-                        acc[r] = fmaf(p0 + p1, rcp_approx(p0 * p1), acc[r]);
-                    }
-                }
-            } else {
-                // ---- edge chunk: per-pair ownership mask ----
-                for (int k = 0; k < W; ++k) {
-                    const float4 c0 = sp[k];
-                    const int j = sj[k];
-#pragma unroll
-                    for (int r = 0; r < R; ++r) {
-                        const int rl = r * NT + tid;
-                        const bool ok = j >= 0 && (unsigned)(off + k - rl) < (unsigned)rlim[r];
-                        const float dx = rx[r] - c0.x, dy = ry[r] - c0.y, dz = rz[r] - c0.z;
-                        const float p = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1.0f)));
-                        acc[r] += ok ? rcp_approx(p) : 0.0f;
-                        m[r] = ok ? fminf(m[r], p) : m[r];
-                    }
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                sum += (double)acc[r];
-                fl |= (m[r] < thr2 ? 1u : 0u) << r;
-            }
-        }
-
-        // ---- slow path: re-scan flagged rows, exact reference predicate ----
-        if (__any_sync(0xffffffffu, fl != 0)) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                if (fl & (1u << r)) {
-                    const int rl = r * NT + tid;
-                    for (int k = 0; k < wc; ++k) {
-                        const float4 c0 = sp[k];
-                        bool cand;
-                        if (DIRECT) {
-                            const float dx = rx[r] - c0.x, dy = ry[r] - c0.y, dz = rz[r] - c0.z;
-                            cand = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1.0f))) < thr2;
-                        } else {
-                            float tt = fmaf(rx[r], c0.x, c0.w);
-                            tt = fmaf(ry[r], c0.y, tt);
-                            tt = fmaf(rz[r], c0.z, tt);
-                            cand = force || tt > rc[r];
-                        }
-                        if (cand && (unsigned)(off + k - rl) < (unsigned)rlim[r]) {
-                            ++checks;
-                            cnt += exact_pair(a.xyz, a.dtype, a.pred, i0 + rl, sj[k]) ? 1ull : 0ull;
-                        }
-                    }
-                }
-            }
-        }
-        __syncthreads();  // buffer `buf` may be restaged next iteration
-        g = g_next;
-        buf ^= 1;
-    }
-
-    // ---- CTA reduction: one slot per CTA ----
-    cnt = warp_sum(cnt);
-    checks = warp_sum(checks);
-    sum = warp_sum(sum);
-    const int w = tid >> 5;
-    if ((tid & 31) == 0) { s_red[w][0] = cnt; s_red[w][1] = checks; s_sum[w] = sum; }
-    __syncthreads();
-    if (tid == 0) {
-        Slot s{0ull, 0ull, 0.0, 0ull};
-        for (int q = 0; q < NT / 32; ++q) { s.count += s_red[q][0]; s.checks += s_red[q][1]; s.sum += s_sum[q]; }
-        a.slots[blockIdx.x] = s;
-    }
-}
+#include "pairs_kernel.cuh"
 
 // Fixed-order sum of the CTA slots into one result record.
 __global__ void finalize_kernel(const Slot* __restrict__ slots, int nslots, const PrepStats* __restrict__ st,
@@ -564,15 +354,15 @@ __global__ void finalize_kernel(const Slot* __restrict__ slots, int nslots, cons
 // host side of the all-pairs path
 // ------------------------------------------------------------------------
 struct KernelCfg {
-    int nt, r, w;
+    int warps, r, w;
 };
-constexpr KernelCfg kBig{128, 8, 256};
-constexpr KernelCfg kSmall{64, 2, 64};
+constexpr KernelCfg kBig{4, 8, 256};   // warp tile 256 rows
+constexpr KernelCfg kSmall{4, 2, 64};  // warp tile 64 rows, for n < kSmallN
 constexpr int kSmallN = 16384;
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-long long max_slots(long long n) { return 148LL * 64 + n / (kSmall.nt * kSmall.r) + 64; }
+long long max_slots(long long n) { return 148LL * 64 + n / (32 * kSmall.r * kSmall.warps) + 64; }
 
 struct WsLayout {
     size_t pts, stats, slots, total;
@@ -608,10 +398,9 @@ int num_sms() {
     return g_num_sms[dev];
 }
 
-template <int NT, int R, int W, bool DIRECT, bool FLAT>
+template <int WARPS, int R, int W, bool DIRECT, bool FLAT>
 int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStream_t s) {
-    constexpr int T = NT * R;
-    auto kern = pairs_kernel<NT, R, W, DIRECT, FLAT>;
+    auto kern = pairs_kernel<WARPS, R, W, DIRECT, FLAT>;
     int grid;
     if (FLAT) {
         static thread_local int occ_cache[64] = {0};
@@ -619,17 +408,16 @@ int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStr
         cudaGetDevice(&dev);
         if (!occ_cache[dev & 63]) {
             int occ = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, 0));
             occ_cache[dev & 63] = occ > 0 ? occ : 1;
         }
-        long long want = (long long)num_sms() * occ_cache[dev & 63];
-        long long chunks = (args.total + W - 1) / W;
-        grid = (int)std::max(1LL, std::min(want, chunks));
+        const long long want = (long long)num_sms() * occ_cache[dev & 63];
+        const long long chunks = (args.total + W - 1) / W;
+        grid = (int)std::max(1LL, std::min(want, (chunks + WARPS - 1) / WARPS));
     } else {
-        grid = args.n_tiles;
+        grid = (args.n_tiles + WARPS - 1) / WARPS;
     }
     if (grid > n_slots_cap) return arg_fail("workspace too small for the CTA slots");
-    (void)T;
     EvPair* ev = nullptr;
     if (g_timing && g_ev_used < 4096) {
         if (g_ev_used == g_ev_made) {
@@ -640,25 +428,25 @@ int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStr
         ev = &g_ev[g_ev_used++];
         CK(cudaEventRecord(ev->a, s));
     }
-    kern<<<grid, NT, 0, s>>>(args);
+    kern<<<grid, WARPS * 32, 0, s>>>(args);
     CK_LAUNCH("pairs_kernel");
     if (ev) CK(cudaEventRecord(ev->b, s));
     *nslots_out = grid;
     return PC_OK;
 }
 
-template <int NT, int R, int W>
+template <int WARPS, int R, int W>
 int dispatch_cfg(PairsArgs args, bool direct, bool flat, long long cap, int* nslots, cudaStream_t s) {
-    constexpr int T = NT * R;
+    constexpr int T = 32 * R;
     args.n_tiles = (args.hi - args.lo + T - 1) / T;
     if (flat) {
         args.L = (long long)(T - 1) + (args.n >> 1);
         args.total = (long long)args.n_tiles * args.L;
-        return direct ? launch_pairs<NT, R, W, true, true>(args, cap, nslots, s)
-                      : launch_pairs<NT, R, W, false, true>(args, cap, nslots, s);
+        return direct ? launch_pairs<WARPS, R, W, true, true>(args, cap, nslots, s)
+                      : launch_pairs<WARPS, R, W, false, true>(args, cap, nslots, s);
     }
-    return direct ? launch_pairs<NT, R, W, true, false>(args, cap, nslots, s)
-                  : launch_pairs<NT, R, W, false, false>(args, cap, nslots, s);
+    return direct ? launch_pairs<WARPS, R, W, true, false>(args, cap, nslots, s)
+                  : launch_pairs<WARPS, R, W, false, false>(args, cap, nslots, s);
 }
 
 int run_pairs(const void* xyz, int dtype, long long n, int interaction, int schedule, int tiling,
@@ -670,7 +458,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     if (interaction < PC_COLLISION || interaction > PC_MANHATTAN1) return arg_fail("unknown interaction");
     if ((interaction == PC_COINCIDE || interaction == PC_MANHATTAN1) && dtype < PC_I32)
         return arg_fail("integer interactions need integer coordinates");
-    if (n < 0 || n >= (1LL << 31) - 4096) return arg_fail("n out of range (0 <= n < 2^31)");
+    if (n < 0 || n >= (1LL << 30)) return arg_fail("n out of range (0 <= n < 2^30)");
     if (nranges < 1 || !bounds) return arg_fail("need at least one row range");
     for (int k = 0; k < nranges; ++k)
         if (bounds[k] < 0 || bounds[k] > bounds[k + 1] || bounds[k + 1] > n) return arg_fail("bad row range bounds");
@@ -715,8 +503,8 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
             args.lo = (int)lo;
             args.hi = (int)hi;
             const bool flat = tiling == PC_TILE_FLAT;
-            int rc = n < kSmallN ? dispatch_cfg<kSmall.nt, kSmall.r, kSmall.w>(args, direct, flat, cap, &nslots, s)
-                                 : dispatch_cfg<kBig.nt, kBig.r, kBig.w>(args, direct, flat, cap, &nslots, s);
+            int rc = n < kSmallN ? dispatch_cfg<kSmall.warps, kSmall.r, kSmall.w>(args, direct, flat, cap, &nslots, s)
+                                 : dispatch_cfg<kBig.warps, kBig.r, kBig.w>(args, direct, flat, cap, &nslots, s);
             if (rc) return rc;
         }
         finalize_kernel<<<1, 256, 0, s>>>(slots, nslots, st, row_pairs(n, lo, hi, schedule), direct ? 1 : 0, dres + k);
