@@ -255,33 +255,48 @@ __device__ __forceinline__ void bbox_centre(const PrepStats& st, int dtype, doub
     }
 }
 
+// Staged value of point i: centred fp32 q and w = -|q|^2/2 (Gram), or the
+// raw fp32 coordinates (direct formula).
+template <bool DIRECT>
+__device__ __forceinline__ float4 staged_point(const void* xyz, int dtype, long long i, const double c[3],
+                                               const long long ci[3], double* nq_out) {
+    float q[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (DIRECT) {
+            q[k] = (float)coord_f64(xyz, dtype, i, k);  // raw coordinates: exact for fp32 input
+        } else if (is_int_dtype(dtype)) {
+            long long v = (long long)((unsigned long long)coord_i64(xyz, dtype, i, k) - (unsigned long long)ci[k]);
+            q[k] = (float)(double)v;
+        } else {
+            q[k] = (float)(coord_f64(xyz, dtype, i, k) - c[k]);
+        }
+    }
+    double nq = (double)q[0] * q[0] + (double)q[1] * q[1] + (double)q[2] * q[2];
+    if (!(nq <= 1e300)) nq = INFINITY;
+    *nq_out = nq;
+    return make_float4(q[0], q[1], q[2], DIRECT ? 0.0f : (float)(-0.5 * nq));
+}
+
+// Pair arrays for packed FP32: entry j>>1 of `even` (j even) / `odd` (j odd)
+// holds points j and (j+1) mod n interleaved as (x_j, x_j1, y_j, y_j1),
+// (z_j, z_j1, w_j, w_j1).  Thread per j; every point is staged twice.
 template <bool DIRECT>
 __global__ void prep_stage_kernel(const void* __restrict__ xyz, int dtype, long long n,
-                                  PrepStats* __restrict__ st, float4* __restrict__ pts) {
+                                  PrepStats* __restrict__ st, float4* __restrict__ even, float4* __restrict__ odd) {
     double c[3];
     long long ci[3];
     bbox_centre(*st, dtype, c, ci);
-    const bool isint = is_int_dtype(dtype);
     double mnorm = 0.0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
-        float q[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            if (DIRECT) {
-                q[k] = (float)coord_f64(xyz, dtype, i, k);  // raw coordinates: exact for fp32 input
-            } else if (isint) {
-                long long v = (long long)((unsigned long long)coord_i64(xyz, dtype, i, k) -
-                                          (unsigned long long)ci[k]);
-                q[k] = (float)(double)v;
-            } else {
-                q[k] = (float)(coord_f64(xyz, dtype, i, k) - c[k]);
-            }
-        }
-        double nq = (double)q[0] * q[0] + (double)q[1] * q[1] + (double)q[2] * q[2];
-        if (!(nq <= 1e300)) nq = INFINITY;
+        double nq, nq1;
+        const float4 p = staged_point<DIRECT>(xyz, dtype, i, c, ci, &nq);
+        const float4 p1 = staged_point<DIRECT>(xyz, dtype, i + 1 == n ? 0 : i + 1, c, ci, &nq1);
         mnorm = fmax(mnorm, nq);
-        pts[i] = make_float4(q[0], q[1], q[2], DIRECT ? 0.0f : (float)(-0.5 * nq));
+        float4* dst = ((i & 1) ? odd : even) + 2 * (i >> 1);
+        dst[0] = make_float4(p.x, p1.x, p.y, p1.y);
+        dst[1] = make_float4(p.z, p1.z, p.w, p1.w);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mnorm = fmax(mnorm, __shfl_xor_sync(0xffffffffu, mnorm, o));
@@ -299,7 +314,8 @@ struct Slot {
 };
 
 struct PairsArgs {
-    const float4* pts;
+    const float4* pts_even;  // pair arrays, see prep_stage_kernel
+    const float4* pts_odd;
     const void* xyz;
     const PrepStats* st;
     Slot* slots;
@@ -369,8 +385,9 @@ struct WsLayout {
 };
 WsLayout ws_layout(long long n) {
     WsLayout l;
-    l.pts = 0;
-    l.stats = align_up((size_t)n * sizeof(float4), 256);
+    const size_t pair_bytes = align_up((size_t)(n / 2 + 1) * 2 * sizeof(float4), 256);
+    l.pts = 0;  // even pairs, then odd pairs
+    l.stats = 2 * pair_bytes;
     l.slots = l.stats + 256;
     l.total = align_up(l.slots + (size_t)max_slots(n) * sizeof(Slot), 256);
     return l;
@@ -469,7 +486,8 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     const WsLayout lay = ws_layout(n);
     if (!workspace || wsb < lay.total) return arg_fail("workspace too small (see pc_pairs_workspace_bytes)");
     char* ws = (char*)workspace;
-    float4* pts = (float4*)(ws + lay.pts);
+    float4* pts_even = (float4*)(ws + lay.pts);
+    float4* pts_odd = (float4*)(ws + lay.pts + lay.stats / 2);
     PrepStats* st = (PrepStats*)(ws + lay.stats);
     Slot* slots = (Slot*)(ws + lay.slots);
     const bool direct = interaction == PC_COLLISION_INVSQ;
@@ -481,12 +499,13 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
         const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)num_sms() * 8);
         prep_bbox_kernel<<<blocks, 256, 0, s>>>(xyz, dtype, n, st);
         CK_LAUNCH("prep_bbox_kernel");
-        if (direct) prep_stage_kernel<true><<<blocks, 256, 0, s>>>(xyz, dtype, n, st, pts);
-        else prep_stage_kernel<false><<<blocks, 256, 0, s>>>(xyz, dtype, n, st, pts);
+        if (direct) prep_stage_kernel<true><<<blocks, 256, 0, s>>>(xyz, dtype, n, st, pts_even, pts_odd);
+        else prep_stage_kernel<false><<<blocks, 256, 0, s>>>(xyz, dtype, n, st, pts_even, pts_odd);
         CK_LAUNCH("prep_stage_kernel");
     }
     PairsArgs args{};
-    args.pts = pts;
+    args.pts_even = pts_even;
+    args.pts_odd = pts_odd;
     args.xyz = xyz;
     args.st = st;
     args.slots = slots;

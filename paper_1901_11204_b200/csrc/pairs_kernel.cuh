@@ -1,24 +1,47 @@
 // The all-pairs kernel (included by paircount.cu inside its anonymous namespace).
 //
 // Unit of work: a WARP tile of T = 32*R outer rows (R rows per lane, row
-// rl = r*32 + lane, coalesced loads) held in registers, streaming partner
-// columns through a warp-private double-buffered shared-memory ring of W
-// points (cp.async, 16 B per point).  Warps never wait for each other: the
-// only CTA barrier is the final reduction.  (The first version staged
-// columns per CTA; ncu showed `barrier` as the top stall at 2.1 warps per
-// issue because any warp in the slow path held up the other three.)
+// rl = r*32 + lane) held in registers, streaming partner columns through a
+// warp-private double-buffered shared-memory ring of W columns.  Warps never
+// wait for each other; the only CTA barrier is the final reduction.  (A
+// first version staged columns per CTA; ncu showed `barrier` as the top
+// stall, 2.1 warps per issue, because one warp in the slow path held up the
+// other three.)
+//
+// Packed FP32: columns are staged as interleaved PAIRS (x_j, x_j+1, y_j,
+// y_j+1)(z_j, z_j+1, w_j, w_j+1), so one FFMA2/FADD2 (sm_100 f32x2) with the
+// row value broadcast evaluates two pairs.  The prep kernel writes the pair
+// arrays E (pairs starting at even j) and O (odd j), each pair holding point
+// j and point (j+1) mod n, so any window position is two 16-byte cp.async.
 //
 // Column space: a warp tile starting at row i0 walks offsets s' = 1..L
 // (partner j = i0 + s', mod n for the balanced schedule); row rl owns offset
 // s' iff 1 <= s' - rl <= lim(i0 + rl) (reference ownership, spi_engine.py:
-// 102-106).  FLAT: the tiles * L rectangle is split evenly over all warps of
-// a persistent grid.  PER_ROW_TILE: warp g of the grid walks tile g.
+// 102-106).  Dense chunks (every cell owned) run unmasked; the few edge
+// chunks of each tile mask per pair.  FLAT: the tiles * L rectangle is split
+// evenly over all warps of a persistent grid.  PER_ROW_TILE: warp g walks
+// tile g.
+
+__device__ __forceinline__ float2 f2_fma(float a, float2 b, float2 c) {  // a*b + c, a broadcast
+    return __ffma2_rn(make_float2(a, a), b, c);
+}
+__device__ __forceinline__ float2 f2_rsub(float a, float2 b) {  // a - b, a broadcast
+    unsigned long long bb = *reinterpret_cast<unsigned long long*>(&b), dd;
+    asm("{.reg .b64 t; mov.b64 t, {%1, %1}; sub.rn.f32x2 %0, t, %2;}" : "=l"(dd) : "f"(a), "l"(bb));
+    return *reinterpret_cast<float2*>(&dd);
+}
+
+// column k of an interleaved pair buffer: (x, y, z, w)
+__device__ __forceinline__ float4 col_of(const float4* sp, int k) {
+    const float4 A = sp[k & ~1], B = sp[k | 1];
+    return (k & 1) ? make_float4(A.y, A.w, B.y, B.w) : make_float4(A.x, A.z, B.x, B.z);
+}
 
 template <int WARPS, int R, int W, bool DIRECT, bool FLAT>
 __global__ void __launch_bounds__(WARPS * 32, 4) pairs_kernel(const PairsArgs a) {
     constexpr int T = 32 * R;
-    static_assert(W % 32 == 0 && W % 2 == 0, "chunk must be a multiple of the warp");
-    __shared__ __align__(16) float4 s_pts[WARPS][2][W];
+    static_assert(W % 64 == 0, "chunk must hold whole column pairs for every lane");
+    __shared__ __align__(16) float4 s_pts[WARPS][2][W];  // W columns = W/2 pairs = W float4
     __shared__ int s_j[WARPS][2][W];
     __shared__ unsigned long long s_red[WARPS][2];
     __shared__ double s_sum[WARPS];
@@ -37,52 +60,73 @@ __global__ void __launch_bounds__(WARPS * 32, 4) pairs_kernel(const PairsArgs a)
     const float half_tb = (float)(0.5 * ((double)a.thr + 3.814697265625e-06 * (M + 4.0)));
     const double bd = 1.52587890625e-05 + (a.dtype == PC_F32 ? 0.0 : 9.5367431640625e-07 * X);
     const float thr2 = (float)(1.0 + (double)a.thr + bd);
+    // a contact's term 1/p exceeds 1/thr2; chunk sums of positive terms keep that (fp32 slack 2^-16)
+    const float sum_flag = (float)((1.0 / (double)thr2) * (1.0 - 1.52587890625e-05));
     const int steps_min = (n & 1) ? (n - 1) >> 1 : (n >> 1) - 1;
 
-    // this warp's column range
-    long long g, g_end;
-    int fixed_tile = 0;
+    // this warp's walk: `left` columns starting at (tile, off); L = window length
+    int tile, off, L;
+    long long left;
     if (FLAT) {
-        g = a.total * gw / nw;
-        g_end = a.total * (gw + 1) / nw;
+        const long long g = a.total * gw / nw;
+        left = a.total * (gw + 1) / nw - g;
+        L = (int)a.L;
+        tile = (int)(g / L);  // the only 64-bit division, once per warp
+        off = (int)(g - (long long)tile * L);
     } else {
-        fixed_tile = (int)gw;
-        g = 0;
-        g_end = 0;
+        tile = (int)gw;
+        off = 0;
+        L = 0;
         if (gw < a.n_tiles) {
-            const int i0 = a.lo + fixed_tile * T;
-            g_end = bal ? (long long)(T - 1 + (n >> 1)) : (long long)(n - 1 - i0);
+            const int i0 = a.lo + tile * T;
+            L = bal ? T - 1 + (n >> 1) : n - 1 - i0;
         }
+        left = L;
     }
-    auto tile_of = [&](long long gg) -> int { return FLAT ? (int)(gg / a.L) : fixed_tile; };
-    auto off_of = [&](long long gg) -> int { return FLAT ? (int)(gg % a.L) : (int)gg; };
-    auto width_of = [&](long long gg) -> int {
-        const long long rem_tile = FLAT ? a.L - gg % a.L : g_end - gg;
-        const long long w = rem_tile < (long long)W ? rem_tile : (long long)W;
-        return (int)(w < g_end - gg ? w : g_end - gg);
+    auto width = [&](int o, long long lft) -> int {
+        const int w = min(W, L - o);
+        return (int)(w < lft ? w : lft);
+    };
+    auto wrap = [&](int j) -> int {
+        if (j >= n) j -= n;
+        if (j >= n) j %= n;
+        return j;
     };
 
     float4* sp0 = s_pts[wid][0];
     int* sj0 = s_j[wid][0];
-    auto stage = [&](int buf, long long gg) {
-        const int t = tile_of(gg), off = off_of(gg), wc = width_of(gg);
-        const int i0 = a.lo + t * T;
+    // a far column (0, 0, 0, fw): its Gram value is -inf, never a candidate
+    const float fw = DIRECT ? 0.f : -INFINITY;
+    auto stage = [&](int buf, int t, int o, int wc) {
+        const int j0 = a.lo + t * T + o + 1;  // column k sits at j0 + k (mod n when balanced)
         float4* sp = sp0 + buf * W;
         int* sj = sj0 + buf * W;
 #pragma unroll
-        for (int q = 0; q < W / 32; ++q) {
-            const int k = q * 32 + lane;
-            if (k < wc) {
-                int j = i0 + off + 1 + k;  // s' = off + 1 + k  (< 2^31: n < 2^31 - 4096)
-                if (bal) {
-                    if (j >= n) j -= n;
-                    if (j >= n) j %= n;
-                }
-                cp_async16(&sp[k], &a.pts[j]);
+        for (int q = 0; q < W / 64; ++q) {
+            const int p = q * 32 + lane;  // column pair p = columns 2p, 2p+1
+            const int k = 2 * p;
+            if (k + 1 < wc) {
+                int j = j0 + k;
+                if (bal) j = wrap(j);
+                const float4* src = (j & 1 ? a.pts_odd : a.pts_even) + 2 * (j >> 1);
+                cp_async16(&sp[k], src);
+                cp_async16(&sp[k + 1], src + 1);
                 sj[k] = j;
+                sj[k + 1] = (bal || j + 1 < n) ? (j + 1 == n ? 0 : j + 1) : -1;
+            } else if (k < wc) {  // last column of an odd-width chunk: second half is a far point
+                int j = j0 + k;
+                if (bal) j = wrap(j);
+                const float4* src = (j & 1 ? a.pts_odd : a.pts_even) + 2 * (j >> 1);
+                const float4 A = src[0], B = src[1];
+                sp[k] = make_float4(A.x, 0.f, A.z, 0.f);
+                sp[k + 1] = make_float4(B.x, 0.f, B.z, fw);
+                sj[k] = j;
+                sj[k + 1] = -1;
             } else {
-                sp[k] = DIRECT ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(0.f, 0.f, 0.f, -INFINITY);
+                sp[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                sp[k + 1] = make_float4(0.f, 0.f, fw, fw);
                 sj[k] = -1;
+                sj[k + 1] = -1;
             }
         }
         cp_async_commit();
@@ -94,28 +138,36 @@ __global__ void __launch_bounds__(WARPS * 32, 4) pairs_kernel(const PairsArgs a)
     unsigned long long cnt = 0, checks = 0;
     double sum = 0.0;
 
-    if (g < g_end) stage(0, g);
+    int wc = left > 0 ? width(off, left) : 0;
+    if (left > 0) stage(0, tile, off, wc);
     int buf = 0;
-    while (g < g_end) {
-        const long long g_next = g + width_of(g);
-        if (g_next < g_end) {
-            stage(buf ^ 1, g_next);
+    while (left > 0) {
+        // next chunk's coordinates (incremental: no divisions in the loop)
+        int ntile = tile, noff = off + wc;
+        if (noff == L) {
+            ++ntile;
+            noff = 0;
+        }
+        const long long nleft = left - wc;
+        const int nwc = nleft > 0 ? width(noff, nleft) : 0;
+        if (nleft > 0) {
+            stage(buf ^ 1, ntile, noff, nwc);
             cp_async_wait<1>();
         } else {
             cp_async_wait<0>();
         }
         __syncwarp();
 
-        const int t = tile_of(g), off = off_of(g), wc = width_of(g);
-        const int i0 = a.lo + t * T;
-        if (t != cur_tile) {
-            cur_tile = t;
+        const int i0 = a.lo + tile * T;
+        if (tile != cur_tile) {
+            cur_tile = tile;
             valid_rows = 0;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int i = i0 + r * 32 + lane;
                 const bool ok = i < a.hi;
-                const float4 v = ok ? a.pts[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float4 v = ok ? col_of((i & 1 ? a.pts_odd : a.pts_even) + 2 * (i >> 1), 0)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
                 rx[r] = v.x;
                 ry[r] = v.y;
                 rz[r] = v.z;
@@ -125,57 +177,76 @@ __global__ void __launch_bounds__(WARPS * 32, 4) pairs_kernel(const PairsArgs a)
         }
         const float4* sp = sp0 + buf * W;
         const int* sj = sj0 + buf * W;
+        // every cell of the chunk owned by its row?  (see header comment)
+        const bool dense = wc == W && i0 + T <= a.hi && off + 1 >= T && (!bal || off + W <= steps_min);
         unsigned fl = 0;
 
         if (!DIRECT) {
-            // ---- Gram filter: 3 FFMA per pair + FMNMX3 per two pairs ----
             float m[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) m[r] = -INFINITY;
+            if (off + 1 >= T) {
+                // ---- Gram filter, packed: 3 FFMA2 + 1 FMNMX3 per two pairs.  Unowned
+                // cells past a row's window only cost a rescan if they are contacts.
 #pragma unroll 4
-            for (int k = 0; k < W; k += 2) {
-                const float4 c0 = sp[k], c1 = sp[k + 1];
+                for (int k = 0; k < W; k += 2) {
+                    const float4 A = sp[k], B = sp[k + 1];
+                    const float2 cx = make_float2(A.x, A.y), cy = make_float2(A.z, A.w);
+                    const float2 cz = make_float2(B.x, B.y), cw = make_float2(B.z, B.w);
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    float t0 = fmaf(rx[r], c0.x, c0.w);
-                    float t1 = fmaf(rx[r], c1.x, c1.w);
-                    t0 = fmaf(ry[r], c0.y, t0);
-                    t1 = fmaf(ry[r], c1.y, t1);
-                    t0 = fmaf(rz[r], c0.z, t0);
-                    t1 = fmaf(rz[r], c1.z, t1);
-                    m[r] = max3f(m[r], t0, t1);
+                    for (int r = 0; r < R; ++r) {
+                        float2 t = f2_fma(rx[r], cx, cw);
+                        t = f2_fma(ry[r], cy, t);
+                        t = f2_fma(rz[r], cz, t);
+                        m[r] = max3f(m[r], t.x, t.y);
+                    }
+                }
+            } else {
+                // ---- leading chunk: mask cells at or before the row (incl. the self pair)
+                for (int k = 0; k < W; k += 2) {
+                    const float4 A = sp[k], B = sp[k + 1];
+                    const float2 cx = make_float2(A.x, A.y), cy = make_float2(A.z, A.w);
+                    const float2 cz = make_float2(B.x, B.y), cw = make_float2(B.z, B.w);
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const int d = off + k - (r * 32 + lane);  // s' - rl - 1 for column k
+                        float2 t = f2_fma(rz[r], cz, f2_fma(ry[r], cy, f2_fma(rx[r], cx, cw)));
+                        m[r] = max3f(m[r], d >= 0 ? t.x : -INFINITY, d + 1 >= 0 ? t.y : -INFINITY);
+                    }
                 }
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) fl |= (m[r] > rc[r] ? 1u : 0u) << r;
             if (force) fl = valid_rows;
         } else {
-            const bool dense = wc == W && i0 + T <= a.hi && off + 1 >= T && (!bal || off + W <= steps_min);
-            float m[R], acc[R];
+            float2 acc[R];
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                m[r] = INFINITY;
-                acc[r] = 0.f;
-            }
+            for (int r = 0; r < R; ++r) acc[r] = make_float2(0.f, 0.f);
             if (dense) {
-                // ---- direct formula, p = 1 + |dr|^2; two pairs share one reciprocal ----
+                // ---- direct formula, packed: p = 1 + |dr|^2 for two columns per FADD2/FFMA2;
+                // two column pairs share one FMUL2/FADD2/FFMA2 for 1/pa + 1/pc = (pa+pc)/(pa*pc)
+                const float2 one = make_float2(1.0f, 1.0f);
 #pragma unroll 2
-                for (int k = 0; k < W; k += 2) {
-                    const float4 c0 = sp[k], c1 = sp[k + 1];
+                for (int k = 0; k < W; k += 4) {
+                    const float4 A0 = sp[k], B0 = sp[k + 1], A1 = sp[k + 2], B1 = sp[k + 3];
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        const float dx0 = rx[r] - c0.x, dy0 = ry[r] - c0.y, dz0 = rz[r] - c0.z;
-                        const float dx1 = rx[r] - c1.x, dy1 = ry[r] - c1.y, dz1 = rz[r] - c1.z;
-                        const float p0 = fmaf(dz0, dz0, fmaf(dy0, dy0, fmaf(dx0, dx0, 1.0f)));
-                        const float p1 = fmaf(dz1, dz1, fmaf(dy1, dy1, fmaf(dx1, dx1, 1.0f)));
-                        m[r] = min3f(m[r], p0, p1);
-                        acc[r] = fmaf(p0 + p1, rcp_approx(p0 * p1), acc[r]);
+                        float2 dx = f2_rsub(rx[r], make_float2(A0.x, A0.y));
+                        float2 dy = f2_rsub(ry[r], make_float2(A0.z, A0.w));
+                        float2 dz = f2_rsub(rz[r], make_float2(B0.x, B0.y));
+                        const float2 p0 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __ffma2_rn(dx, dx, one)));
+                        dx = f2_rsub(rx[r], make_float2(A1.x, A1.y));
+                        dy = f2_rsub(ry[r], make_float2(A1.z, A1.w));
+                        dz = f2_rsub(rz[r], make_float2(B1.x, B1.y));
+                        const float2 p1 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __ffma2_rn(dx, dx, one)));
+                        const float2 pr = __fmul2_rn(p0, p1), sm = __fadd2_rn(p0, p1);
+                        acc[r] = __ffma2_rn(sm, make_float2(rcp_approx(pr.x), rcp_approx(pr.y)), acc[r]);
                     }
                 }
             } else {
                 // ---- edge chunk: per-pair ownership mask ----
                 for (int k = 0; k < W; ++k) {
-                    const float4 c0 = sp[k];
+                    const float4 c0 = col_of(sp, k);
                     const int j = sj[k];
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
@@ -185,19 +256,20 @@ __global__ void __launch_bounds__(WARPS * 32, 4) pairs_kernel(const PairsArgs a)
                         const bool ok = j >= 0 && (unsigned)(off + k - rl) < (unsigned)lim;
                         const float dx = rx[r] - c0.x, dy = ry[r] - c0.y, dz = rz[r] - c0.z;
                         const float p = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1.0f)));
-                        acc[r] += ok ? rcp_approx(p) : 0.0f;
-                        m[r] = ok ? fminf(m[r], p) : m[r];
+                        acc[r].x += ok ? rcp_approx(p) : 0.0f;
                     }
                 }
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                sum += (double)acc[r];
-                fl |= (m[r] < thr2 ? 1u : 0u) << r;
+                const float cs = acc[r].x + acc[r].y;
+                sum += (double)cs;
+                fl |= (cs > sum_flag ? 1u : 0u) << r;  // conservative: a contact's term alone exceeds it
             }
         }
 
-        // ---- slow path: re-scan flagged rows with the exact reference predicate ----
+        // ---- slow path: re-scan flagged rows 8 columns at a time (independent
+        // FMA chains), exact reference predicate on each owned candidate ----
         if (__any_sync(0xffffffffu, fl != 0)) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -205,28 +277,37 @@ __global__ void __launch_bounds__(WARPS * 32, 4) pairs_kernel(const PairsArgs a)
                     const int rl = r * 32 + lane;
                     const int i = i0 + rl;
                     const int lim = bal ? steps_for_dev(n, i) : n - 1 - i;  // flagged rows are valid rows
-                    for (int k = 0; k < wc; ++k) {
-                        const float4 c0 = sp[k];
-                        bool cand;
-                        if (DIRECT) {
-                            const float dx = rx[r] - c0.x, dy = ry[r] - c0.y, dz = rz[r] - c0.z;
-                            cand = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1.0f))) < thr2;
-                        } else {
-                            float tt = fmaf(rx[r], c0.x, c0.w);
-                            tt = fmaf(ry[r], c0.y, tt);
-                            tt = fmaf(rz[r], c0.z, tt);
-                            cand = force || tt > rc[r];
+                    for (int k0 = 0; k0 < wc; k0 += 8) {
+                        unsigned cm = 0;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const float4 c0 = col_of(sp, k0 + u);
+                            bool cand;
+                            if (DIRECT) {
+                                const float dx = rx[r] - c0.x, dy = ry[r] - c0.y, dz = rz[r] - c0.z;
+                                cand = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1.0f))) < thr2;
+                            } else {
+                                const float tt = fmaf(rz[r], c0.z, fmaf(ry[r], c0.y, fmaf(rx[r], c0.x, c0.w)));
+                                cand = force || tt > rc[r];
+                            }
+                            cm |= (cand && (unsigned)(off + k0 + u - rl) < (unsigned)lim && k0 + u < wc ? 1u : 0u)
+                                  << u;
                         }
-                        if (cand && (unsigned)(off + k - rl) < (unsigned)lim) {
+                        while (cm) {
+                            const int u = __ffs(cm) - 1;
+                            cm &= cm - 1;
                             ++checks;
-                            cnt += exact_pair(a.xyz, a.dtype, a.pred, i, sj[k]) ? 1ull : 0ull;
+                            cnt += exact_pair(a.xyz, a.dtype, a.pred, i, sj[k0 + u]) ? 1ull : 0ull;
                         }
                     }
                 }
             }
         }
         __syncwarp();  // the buffer just read is restaged next iteration
-        g = g_next;
+        tile = ntile;
+        off = noff;
+        left = nleft;
+        wc = nwc;
         buf ^= 1;
     }
 
