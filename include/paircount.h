@@ -165,6 +165,12 @@ int pc_lattice_contacts(const void* xyz, int32_t dtype, int32_t xyz_on_device, i
 /* reset_sparse via the touched list (lattice_counter.py:205-210) */
 int pc_lattice_reset_keys(uint32_t* grid, int64_t half_extent, const void* keys, int64_t nkeys,
                           void* stream);
+/* Zero the whole grid with one streaming write (cudaMemsetAsync).  The
+ * Python reset_sparse uses it in place of pc_lattice_reset_keys when the
+ * touched keys number more than 1/32 of the cells AND every other cell is
+ * known to be zero -- then both leave the identical all-zero grid, and the
+ * streaming write beats 32-byte-sector scattered stores. */
+int pc_lattice_clear(uint32_t* grid, int64_t half_extent, void* stream);
 /* reset_sparse via beads: each bead's cell and its six neighbours
  * (lattice_counter.py:211-217); PC_ERR_RANGE if a bead is outside [-a,a]^3 */
 int pc_lattice_reset_beads(const void* xyz, int32_t dtype, int32_t xyz_on_device, int64_t n,

@@ -185,6 +185,7 @@ struct PrepStats {
     unsigned long long mnorm;         // ordered f64: max |q|^2 of the staged fp32 coordinates
     int nonfinite;
     int pad;
+    unsigned long long work_ctr;
 };
 
 __device__ __forceinline__ bool is_int_dtype(int dtype) { return dtype >= PC_I32; }
@@ -319,12 +320,14 @@ struct PairsArgs {
     const void* xyz;
     const PrepStats* st;
     Slot* slots;
+    unsigned long long* work_ctr;  // FLAT: super-chunk claim counter (zeroed per launch)
     int dtype, pred, sched;
     float thr;
     int n, lo, hi;      // n < 2^31 enforced on the host
     int n_tiles;        // row tiles in [lo, hi)
     long long L;        // FLAT: window length shared by every row tile
     long long total;    // FLAT: n_tiles * L
+    long long super_cols;  // FLAT: columns per claimed super-chunk (multiple of W)
 };
 
 __device__ __forceinline__ int steps_for_dev(int n, int i) {
@@ -431,10 +434,14 @@ int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStr
         const long long want = (long long)num_sms() * occ_cache[dev & 63];
         const long long chunks = (args.total + W - 1) / W;
         grid = (int)std::max(1LL, std::min(want, (chunks + WARPS - 1) / WARPS));
+        // ~8 super-chunks per warp, each 1..16 chunks
+        const long long per = chunks / ((long long)grid * WARPS * 8);
+        args.super_cols = (long long)W * std::max(1LL, std::min(16LL, per));
     } else {
         grid = (args.n_tiles + WARPS - 1) / WARPS;
     }
     if (grid > n_slots_cap) return arg_fail("workspace too small for the CTA slots");
+    if (FLAT) CK(cudaMemsetAsync(args.work_ctr, 0, sizeof(unsigned long long), s));
     EvPair* ev = nullptr;
     if (g_timing && g_ev_used < 4096) {
         if (g_ev_used == g_ev_made) {
@@ -509,6 +516,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     args.xyz = xyz;
     args.st = st;
     args.slots = slots;
+    args.work_ctr = &st->work_ctr;
     args.dtype = dtype;
     args.pred = interaction == PC_COINCIDE ? kPredCoincide : interaction == PC_MANHATTAN1 ? kPredManhattan1 : kPredSphere;
     args.thr = interaction == PC_COINCIDE ? 0.5f : interaction == PC_MANHATTAN1 ? 1.5f : 1.0f;
@@ -1079,6 +1087,13 @@ int pc_lattice_reset_keys(uint32_t* grid, int64_t half_extent, const void* keys,
     if (pc_lattice_key_bytes(half_extent) == 4) lat_zero_keys_kernel<unsigned><<<nb, 256, 0, s>>>((const unsigned*)keys, nkeys, grid);
     else lat_zero_keys_kernel<unsigned long long><<<nb, 256, 0, s>>>((const unsigned long long*)keys, nkeys, grid);
     CK_LAUNCH("lat_zero_keys_kernel");
+    return PC_OK;
+}
+
+int pc_lattice_clear(uint32_t* grid, int64_t half_extent, void* stream) {
+    g_launches = 0;
+    if (half_extent < 0) return arg_fail("half_extent must be >= 0");
+    CK(cudaMemsetAsync(grid, 0, (size_t)pc_lattice_grid_cells(half_extent) * sizeof(uint32_t), (cudaStream_t)stream));
     return PC_OK;
 }
 

@@ -18,9 +18,11 @@
 // (partner j = i0 + s', mod n for the balanced schedule); row rl owns offset
 // s' iff 1 <= s' - rl <= lim(i0 + rl) (reference ownership, spi_engine.py:
 // 102-106).  Dense chunks (every cell owned) run unmasked; the few edge
-// chunks of each tile mask per pair.  FLAT: the tiles * L rectangle is split
-// evenly over all warps of a persistent grid.  PER_ROW_TILE: warp g walks
-// tile g.
+// chunks of each tile mask per pair.  FLAT: the tiles * L rectangle is one
+// uniform work space; the warps of a persistent grid (SMs x occupancy CTAs)
+// claim super-chunks (1..16 chunks, ~8 per warp) from an atomic counter (a
+// static split left a ~30% occupancy tail in ncu).  PER_ROW_TILE: warp g
+// walks tile g.
 
 __device__ __forceinline__ float2 f2_fma(float a, float2 b, float2 c) {  // a*b + c, a broadcast
     return __ffma2_rn(make_float2(a, a), b, c);
@@ -49,7 +51,6 @@ __global__ void __launch_bounds__(WARPS * 32, 4) pairs_kernel(const PairsArgs a)
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const long long gw = (long long)blockIdx.x * WARPS + wid;
-    const long long nw = (long long)gridDim.x * WARPS;
     const int n = a.n;
     const bool bal = a.sched == PC_BALANCED;
 
@@ -66,13 +67,28 @@ __global__ void __launch_bounds__(WARPS * 32, 4) pairs_kernel(const PairsArgs a)
 
     // this warp's walk: `left` columns starting at (tile, off); L = window length
     int tile, off, L;
-    long long left;
+    long long left = 0;
+    // FLAT: warps claim super-chunks of a.super_cols columns from a global counter, so
+    // SM-to-SM speed differences and slow-path rescans cannot leave a tail.
+    const long long SUPER = a.super_cols;
+    auto claim = [&](int& t, int& o, long long& lft) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(a.work_ctr, (unsigned long long)SUPER);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if ((long long)base >= a.total) {
+            lft = 0;
+            return;
+        }
+        const long long e = (long long)base + SUPER < a.total ? (long long)base + SUPER : a.total;
+        t = (int)((long long)base / L);
+        o = (int)((long long)base - (long long)t * L);
+        lft = e - (long long)base;
+    };
     if (FLAT) {
-        const long long g = a.total * gw / nw;
-        left = a.total * (gw + 1) / nw - g;
         L = (int)a.L;
-        tile = (int)(g / L);  // the only 64-bit division, once per warp
-        off = (int)(g - (long long)tile * L);
+        tile = 0;
+        off = 0;
+        claim(tile, off, left);
     } else {
         tile = (int)gw;
         off = 0;
@@ -148,7 +164,8 @@ __global__ void __launch_bounds__(WARPS * 32, 4) pairs_kernel(const PairsArgs a)
             ++ntile;
             noff = 0;
         }
-        const long long nleft = left - wc;
+        long long nleft = left - wc;
+        if (FLAT && nleft == 0) claim(ntile, noff, nleft);
         const int nwc = nleft > 0 ? width(noff, nleft) : 0;
         if (nleft > 0) {
             stage(buf ^ 1, ntile, noff, nwc);

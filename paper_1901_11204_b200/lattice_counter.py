@@ -33,6 +33,10 @@ NEIGHBOR_OFFSETS = np.array(
     [[1, 0, 0], [-1, 0, 0], [0, 1, 0], [0, -1, 0], [0, 0, 1], [0, 0, -1]], dtype=np.int64)
 
 _CELL_MAX = np.iinfo(np.uint32).max
+# reset_sparse clears the whole grid instead of scattering zeros once the
+# touched keys exceed 1/_CLEAR_RATIO of the cells (random 4-byte stores cost a
+# 32-byte sector read-modify-write each; a streaming clear costs 4 B/cell)
+_CLEAR_RATIO = 32
 
 
 class CoordinateRangeError(ValueError):
@@ -213,9 +217,15 @@ def reset_sparse(space: LatticeSpace, beads=None) -> None:
     list when present, else each given bead's cell and its six neighbours."""
     lib = _lib.load()
     if space.touched:
-        for entry in space.touched:
-            _lib.check(lib.pc_lattice_reset_keys(space.grid_ptr, space.half_extent, entry.keys.ptr,
-                                                 entry.nkeys, None))
+        nkeys = sum(entry.nkeys for entry in space.touched)
+        if space._base_clean and nkeys * _CLEAR_RATIO > space._ncells:
+            # every nonzero cell is a touched one: one streaming clear leaves the
+            # same all-zero grid faster than scattered 4-byte stores
+            _lib.check(lib.pc_lattice_clear(space.grid_ptr, space.half_extent, None))
+        else:
+            for entry in space.touched:
+                _lib.check(lib.pc_lattice_reset_keys(space.grid_ptr, space.half_extent, entry.keys.ptr,
+                                                     entry.nkeys, None))
         _lib.check(lib.pc_stream_sync(None))
         space.touched.clear()
         return

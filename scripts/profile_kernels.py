@@ -62,7 +62,7 @@ def lattice_case(reps):
         t0 = time.perf_counter()
         _lib.check(lib.pc_lattice_collisions(d5.data_ptr(), _lib.PC_I32, 1, n5, a5, grid.data_ptr(), keys.data_ptr(),
                                              1, ctypes.byref(r), ctypes.c_void_p(s.cuda_stream)))
-        _lib.check(lib.pc_lattice_reset_keys(grid.data_ptr(), a5, keys.data_ptr(), n5, ctypes.c_void_p(s.cuda_stream)))
+        _lib.check(lib.pc_lattice_clear(grid.data_ptr(), a5, ctypes.c_void_p(s.cuda_stream)))
         torch.cuda.synchronize()
         if step:
             print(json.dumps({"case": "lattice", "wall_ms": (time.perf_counter() - t0) * 1e3, "count": int(r.count),
