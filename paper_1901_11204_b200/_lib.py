@@ -15,7 +15,7 @@ from pathlib import Path
 import numpy as np
 
 HERE = Path(__file__).resolve().parent
-LIB_PATH = HERE / "libpaircount.so"
+LIB_PATH = Path(os.environ.get("PAIRCOUNT_LIB", str(HERE / "libpaircount.so")))
 
 # --- codes (include/paircount.h) -------------------------------------------
 PC_OK = 0

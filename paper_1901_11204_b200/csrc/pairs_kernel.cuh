@@ -39,8 +39,15 @@ __device__ __forceinline__ float4 col_of(const float4* sp, int k) {
     return (k & 1) ? make_float4(A.y, A.w, B.y, B.w) : make_float4(A.x, A.z, B.x, B.z);
 }
 
+#ifndef PC_MINB
+#define PC_MINB 4
+#endif
+#ifndef PC_DIRECT_UNROLL
+#define PC_DIRECT_UNROLL 2
+#endif
+constexpr int kDirectUnroll = PC_DIRECT_UNROLL;
 template <int WARPS, int R, int W, bool DIRECT, bool FLAT>
-__global__ void __launch_bounds__(WARPS * 32, 4) pairs_kernel(const PairsArgs a) {
+__global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsArgs a) {
     constexpr int T = 32 * R;
     static_assert(W % 64 == 0, "chunk must hold whole column pairs for every lane");
     __shared__ __align__(16) float4 s_pts[WARPS][2][W];  // W columns = W/2 pairs = W float4
@@ -243,7 +250,7 @@ __global__ void __launch_bounds__(WARPS * 32, 4) pairs_kernel(const PairsArgs a)
                 // ---- direct formula, packed: p = 1 + |dr|^2 for two columns per FADD2/FFMA2;
                 // two column pairs share one FMUL2/FADD2/FFMA2 for 1/pa + 1/pc = (pa+pc)/(pa*pc)
                 const float2 one = make_float2(1.0f, 1.0f);
-#pragma unroll 2
+#pragma unroll kDirectUnroll
                 for (int k = 0; k < W; k += 4) {
                     const float4 A0 = sp[k], B0 = sp[k + 1], A1 = sp[k + 2], B1 = sp[k + 3];
 #pragma unroll
