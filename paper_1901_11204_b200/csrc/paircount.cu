@@ -421,6 +421,16 @@ int num_sms() {
 template <int WARPS, int R, int W, bool DIRECT, bool FLAT>
 int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStream_t s) {
     auto kern = pairs_kernel<WARPS, R, W, DIRECT, FLAT>;
+    constexpr int smem = WARPS * pairs_smem_per_warp<R, W>();
+    {
+        static thread_local bool attr_set[64] = {false};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!attr_set[dev & 63]) {
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            attr_set[dev & 63] = true;
+        }
+    }
     int grid;
     if (FLAT) {
         static thread_local int occ_cache[64] = {0};
@@ -428,7 +438,7 @@ int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStr
         cudaGetDevice(&dev);
         if (!occ_cache[dev & 63]) {
             int occ = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, 0));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, smem));
             occ_cache[dev & 63] = occ > 0 ? occ : 1;
         }
         const long long want = (long long)num_sms() * occ_cache[dev & 63];
@@ -452,7 +462,7 @@ int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStr
         ev = &g_ev[g_ev_used++];
         CK(cudaEventRecord(ev->a, s));
     }
-    kern<<<grid, WARPS * 32, 0, s>>>(args);
+    kern<<<grid, WARPS * 32, smem, s>>>(args);
     CK_LAUNCH("pairs_kernel");
     if (ev) CK(cudaEventRecord(ev->b, s));
     *nslots_out = grid;

@@ -13,6 +13,9 @@
 // row value broadcast evaluates two pairs.  The prep kernel writes the pair
 // arrays E (pairs starting at even j) and O (odd j), each pair holding point
 // j and point (j+1) mod n, so any window position is two 16-byte cp.async.
+// A tile's rows are staged the same way (cp.async into a warp-private row
+// buffer, issued with the chunk that first needs them) so a tile switch
+// never stalls on a global load.
 //
 // Column space: a warp tile starting at row i0 walks offsets s' = 1..L
 // (partner j = i0 + s', mod n for the balanced schedule); row rl owns offset
@@ -33,7 +36,7 @@ __device__ __forceinline__ float2 f2_rsub(float a, float2 b) {  // a - b, a broa
     return *reinterpret_cast<float2*>(&dd);
 }
 
-// column k of an interleaved pair buffer: (x, y, z, w)
+// element k of an interleaved pair buffer: (x, y, z, w)
 __device__ __forceinline__ float4 col_of(const float4* sp, int k) {
     const float4 A = sp[k & ~1], B = sp[k | 1];
     return (k & 1) ? make_float4(A.y, A.w, B.y, B.w) : make_float4(A.x, A.z, B.x, B.z);
@@ -46,12 +49,18 @@ __device__ __forceinline__ float4 col_of(const float4* sp, int k) {
 #define PC_DIRECT_UNROLL 2
 #endif
 constexpr int kDirectUnroll = PC_DIRECT_UNROLL;
+
+// dynamic shared memory per warp: 2 column buffers of W + one row buffer of T (float4 each)
+template <int R, int W>
+constexpr int pairs_smem_per_warp() {
+    return (2 * W + 32 * R) * (int)sizeof(float4);
+}
+
 template <int WARPS, int R, int W, bool DIRECT, bool FLAT>
 __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsArgs a) {
     constexpr int T = 32 * R;
-    static_assert(W % 64 == 0, "chunk must hold whole column pairs for every lane");
-    __shared__ __align__(16) float4 s_pts[WARPS][2][W];  // W columns = W/2 pairs = W float4
-    __shared__ int s_j[WARPS][2][W];
+    static_assert(W % 64 == 0 && T % 64 == 0, "buffers must hold whole pairs for every lane");
+    extern __shared__ __align__(16) float4 s_dyn[];
     __shared__ unsigned long long s_red[WARPS][2];
     __shared__ double s_sum[WARPS];
 
@@ -115,44 +124,46 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
         if (j >= n) j %= n;
         return j;
     };
+    auto pair_src = [&](int j) -> const float4* {  // pair (j, (j+1) mod n)
+        return (j & 1 ? a.pts_odd : a.pts_even) + 2 * (j >> 1);
+    };
 
-    float4* sp0 = s_pts[wid][0];
-    int* sj0 = s_j[wid][0];
+    float4* sp0 = s_dyn + (size_t)wid * (2 * W + T);  // column buffers [2][W]
+    float4* rowbuf = sp0 + 2 * W;                      // row buffer [T]
     // a far column (0, 0, 0, fw): its Gram value is -inf, never a candidate
     const float fw = DIRECT ? 0.f : -INFINITY;
-    auto stage = [&](int buf, int t, int o, int wc) {
+    auto stage_cols = [&](int buf, int t, int o, int wc) {
         const int j0 = a.lo + t * T + o + 1;  // column k sits at j0 + k (mod n when balanced)
         float4* sp = sp0 + buf * W;
-        int* sj = sj0 + buf * W;
 #pragma unroll
         for (int q = 0; q < W / 64; ++q) {
-            const int p = q * 32 + lane;  // column pair p = columns 2p, 2p+1
-            const int k = 2 * p;
+            const int k = 2 * (q * 32 + lane);  // columns k, k+1
             if (k + 1 < wc) {
-                int j = j0 + k;
-                if (bal) j = wrap(j);
-                const float4* src = (j & 1 ? a.pts_odd : a.pts_even) + 2 * (j >> 1);
+                const float4* src = pair_src(bal ? wrap(j0 + k) : j0 + k);
                 cp_async16(&sp[k], src);
                 cp_async16(&sp[k + 1], src + 1);
-                sj[k] = j;
-                sj[k + 1] = (bal || j + 1 < n) ? (j + 1 == n ? 0 : j + 1) : -1;
             } else if (k < wc) {  // last column of an odd-width chunk: second half is a far point
-                int j = j0 + k;
-                if (bal) j = wrap(j);
-                const float4* src = (j & 1 ? a.pts_odd : a.pts_even) + 2 * (j >> 1);
+                const float4* src = pair_src(bal ? wrap(j0 + k) : j0 + k);
                 const float4 A = src[0], B = src[1];
                 sp[k] = make_float4(A.x, 0.f, A.z, 0.f);
                 sp[k + 1] = make_float4(B.x, 0.f, B.z, fw);
-                sj[k] = j;
-                sj[k + 1] = -1;
             } else {
                 sp[k] = make_float4(0.f, 0.f, 0.f, 0.f);
                 sp[k + 1] = make_float4(0.f, 0.f, fw, fw);
-                sj[k] = -1;
-                sj[k + 1] = -1;
             }
         }
-        cp_async_commit();
+    };
+    auto stage_rows = [&](int t) {  // rows i0 .. i0+T-1 (only those < n are read)
+        const int i0 = a.lo + t * T;
+#pragma unroll
+        for (int q = 0; q < T / 64; ++q) {
+            const int rl = 2 * (q * 32 + lane);  // rows rl, rl+1
+            if (i0 + rl < n) {
+                const float4* src = pair_src(i0 + rl);
+                cp_async16(&rowbuf[rl], src);
+                cp_async16(&rowbuf[rl + 1], src + 1);
+            }
+        }
     };
 
     float rx[R], ry[R], rz[R], rc[R];
@@ -162,10 +173,35 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     double sum = 0.0;
 
     int wc = left > 0 ? width(off, left) : 0;
-    if (left > 0) stage(0, tile, off, wc);
+    if (left > 0) {
+        stage_rows(tile);
+        stage_cols(0, tile, off, wc);
+        cp_async_commit();
+    }
     int buf = 0;
+    int staged_tile = tile;  // tile whose rows the row buffer receives / holds
     while (left > 0) {
-        // next chunk's coordinates (incremental: no divisions in the loop)
+        cp_async_wait<0>();  // chunk `buf` (and, on a switch, its tile's rows) landed
+        __syncwarp();
+        const int i0 = a.lo + tile * T;
+        if (tile != cur_tile) {
+            cur_tile = tile;
+            valid_rows = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int rl = r * 32 + lane;
+                const bool ok = i0 + rl < a.hi;
+                const float4 v = col_of(rowbuf, rl);
+                rx[r] = ok ? v.x : 0.f;
+                ry[r] = ok ? v.y : 0.f;
+                rz[r] = ok ? v.z : 0.f;
+                rc[r] = ok ? (force ? -INFINITY : -v.w - half_tb) : INFINITY;
+                valid_rows |= (ok ? 1u : 0u) << r;
+            }
+            __syncwarp();  // the row buffer may be restaged below
+        }
+
+        // next chunk's coordinates (incremental: no divisions in the loop); stage it now
         int ntile = tile, noff = off + wc;
         if (noff == L) {
             ++ntile;
@@ -175,32 +211,16 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
         if (FLAT && nleft == 0) claim(ntile, noff, nleft);
         const int nwc = nleft > 0 ? width(noff, nleft) : 0;
         if (nleft > 0) {
-            stage(buf ^ 1, ntile, noff, nwc);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncwarp();
-
-        const int i0 = a.lo + tile * T;
-        if (tile != cur_tile) {
-            cur_tile = tile;
-            valid_rows = 0;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int i = i0 + r * 32 + lane;
-                const bool ok = i < a.hi;
-                const float4 v = ok ? col_of((i & 1 ? a.pts_odd : a.pts_even) + 2 * (i >> 1), 0)
-                                    : make_float4(0.f, 0.f, 0.f, 0.f);
-                rx[r] = v.x;
-                ry[r] = v.y;
-                rz[r] = v.z;
-                rc[r] = ok ? (force ? -INFINITY : -v.w - half_tb) : INFINITY;
-                valid_rows |= (ok ? 1u : 0u) << r;
+            if (ntile != staged_tile) {
+                stage_rows(ntile);
+                staged_tile = ntile;
             }
+            stage_cols(buf ^ 1, ntile, noff, nwc);
+            cp_async_commit();
         }
+
         const float4* sp = sp0 + buf * W;
-        const int* sj = sj0 + buf * W;
+        const int j0 = i0 + off + 1;
         // every cell of the chunk owned by its row?  (see header comment)
         const bool dense = wc == W && i0 + T <= a.hi && off + 1 >= T && (!bal || off + W <= steps_min);
         unsigned fl = 0;
@@ -271,13 +291,12 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 // ---- edge chunk: per-pair ownership mask ----
                 for (int k = 0; k < W; ++k) {
                     const float4 c0 = col_of(sp, k);
-                    const int j = sj[k];
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int rl = r * 32 + lane;
                         const int i = i0 + rl;
                         const int lim = i < a.hi ? (bal ? steps_for_dev(n, i) : n - 1 - i) : 0;
-                        const bool ok = j >= 0 && (unsigned)(off + k - rl) < (unsigned)lim;
+                        const bool ok = k < wc && (unsigned)(off + k - rl) < (unsigned)lim;
                         const float dx = rx[r] - c0.x, dy = ry[r] - c0.y, dz = rz[r] - c0.z;
                         const float p = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1.0f)));
                         acc[r].x += ok ? rcp_approx(p) : 0.0f;
@@ -292,36 +311,40 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             }
         }
 
-        // ---- slow path: re-scan flagged rows 8 columns at a time (independent
-        // FMA chains), exact reference predicate on each owned candidate ----
+        // ---- slow path (warp-cooperative): each flagged row is broadcast and all
+        // 32 lanes re-test its W columns in parallel; every owned candidate is
+        // re-evaluated with the exact reference predicate by the lane that found it.
+        // (A lane-serial rescan cost ~800 instructions per flagged row and, 8x
+        // unrolled, thrashed the I-cache at N = 65,536 where ~1 chunk in 1 flags.)
         if (__any_sync(0xffffffffu, fl != 0)) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                if (fl & (1u << r)) {
-                    const int rl = r * 32 + lane;
+                unsigned owners = __ballot_sync(0xffffffffu, (fl >> r) & 1u);
+                while (owners) {
+                    const int src = __ffs(owners) - 1;
+                    owners &= owners - 1;
+                    const float qx = __shfl_sync(0xffffffffu, rx[r], src);
+                    const float qy = __shfl_sync(0xffffffffu, ry[r], src);
+                    const float qz = __shfl_sync(0xffffffffu, rz[r], src);
+                    const float qc = __shfl_sync(0xffffffffu, rc[r], src);
+                    const int rl = r * 32 + src;
                     const int i = i0 + rl;
                     const int lim = bal ? steps_for_dev(n, i) : n - 1 - i;  // flagged rows are valid rows
-                    for (int k0 = 0; k0 < wc; k0 += 8) {
-                        unsigned cm = 0;
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            const float4 c0 = col_of(sp, k0 + u);
-                            bool cand;
-                            if (DIRECT) {
-                                const float dx = rx[r] - c0.x, dy = ry[r] - c0.y, dz = rz[r] - c0.z;
-                                cand = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1.0f))) < thr2;
-                            } else {
-                                const float tt = fmaf(rz[r], c0.z, fmaf(ry[r], c0.y, fmaf(rx[r], c0.x, c0.w)));
-                                cand = force || tt > rc[r];
-                            }
-                            cm |= (cand && (unsigned)(off + k0 + u - rl) < (unsigned)lim && k0 + u < wc ? 1u : 0u)
-                                  << u;
+#pragma unroll 2
+                    for (int q = 0; q < W / 32; ++q) {
+                        const int k = q * 32 + lane;
+                        const float4 c0 = col_of(sp, k);
+                        bool cand;
+                        if (DIRECT) {
+                            const float dx = qx - c0.x, dy = qy - c0.y, dz = qz - c0.z;
+                            cand = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1.0f))) < thr2;
+                        } else {
+                            const float tt = fmaf(qz, c0.z, fmaf(qy, c0.y, fmaf(qx, c0.x, c0.w)));
+                            cand = force || tt > qc;
                         }
-                        while (cm) {
-                            const int u = __ffs(cm) - 1;
-                            cm &= cm - 1;
+                        if (cand && k < wc && (unsigned)(off + k - rl) < (unsigned)lim) {
                             ++checks;
-                            cnt += exact_pair(a.xyz, a.dtype, a.pred, i, sj[k0 + u]) ? 1ull : 0ull;
+                            cnt += exact_pair(a.xyz, a.dtype, a.pred, i, bal ? wrap(j0 + k) : j0 + k) ? 1ull : 0ull;
                         }
                     }
                 }
