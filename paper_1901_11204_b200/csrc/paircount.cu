@@ -773,6 +773,8 @@ __global__ void count_nonzero_kernel(const uint4* __restrict__ grid4, long long 
 }
 
 // Scratch layout for one lattice call: [coords copy][bad u64][overflow int][slots][sums]
+#include "lattice_slab.cuh"
+
 struct LatScratch {
     const void* xyz;
     unsigned long long* bad;
@@ -787,11 +789,11 @@ int lattice_blocks(long long n) {
 }
 
 int lat_prepare(const void* xyz, int dtype, int on_device, long long n, Arena** ar_out, LatScratch* sc,
-                cudaStream_t* s_inout) {
+                cudaStream_t* s_inout, size_t extra = 0, char** extra_out = nullptr) {
     if (dtype != PC_I32 && dtype != PC_I64) return arg_fail("lattice beads must be int32 or int64");
     const int nb = lattice_blocks(n);
     const size_t cbytes = on_device ? 0 : align_up((size_t)n * 3 * dtype_bytes(dtype), 256);
-    const size_t need = cbytes + 256 + align_up((size_t)nb * sizeof(LatSlot), 256) + 256;
+    const size_t need = cbytes + 256 + align_up((size_t)nb * sizeof(LatSlot), 256) + 256 + align_up(extra, 256);
     Arena* ar = nullptr;
     int rc = arena_get(need, &ar);
     if (rc) return rc;
@@ -808,6 +810,7 @@ int lat_prepare(const void* xyz, int dtype, int on_device, long long n, Arena** 
     sc->slots = (LatSlot*)(base + cbytes + 256);
     sc->sums = (unsigned long long*)(base + cbytes + 256 + align_up((size_t)nb * sizeof(LatSlot), 256));
     sc->nslots = nb;
+    if (extra_out) *extra_out = (char*)sc->sums + 256;
     CK(cudaMemsetAsync(sc->bad, 0xff, 8, s));
     CK(cudaMemsetAsync(sc->overflow, 0, 4, s));
     *ar_out = ar;
@@ -832,12 +835,56 @@ int lattice_run(const void* xyz_in, int dtype, int on_device, long long n, long 
         CK(cudaGetDevice(&dev));
         lock = std::unique_lock<std::mutex>(g_arena[dev & 63].mu);
     }
-    int rc = lat_prepare(xyz_in, dtype, on_device, n, &ar, &sc, &s);
+    const unsigned long long cells = (unsigned long long)side * side * side;
+    // dense regime on a clean grid: shared-memory slab histogram (lattice_slab.cuh)
+    // crossover: n scattered atomics at ~21 G/s vs streaming 4 B/cell + ~40 B/bead at HBM rate -> n > cells/67
+    const bool slab = clean && !contacts && sizeof(KT) == 4 && (unsigned long long)n * 64 > cells &&
+                      n < (1LL << 32) - 1;
+    const int nbuckets = (int)((cells + (1ull << kBucketShift) - 1) >> kBucketShift);
+    const size_t kbytes = align_up((size_t)n * 4, 256);
+    const size_t extra = slab ? 2 * kbytes + 3 * align_up((kMaxBuckets + 1) * 4, 256) +
+                                    align_up((size_t)nbuckets * sizeof(LatSlot), 256)
+                              : 0;
+    char* ex = nullptr;
+    int rc = lat_prepare(xyz_in, dtype, on_device, n, &ar, &sc, &s, extra, &ex);
     if (rc) return rc;
     const int nb = sc.nslots;
-    lat_keys_kernel<KT><<<nb, 256, 0, s>>>(sc.xyz, dtype, n, a, side, keys, sc.bad);
-    CK_LAUNCH("lat_keys_kernel");
-    if (clean && !contacts) {
+    if (slab) {
+        unsigned* sorted = (unsigned*)ex;
+        unsigned* scratch = (unsigned*)(ex + kbytes);
+        unsigned* hist = (unsigned*)(ex + 2 * kbytes);
+        unsigned* base = hist + align_up((kMaxBuckets + 1) * 4, 256) / 4;
+        unsigned* cursor = base + align_up((kMaxBuckets + 1) * 4, 256) / 4;
+        LatSlot* bslots = (LatSlot*)(cursor + align_up((kMaxBuckets + 1) * 4, 256) / 4);
+        static thread_local bool attr_set[64] = {false};
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        if (!attr_set[dev & 63]) {
+            CK(cudaFuncSetAttribute(lat_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSlabSmem));
+            attr_set[dev & 63] = true;
+        }
+        CK(cudaMemsetAsync(hist, 0, nbuckets * 4, s));
+        lat_keys_hist_kernel<<<nb, 256, nbuckets * 4, s>>>(sc.xyz, dtype, n, a, side, (unsigned*)keys, sc.bad, hist,
+                                                           nbuckets);
+        CK_LAUNCH("lat_keys_hist_kernel");
+        lat_bucket_scan_kernel<<<1, 1024, 0, s>>>(hist, base, cursor, nbuckets);
+        CK_LAUNCH("lat_bucket_scan_kernel");
+        lat_bucket_scatter_kernel<<<num_sms() * 3, 512, 2 * nbuckets * 4, s>>>((const unsigned*)keys, n, cursor,
+                                                                              sorted, nbuckets, sc.bad);
+        CK_LAUNCH("lat_bucket_scatter_kernel");
+        const int sgrid = std::min(num_sms(), nbuckets);
+        lat_slab_kernel<<<sgrid, 1024, kSlabSmem, s>>>(sorted, scratch, base, nbuckets, grid, cells, sc.bad, bslots,
+                                                       sc.overflow);
+        CK_LAUNCH("lat_slab_kernel");
+        lat_sum_slots_kernel<<<1, 256, 0, s>>>(bslots, sgrid, sc.sums);
+        CK_LAUNCH("lat_sum_slots_kernel");
+    } else {
+        lat_keys_kernel<KT><<<nb, 256, 0, s>>>(sc.xyz, dtype, n, a, side, keys, sc.bad);
+        CK_LAUNCH("lat_keys_kernel");
+    }
+    if (slab) {
+        // count / cells_touched are in sums[0], sums[1], as for the atomic path
+    } else if (clean && !contacts) {
         lat_place_clean_kernel<KT><<<nb, 256, 0, s>>>(keys, n, grid, sc.bad, sc.slots, sc.overflow);
         CK_LAUNCH("lat_place_clean_kernel");
         lat_sum_slots_kernel<<<1, 256, 0, s>>>(sc.slots, nb, sc.sums);
