@@ -237,17 +237,18 @@ def secondary(torch, lib, stream):
         if step >= 3:
             times.append(e0.elapsed_time(e1))
     ms = float(np.median(times))
-    # coords (int32 SoA-in-AoS, 12 B) + key write/read (8 B) + atomic RMW (8 B) per bead, 4 B/cell clear
-    b_alg = 28 * n5 + 4 * ncell
+    # SURVEY.md §8(d) B_alg: 12 B coords + 8 B counter RMW per bead, 8 B per cell (write + clear)
+    b_alg = 20 * n5 + 8 * ncell
+    peaks = ROOT / "MEASURED_PEAKS.json"
+    hbm = json.loads(peaks.read_text()).get("hbm_gbs", 6532.5) if peaks.exists() else 6532.5
     out["cfg5_counting_array_n2^26"] = {
         "wall_ms_per_step": ms, "count": int(r.count), "cells_touched": int(r.cells_touched),
         "expected_count": 2101067, "grid_cells": ncell,
-        "step": "count_collisions (validate+keys, Alg. 1 atomic histogram, sum of old) + reset_sparse "
-                "(streaming clear: keys > cells/32 on a clean grid)",
-        "alg_bytes": b_alg, "achieved_GBps": b_alg / (ms * 1e-3) / 1e9,
-        "hbm_frac_of_measured": b_alg / (ms * 1e-3) / 1e9 / 6532.5,
-        "note": "the 2^26 scattered atomics run at the measured scattered-atomic ceiling (~22 G/s, "
-                "scripts/microbench_hist.cu), not at HBM bandwidth"}
+        "step": "count_collisions (dense regime: validate+keys, bucket partition, Alg. 1 on shared-memory "
+                "slabs, TMA bulk slab stores) + reset_sparse (streaming clear)",
+        "alg_bytes_survey": b_alg, "achieved_GBps": b_alg / (ms * 1e-3) / 1e9,
+        "hbm_frac_of_measured": b_alg / (ms * 1e-3) / 1e9 / hbm,
+        "note": "scattered global atomics would cap this at ~21 G beads/s (scripts/microbench_l2atomic.cu)"}
     del d5, grid, keys
     return out
 
