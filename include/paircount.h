@@ -165,6 +165,17 @@ int pc_lattice_contacts(const void* xyz, int32_t dtype, int32_t xyz_on_device, i
 /* reset_sparse via the touched list (lattice_counter.py:205-210) */
 int pc_lattice_reset_keys(uint32_t* grid, int64_t half_extent, const void* keys, int64_t nkeys,
                           void* stream);
+/* Batched small vectors -- the paper's experiments count 100-1000 bead
+ * vectors per execution (bench_cli.py:129-141 `_linear_pass`).
+ * Vector v is beads [offsets[v], offsets[v+1]) of xyz (offsets: host, nvec+1
+ * entries); results[v] equals count_collisions(vector, space) on a clean
+ * space followed by reset_sparse -- one launch for all vectors, one CTA per
+ * vector, Alg. 1 on an on-chip hashed counting array.  results[v].error:
+ * PC_ERR_RANGE (detail = first bad bead within the vector) or PC_ERR_ARG for
+ * a vector longer than 4096 beads, which the caller counts through a grid. */
+int pc_lattice_collisions_batch(const void* xyz, int32_t dtype, int32_t xyz_on_device, const int64_t* offsets,
+                                int32_t nvec, int64_t half_extent, pc_lattice_result* results, void* stream);
+
 /* Zero the whole grid with one streaming write (cudaMemsetAsync).  The
  * Python reset_sparse uses it in place of pc_lattice_reset_keys when the
  * touched keys number more than 1/32 of the cells AND every other cell is

@@ -47,6 +47,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 namespace {
 
@@ -775,6 +776,76 @@ __global__ void count_nonzero_kernel(const uint4* __restrict__ grid4, long long 
 // Scratch layout for one lattice call: [coords copy][bad u64][overflow int][slots][sums]
 #include "lattice_slab.cuh"
 
+// ---- batched small vectors (the paper's 100-1000 vectors per execution) ----
+// One CTA per vector; Alg. 1 (collisions += space[b]; space[b]++) on a
+// shared-memory counting array addressed by an open-addressing hash of the
+// cell key (the dense (2a+3)^3 grid does not fit on chip).  Equivalent to
+// count_collisions + reset_sparse per vector on a clean space.
+constexpr int kBatchSlots = 8192;  // vectors up to kBatchSlots/2 beads; larger ones go through the grid
+constexpr unsigned long long kEmptyKey = ~0ull;
+constexpr int kBatchSmem = kBatchSlots * 12;
+
+__global__ void __launch_bounds__(256) lat_batch_kernel(const void* __restrict__ xyz, int dtype,
+                                                        const long long* __restrict__ offs, int nvec, long long a,
+                                                        long long side, unsigned long long* __restrict__ out) {
+    extern __shared__ unsigned long long tkey[];  // [kBatchSlots] keys, then [kBatchSlots] uint32 counts
+    unsigned* tcnt = reinterpret_cast<unsigned*>(tkey + kBatchSlots);
+    __shared__ unsigned long long s_acc[8], s_first[8];
+    __shared__ long long s_bad;
+    for (int v = blockIdx.x; v < nvec; v += gridDim.x) {
+        const long long lo = offs[v], hi = offs[v + 1];
+        for (int q = threadIdx.x; q < kBatchSlots; q += blockDim.x) {
+            tkey[q] = kEmptyKey;
+            tcnt[q] = 0u;
+        }
+        if (threadIdx.x == 0) s_bad = -1;
+        __syncthreads();
+        unsigned long long acc = 0, first = 0;
+        if (hi - lo <= kBatchSlots / 2) {
+            for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+                const long long x = coord_i64(xyz, dtype, i, 0), y = coord_i64(xyz, dtype, i, 1),
+                                z = coord_i64(xyz, dtype, i, 2);
+                if (x < -a || x > a || y < -a || y > a || z < -a || z > a) {
+                    atomicMin((unsigned long long*)&s_bad, (unsigned long long)(i - lo));
+                    continue;
+                }
+                const unsigned long long key = (unsigned long long)(((x + a + 1) * side + (y + a + 1)) * side + (z + a + 1));
+                unsigned h = (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 51) & (kBatchSlots - 1);
+                for (;;) {
+                    const unsigned long long prev = atomicCAS(&tkey[h], kEmptyKey, key);
+                    if (prev == kEmptyKey || prev == key) {
+                        const unsigned old = atomicAdd(&tcnt[h], 1u);  // Alg. 1
+                        acc += old;
+                        first += old == 0u;
+                        break;
+                    }
+                    h = (h + 1) & (kBatchSlots - 1);
+                }
+            }
+        }
+        acc = warp_sum(acc);
+        first = warp_sum(first);
+        if ((threadIdx.x & 31) == 0) {
+            s_acc[threadIdx.x >> 5] = acc;
+            s_first[threadIdx.x >> 5] = first;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long c = 0, f = 0;
+            for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+                c += s_acc[q];
+                f += s_first[q];
+            }
+            const bool big = hi - lo > kBatchSlots / 2;
+            out[3 * v] = c;
+            out[3 * v + 1] = f;
+            // first out-of-range bead (vector-relative), ~0 if none, ~1 if the vector was too long
+            out[3 * v + 2] = big ? ~1ull : (unsigned long long)s_bad;
+        }
+        __syncthreads();
+    }
+}
+
 struct LatScratch {
     const void* xyz;
     unsigned long long* bad;
@@ -1144,6 +1215,63 @@ int pc_lattice_reset_keys(uint32_t* grid, int64_t half_extent, const void* keys,
     if (pc_lattice_key_bytes(half_extent) == 4) lat_zero_keys_kernel<unsigned><<<nb, 256, 0, s>>>((const unsigned*)keys, nkeys, grid);
     else lat_zero_keys_kernel<unsigned long long><<<nb, 256, 0, s>>>((const unsigned long long*)keys, nkeys, grid);
     CK_LAUNCH("lat_zero_keys_kernel");
+    return PC_OK;
+}
+
+int pc_lattice_collisions_batch(const void* xyz, int32_t dtype, int32_t xyz_on_device, const int64_t* offsets,
+                                int32_t nvec, int64_t half_extent, pc_lattice_result* results, void* stream) {
+    g_launches = 0;
+    if (nvec < 0 || !offsets) return arg_fail("bad vector offsets");
+    if (half_extent < 0) return arg_fail("half_extent must be >= 0");
+    if (dtype != PC_I32 && dtype != PC_I64) return arg_fail("lattice beads must be int32 or int64");
+    for (int v = 0; v < nvec; ++v)
+        if (offsets[v] < 0 || offsets[v] > offsets[v + 1]) return arg_fail("vector offsets must be non-decreasing");
+    if (nvec == 0) return PC_OK;
+    const long long n = offsets[nvec];
+    const size_t cbytes = xyz_on_device ? 0 : align_up((size_t)n * 3 * dtype_bytes(dtype), 256);
+    const size_t obytes = align_up((size_t)(nvec + 1) * 8, 256), rbytes = align_up((size_t)nvec * 24, 256);
+    cudaStream_t s = (cudaStream_t)stream;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_arena[dev & 63].mu);
+    Arena* ar = nullptr;
+    int rc = arena_get(cbytes + obytes + rbytes, &ar);
+    if (rc) return rc;
+    char* base = (char*)ar->dev;
+    const void* dxyz = xyz;
+    if (!xyz_on_device) {
+        if (n > 0) CK(cudaMemcpyAsync(base, xyz, (size_t)n * 3 * dtype_bytes(dtype), cudaMemcpyHostToDevice, s));
+        dxyz = base;
+    }
+    long long* doffs = (long long*)(base + cbytes);
+    unsigned long long* dout = (unsigned long long*)(base + cbytes + obytes);
+    CK(cudaMemcpyAsync(doffs, offsets, (size_t)(nvec + 1) * 8, cudaMemcpyHostToDevice, s));
+    static thread_local bool attr_set[64] = {false};
+    if (!attr_set[dev & 63]) {
+        CK(cudaFuncSetAttribute(lat_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBatchSmem));
+        attr_set[dev & 63] = true;
+    }
+    const int grid = std::min(nvec, 2 * num_sms());
+    lat_batch_kernel<<<grid, 256, kBatchSmem, s>>>(dxyz, dtype, doffs, nvec, half_extent, 2 * half_extent + 3, dout);
+    CK_LAUNCH("lat_batch_kernel");
+    std::vector<unsigned long long> host((size_t)nvec * 3);
+    CK(cudaMemcpyAsync(host.data(), dout, host.size() * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int v = 0; v < nvec; ++v) {
+        pc_lattice_result& r = results[v];
+        memset(&r, 0, sizeof r);
+        r.beads_processed = offsets[v + 1] - offsets[v];
+        const unsigned long long st = host[3 * v + 2];
+        if (st == ~1ull) {
+            r.error = PC_ERR_ARG;  // longer than the on-chip table: caller counts it through a grid
+        } else if (st != ~0ull) {
+            r.error = PC_ERR_RANGE;
+            r.detail = (long long)st;
+        } else {
+            r.count = (long long)host[3 * v];
+            r.cells_touched = (long long)host[3 * v + 1];
+        }
+    }
     return PC_OK;
 }
 

@@ -244,6 +244,44 @@ def reset_sparse(space: LatticeSpace, beads=None) -> None:
     space._base_clean = False
 
 
+def count_collisions_batch(vectors, space: LatticeSpace) -> list[CountReport]:
+    """Count every bead vector as ``count_collisions(v, space)`` on a clean
+    space followed by ``reset_sparse`` -- the reference's per-vector loop
+    (bench_cli.py:129-141 ``_linear_pass``; the paper counts 100-1000 vectors
+    per execution) -- in one GPU launch: one CTA per
+    vector, Alg. 1 on an on-chip hashed counting array.  Vectors longer than
+    4096 beads go through ``space``'s grid.  The space must be clean on entry
+    and is clean on return.  Raises CoordinateRangeError for the first vector
+    holding a bead outside [-a, a]^3."""
+    if not space._clean():
+        raise ValueError("count_collisions_batch needs a clean space (fresh or reset)")
+    arrays = [np.ascontiguousarray(as_bead_array(v)) for v in vectors]
+    if not arrays:
+        return []
+    offsets = np.zeros(len(arrays) + 1, dtype=np.int64)
+    np.cumsum([len(a) for a in arrays], out=offsets[1:])
+    allb = np.concatenate(arrays) if offsets[-1] else np.zeros((0, 3), dtype=np.int64)
+    if len(allb) and np.abs(allb).max() < 2**31 - 1:
+        allb = allb.astype(np.int32)
+    allb = np.ascontiguousarray(allb)
+    res = (_lib.LatticeResult * len(arrays))()
+    lib = _lib.load()
+    _lib.check(lib.pc_lattice_collisions_batch(allb.ctypes.data, _lib.DTYPE_CODES[allb.dtype], 0,
+                                               offsets.ctypes.data, len(arrays), space.half_extent,
+                                               ctypes.addressof(res), None))
+    reports = []
+    for arr, r in zip(arrays, res):
+        if r.error == _lib.PC_ERR_RANGE:
+            _raise_for(r, space, arr)
+        if r.error == _lib.PC_ERR_ARG:  # too long for the on-chip table: through the grid
+            rep = count_collisions(arr, space)
+            reset_sparse(space)
+            reports.append(rep)
+            continue
+        reports.append(CountReport(count=int(r.count), beads_processed=len(arr), cells_touched=int(r.cells_touched)))
+    return reports
+
+
 def _integer_pairs(beads, interaction: int) -> int:
     arr = as_bead_array(beads)
     n = len(arr)

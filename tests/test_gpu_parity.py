@@ -293,3 +293,20 @@ def test_chains_vs_oracle():
 def test_smoke_entry():
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+def test_batched_small_vectors():
+    # §8(f4): one launch for many vectors == count_collisions + reset_sparse per vector
+    vectors = [gen.random_chain(n, 5000 + v)[0] for n in (1, 2, 3, 16, 64, 257, 1024, 4096) for v in range(12)]
+    vectors += [np.zeros((40, 3), dtype=np.int64), np.zeros((0, 3), dtype=np.int64), gen.random_chain(6000, 1)[0]]
+    ext = max(int(np.abs(v).max()) if len(v) else 0 for v in vectors)
+    sp = pc.new_space(ext)
+    reps = pc.count_collisions_batch(vectors, sp)
+    assert sp.is_zero() and not sp.touched
+    for v, rep in zip(vectors, reps):
+        want = c_oracle.int_pairs(v)[0] if len(v) else 0
+        ref = lc.count_collisions(v, sp)
+        pc.reset_sparse(sp)
+        assert (rep.count, rep.beads_processed, rep.cells_touched) == (want, len(v), ref.cells_touched)
+    with pytest.raises(lc.CoordinateRangeError, match="bead 1"):
+        pc.count_collisions_batch([[(0, 0, 0)], [(0, 0, 0), (ext + 1, 0, 0)]], sp)
