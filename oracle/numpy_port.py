@@ -158,6 +158,36 @@ def count_collisions(beads, half_extent: int):
     return int((counts * (counts - 1) // 2).sum()), len(arr), len(counts)
 
 
+def new_dense_space(half_extent: int) -> np.ndarray:
+    """Dense uint32 grid of side 2a+3 (LatticeSpace.__init__, lattice_counter.py:70-88)."""
+    side = 2 * half_extent + 3
+    return np.zeros((side, side, side), dtype=np.uint32)
+
+
+def count_collisions_dense(beads, cells: np.ndarray, half_extent: int):
+    """Alg. 1 exactly as the reference runs it on its dense numpy grid:
+    validate, flatten, np.unique, np.add.at, overflow check, occ gather,
+    sum(occ-1)//2, then reset_sparse through the unique cells
+    (lattice_counter.py:98-156, 198-210).  Used as the timed CPU baseline of
+    the counting-array rows.  Returns (count, n, cells_touched)."""
+    arr = np.asarray(beads, dtype=np.int64).reshape(-1, 3)
+    if len(arr) == 0:
+        return 0, 0, 0
+    if (np.abs(arr) > half_extent).any():
+        raise ValueError("bead out of range")
+    shifted = arr + (half_extent + 1)
+    flat = np.ravel_multi_index((shifted[:, 0], shifted[:, 1], shifted[:, 2]), cells.shape)
+    occupied = np.unique(flat)
+    flat_cells = cells.reshape(-1)
+    np.add.at(flat_cells, flat, 1)
+    if flat_cells[occupied].max(initial=0) >= np.iinfo(np.uint32).max:
+        raise OverflowError("cell occupancy overflow")
+    occ = flat_cells[flat].astype(np.int64)
+    count = int((occ - 1).sum()) // 2
+    flat_cells[occupied] = 0
+    return count, len(arr), len(occupied)
+
+
 def count_contacts(beads, half_extent: int):
     """Alg. 2 (lattice_counter.py:159-195): doubled neighbour-occupancy sum
     over the six axial offsets, halved; cells_touched counts the distinct

@@ -82,6 +82,9 @@ def test_lattice_port(golden_small):
         assert (col, con) == (case["oracle_collisions"], case["oracle_contacts"]), case["tag"]
         if "count_collisions" in case:
             assert list(npo.count_collisions(beads, case["half_extent"])) == case["count_collisions"], case["tag"]
+            cells = npo.new_dense_space(case["half_extent"])
+            assert list(npo.count_collisions_dense(beads, cells, case["half_extent"])) == case["count_collisions"]
+            assert not cells.any()  # left clean by the sparse reset
             assert list(npo.count_contacts(beads, case["half_extent"])) == case["count_contacts"], case["tag"]
 
 
