@@ -251,6 +251,37 @@ def secondary(torch, lib, stream):
         "note": "scattered global atomics would cap this at ~21 G beads/s (scripts/microbench_l2atomic.cu)"}
     del d5, grid, keys
 
+    # ---- config 4: 2^22 clustered points, count; the per-rank slabs of a 2/4/8-GPU split timed
+    # one after another on this GPU (ranks never wait on each other: the only exchange is the final
+    # all-reduce), giving the load balance of the split and a projected multi-GPU step.
+    from paper_1901_11204_b200.distributed import row_slabs
+
+    n4 = 2**22
+    obj4 = gen.clustered_spheres(n4).astype(np.float32)
+    d4 = torch.from_numpy(obj4).cuda()
+    ws4 = torch.empty(_lib.workspace_bytes(n4), dtype=torch.uint8, device="cuda")
+    res4 = torch.zeros(8, dtype=torch.int64, device="cuda")
+
+    def run_slab(lo, hi):
+        _lib.kernel_timing(True)
+        _lib.pairs_async(d4.data_ptr(), _lib.PC_F32, n4, _lib.PC_COLLISION, _lib.PC_BALANCED, np.array([lo, hi]),
+                         ws4.data_ptr(), ws4.numel(), res4.data_ptr(), stream.cuda_stream, _lib.PC_TILE_FLAT)
+        ms_k, _ = _lib.kernel_timing_read()
+        _lib.kernel_timing(False)
+        return ms_k, int(res4[0].item())
+
+    run_slab(0, n4)  # warm-up
+    full_ms, full_count = run_slab(0, n4)
+    pairs4 = n4 * (n4 - 1) // 2
+    cfg4 = {"kernel_ms_1gpu": full_ms, "Gpair_per_s_1gpu": pairs4 / (full_ms * 1e-3) / 1e9, "count": full_count}
+    for g in (2, 4, 8):
+        times, counts = zip(*(run_slab(lo, hi) for lo, hi in row_slabs(n4, g, "balanced")))
+        cfg4[f"split{g}"] = {"slab_ms_max": max(times), "slab_ms_min": min(times),
+                             "projected_step_ms": max(times), "projected_speedup": full_ms / max(times),
+                             "partials_sum_equals_total": sum(counts) == full_count}
+    out["cfg4_clustered_n2^22_count"] = cfg4
+    del d4, ws4
+
     # ---- many small vectors: the paper's setting (1000 chain vectors per execution)
     from oracle import numpy_port as npo
     from paper_1901_11204_b200 import lattice_counter as lc

@@ -310,3 +310,30 @@ def test_batched_small_vectors():
         assert (rep.count, rep.beads_processed, rep.cells_touched) == (want, len(v), ref.cells_touched)
     with pytest.raises(lc.CoordinateRangeError, match="bead 1"):
         pc.count_collisions_batch([[(0, 0, 0)], [(0, 0, 0), (ext + 1, 0, 0)]], sp)
+
+
+def test_filter_bypass_for_huge_spans():
+    # spans beyond ~1e15 make the fp32 Gram filter meaningless: every pair takes the exact path
+    rng = np.random.default_rng(3)
+    pts = rng.random((300, 3)) * 4.0
+    pts[::7] += 1e20
+    pts[1::7] = pts[::7][: len(pts[1::7])] + 0.3  # near pairs far out
+    want, _, _ = c_oracle.rows(pts, 0, len(pts), "balanced")
+    assert se.spi_balanced(pts, se.collision_indicator).total == want
+    assert se.spi_standard(pts, se.collision_indicator).total == want
+    ints = np.array([[2**62, 0, 0], [2**62, 0, 0], [-2**62, 1, 0], [-2**62, 0, 0], [5, 5, 5]], dtype=np.int64)
+    assert pc.oracle_collisions(ints) == c_oracle.int_pairs(ints)[0] == 1
+    assert pc.oracle_contacts(ints) == c_oracle.int_pairs(ints)[1]
+    with pytest.raises(ValueError):
+        se.spi_balanced(np.array([[0.0, 0, 0], [1e19, 0, 0]]), se.inverse_square)
+
+
+def test_row_range_api_edges():
+    objs = gen.random_spheres(5000, 12.0, 8).astype(np.float32)
+    for rows in ((0, 0), (4999, 5000), (2500, 2500), (0, 1), (17, 4000)):
+        for sched in se.SCHEDULES:
+            got, pairs = se.spi_rows(objs, se.collision_indicator, rows, sched)
+            c, _, p = c_oracle.rows(objs, rows[0], rows[1], sched)
+            assert (got, pairs) == (c, p)
+    with pytest.raises(ValueError):
+        se.spi_rows(objs, se.collision_indicator, (10, 5), "balanced")
