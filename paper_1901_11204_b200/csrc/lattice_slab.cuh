@@ -8,13 +8,14 @@
 // path is bound by streaming the finished slabs to HBM instead.
 //
 //   K1 lat_keys_hist_kernel   validate, write each bead's key (the touched
-//                             list), histogram keys by 256K-cell bucket
+//                             list), histogram keys by 128K-cell bucket
 //   K2 lat_bucket_scan_kernel exclusive scan of the bucket histogram
 //   K3 lat_bucket_scatter_kernel  partition keys by bucket (tile-local ranks
 //                             + one global reservation per tile and bucket)
 //   K4 lat_slab_kernel        persistent, one CTA per SM, buckets round-robin:
-//                             sub-partition a bucket into 16 slabs of 16K
-//                             cells, then per slab zero a 64 KB shared-memory
+//                             stage a bucket's keys on chip, counting-sort them
+//                             into 16 slabs of 8K cells, then per slab zero a
+//                             32 KB shared-memory
 //                             counting array, atomicAdd each bead (old value =
 //                             its new collisions; old == 0 marks a touched
 //                             cell) and hand the slab to a TMA bulk store
@@ -24,12 +25,13 @@
 // Valid only on a clean grid (every cell zero on entry): the slab stores
 // overwrite whole cell ranges.  Used when beads outnumber cells/64.
 
-constexpr int kBucketShift = 18;  // 256K cells per bucket
-constexpr int kSlabShift = 14;    // 16K cells per shared-memory slab (2 x 64 KB buffers, 1 CTA per SM)
+constexpr int kBucketShift = 17;  // 128K cells per bucket
+constexpr int kSlabShift = 13;    // 8K cells per shared-memory slab (2 x 32 KB buffers)
 constexpr int kSlabCells = 1 << kSlabShift;
 constexpr int kSubSlabs = 1 << (kBucketShift - kSlabShift);  // 16
 constexpr int kMaxBuckets = 16384;                             // grids below 2^32 cells
-constexpr int kSlabSmem = 2 * kSlabCells * 4 + 3 * kSubSlabs * 4;
+constexpr int kKeyCap = 16384;    // keys of one bucket staged on chip (2x the uniform mean)
+constexpr int kSlabSmem = (kKeyCap + 8 + kKeyCap + 2 * kSlabCells + 3 * kSubSlabs) * 4;
 
 __global__ void lat_keys_hist_kernel(const void* __restrict__ xyz, int dtype, long long n, long long a,
                                      long long side, unsigned* __restrict__ keys,
@@ -148,70 +150,120 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Persistent: CTA c walks buckets c, c + gridDim.x, ...  Alg. 1 on shared-memory slabs.
+// A bucket's keys (<= kKeyCap) are staged on chip with cp.async -- the next
+// bucket's while this one's slabs run -- and counting-sorted by slab in shared
+// memory; larger buckets (clustered input) fall back to a global-memory
+// sub-partition through `scratch`.
 __global__ void __launch_bounds__(1024, 1)
     lat_slab_kernel(const unsigned* __restrict__ sorted, unsigned* __restrict__ scratch,
                     const unsigned* __restrict__ base, int nbuckets, unsigned* __restrict__ grid,
                     unsigned long long cells, const unsigned long long* __restrict__ bad,
                     LatSlot* __restrict__ slots, int* __restrict__ overflow) {
     extern __shared__ __align__(128) unsigned smem[];
-    unsigned* cbuf[2] = {smem, smem + kSlabCells};    // double-buffered counting arrays
-    unsigned* sub_n = smem + 2 * kSlabCells;          // [kSubSlabs] keys per slab
-    unsigned* sub_cur = sub_n + kSubSlabs;            // [kSubSlabs] scatter cursors
-    unsigned* sub_start = sub_cur + kSubSlabs;        // [kSubSlabs] slab start offsets
+    unsigned* keys_in = smem;                           // [kKeyCap + 8] staged keys (16 B aligned window)
+    unsigned* keys_s = keys_in + kKeyCap + 8;           // [kKeyCap] keys grouped by slab
+    unsigned* cbuf0 = keys_s + kKeyCap;                 // [2][kSlabCells] double-buffered counting arrays
+    unsigned* sub_n = cbuf0 + 2 * kSlabCells;           // [kSubSlabs] keys per slab
+    unsigned* sub_cur = sub_n + kSubSlabs;              // [kSubSlabs] scatter cursors
+    unsigned* sub_start = sub_cur + kSubSlabs;          // [kSubSlabs] slab start offsets
     __shared__ unsigned long long s_a[32], s_b[32];
     unsigned long long acc = 0, first = 0;
     int ovf = 0;
     const bool ok = *bad == kNoBad;
     int flip = 0;
-    for (int b = blockIdx.x; ok && b < nbuckets; b += gridDim.x) {
-        const unsigned lo = base[b], hi = base[b + 1];
-        // sub-partition the bucket's keys by slab (into the same range of `scratch`)
-        if (threadIdx.x < kSubSlabs) sub_n[threadIdx.x] = 0u;
-        __syncthreads();
-        for (unsigned i = lo + threadIdx.x; i < hi; i += blockDim.x)
-            atomicAdd(&sub_n[(sorted[i] >> kSlabShift) & (kSubSlabs - 1)], 1u);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned run = 0;
-            for (int s = 0; s < kSubSlabs; ++s) {
-                sub_start[s] = run;
-                sub_cur[s] = run;
-                run += sub_n[s];
-            }
-        }
-        __syncthreads();
-        for (unsigned i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-            const unsigned k = sorted[i];
-            scratch[lo + atomicAdd(&sub_cur[(k >> kSlabShift) & (kSubSlabs - 1)], 1u)] = k;
-        }
-        __syncthreads();
 
+    auto stage = [&](int b) {  // cp.async the bucket's keys (aligned superset) into keys_in
+        if (b >= nbuckets) return;
+        const unsigned lo = base[b], hi = base[b + 1];
+        if (hi - lo > (unsigned)kKeyCap) return;
+        const unsigned a0 = lo & ~3u, a1 = (hi + 3u) & ~3u;  // `sorted` is padded by 16 keys
+        for (unsigned q = threadIdx.x; q < (a1 - a0) / 4; q += blockDim.x)
+            cp_async16(&keys_in[4 * q], &sorted[a0 + 4 * q]);
+        cp_async_commit();
+    };
+    auto slab_pass = [&](int b, const unsigned* keys, bool keys_on_chip) {
+        // keys[sub_start[s] .. + sub_n[s]) hold slab s's keys (shared or global memory)
         for (int s = 0; s < kSubSlabs; ++s) {
             const unsigned long long cell0 =
                 ((unsigned long long)b << kBucketShift) + ((unsigned long long)s << kSlabShift);
             if (cell0 >= cells) break;
             const unsigned ncell =
                 (unsigned)(cells - cell0 < (unsigned long long)kSlabCells ? cells - cell0 : kSlabCells);
-            unsigned* cnt = cbuf[flip];
+            unsigned* cnt = cbuf0 + flip * kSlabCells;
             // the bulk store issued two slabs ago read this buffer: wait for it
             if (threadIdx.x == 0) bulk_wait_read_le1();
             __syncthreads();
             uint4* cnt4 = reinterpret_cast<uint4*>(cnt);
             for (int q = threadIdx.x; q < kSlabCells / 4; q += blockDim.x) cnt4[q] = make_uint4(0u, 0u, 0u, 0u);
             __syncthreads();
-            const unsigned s0 = lo + sub_start[s], s1 = s0 + sub_n[s];
+            const unsigned s0 = sub_start[s], s1 = s0 + sub_n[s];
             for (unsigned i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
-                const unsigned old = atomicAdd(&cnt[scratch[i] & (kSlabCells - 1)], 1u);  // Alg. 1
+                const unsigned old = atomicAdd(&cnt[keys[i] & (kSlabCells - 1)], 1u);  // Alg. 1
                 acc += old;
                 first += old == 0u;
                 ovf |= old >= 0xfffffffeu;
             }
+            (void)keys_on_chip;
             fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk copy
             __syncthreads();
             const unsigned vec_bytes = (ncell * 4u) & ~15u;
             if (threadIdx.x == 0 && vec_bytes) bulk_store_s2g(grid + cell0, cnt, vec_bytes);
             for (unsigned q = vec_bytes / 4 + threadIdx.x; q < ncell; q += blockDim.x) grid[cell0 + q] = cnt[q];
             flip ^= 1;
+        }
+    };
+
+    if (ok) stage(blockIdx.x);
+    for (int b = blockIdx.x; ok && b < nbuckets; b += gridDim.x) {
+        const unsigned lo = base[b], hi = base[b + 1];
+        const bool on_chip = hi - lo <= (unsigned)kKeyCap;
+        if (threadIdx.x < kSubSlabs) sub_n[threadIdx.x] = 0u;
+        cp_async_wait<0>();
+        __syncthreads();
+        if (on_chip) {
+            // counting sort by slab, shared memory -> shared memory
+            const unsigned* kin = keys_in + (lo & 3u);
+            const unsigned cnt_b = hi - lo;
+            for (unsigned i = threadIdx.x; i < cnt_b; i += blockDim.x)
+                atomicAdd(&sub_n[(kin[i] >> kSlabShift) & (kSubSlabs - 1)], 1u);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned run = 0;
+                for (int s = 0; s < kSubSlabs; ++s) {
+                    sub_start[s] = run;
+                    sub_cur[s] = run;
+                    run += sub_n[s];
+                }
+            }
+            __syncthreads();
+            for (unsigned i = threadIdx.x; i < cnt_b; i += blockDim.x) {
+                const unsigned k = kin[i];
+                keys_s[atomicAdd(&sub_cur[(k >> kSlabShift) & (kSubSlabs - 1)], 1u)] = k;
+            }
+            __syncthreads();
+            stage(b + gridDim.x);  // keys_in is free again: prefetch the next bucket under this one's slabs
+            slab_pass(b, keys_s, true);
+        } else {
+            // oversized bucket: sub-partition through global scratch
+            for (unsigned i = lo + threadIdx.x; i < hi; i += blockDim.x)
+                atomicAdd(&sub_n[(sorted[i] >> kSlabShift) & (kSubSlabs - 1)], 1u);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned run = lo;
+                for (int s = 0; s < kSubSlabs; ++s) {
+                    sub_start[s] = run;
+                    sub_cur[s] = run;
+                    run += sub_n[s];
+                }
+            }
+            __syncthreads();
+            for (unsigned i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+                const unsigned k = sorted[i];
+                scratch[atomicAdd(&sub_cur[(k >> kSlabShift) & (kSubSlabs - 1)], 1u)] = k;
+            }
+            __syncthreads();
+            stage(b + gridDim.x);
+            slab_pass(b, scratch, false);
         }
     }
     if (threadIdx.x == 0) bulk_wait_all();

@@ -912,7 +912,7 @@ int lattice_run(const void* xyz_in, int dtype, int on_device, long long n, long 
     const bool slab = clean && !contacts && sizeof(KT) == 4 && (unsigned long long)n * 64 > cells &&
                       n < (1LL << 32) - 1;
     const int nbuckets = (int)((cells + (1ull << kBucketShift) - 1) >> kBucketShift);
-    const size_t kbytes = align_up((size_t)n * 4, 256);
+    const size_t kbytes = align_up((size_t)n * 4 + 64, 256);  // +16 keys: aligned staging windows may overrun
     const size_t extra = slab ? 2 * kbytes + 3 * align_up((kMaxBuckets + 1) * 4, 256) +
                                     align_up((size_t)nbuckets * sizeof(LatSlot), 256)
                               : 0;
@@ -932,6 +932,8 @@ int lattice_run(const void* xyz_in, int dtype, int on_device, long long n, long 
         CK(cudaGetDevice(&dev));
         if (!attr_set[dev & 63]) {
             CK(cudaFuncSetAttribute(lat_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSlabSmem));
+            CK(cudaFuncSetAttribute(lat_bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    2 * kMaxBuckets * 4));
             attr_set[dev & 63] = true;
         }
         CK(cudaMemsetAsync(hist, 0, nbuckets * 4, s));
