@@ -10,8 +10,9 @@
 //   K1 lat_keys_hist_kernel   validate, write each bead's key (the touched
 //                             list), histogram keys by 128K-cell bucket
 //   K2 lat_bucket_scan_kernel exclusive scan of the bucket histogram
-//   K3 lat_bucket_scatter_kernel  partition keys by bucket (tile-local ranks
-//                             + one global reservation per tile and bucket)
+//   K3 lat_partition_{coarse,fine}_kernel  two-level partition of the keys
+//                             by bucket; tiles sorted on chip, runs written
+//                             contiguously
 //   K4 lat_slab_kernel        persistent, one CTA per SM, buckets round-robin:
 //                             stage a bucket's keys on chip, counting-sort them
 //                             into 16 slabs of 8K cells, then per slab zero a
@@ -90,52 +91,126 @@ __global__ void lat_bucket_scan_kernel(const unsigned* __restrict__ hist, unsign
     if (threadIdx.x == 1023) base[nbuckets] = s_part[1023];
 }
 
-// Partition keys by bucket.  Order inside a bucket is irrelevant (a histogram
-// does not care), so ranks come from shared-memory atomics and each tile
-// reserves its bucket ranges with one global atomic per (tile, bucket).
-// 512 threads x 8 keys (two 16-byte loads) per tile.  (A 32K-key tile with a
-// second pass was slower: the scattered 4-byte stores, not the reservations,
-// bound this kernel -- ~0.6 ms for 2^26 keys.)
-__global__ void __launch_bounds__(512) lat_bucket_scatter_kernel(const unsigned* __restrict__ keys, long long n,
-                                                                 unsigned* __restrict__ cursor,
-                                                                 unsigned* __restrict__ out, int nbuckets,
-                                                                 const unsigned long long* __restrict__ bad) {
-    if (*bad != kNoBad) return;
-    extern __shared__ unsigned sm[];
-    unsigned* h = sm;               // [nbuckets] tile histogram
-    unsigned* off = sm + nbuckets;  // [nbuckets] reserved global offsets
-    constexpr int kPer = 8;
-    const long long tile = (long long)blockDim.x * kPer;
-    const bool vec = (reinterpret_cast<uintptr_t>(keys) & 15) == 0;
-    for (long long t0 = (long long)blockIdx.x * tile; t0 < n; t0 += (long long)gridDim.x * tile) {
-        for (int b = threadIdx.x; b < nbuckets; b += blockDim.x) h[b] = 0u;
-        __syncthreads();
-        unsigned k[kPer], rank[kPer];
-        const long long i0 = t0 + 4LL * threadIdx.x;                 // keys i0..i0+3
-        const long long i1 = t0 + 4LL * (threadIdx.x + blockDim.x);  // keys i1..i1+3
-        if (vec && i1 + 3 < n) {
-            const uint4 a4 = reinterpret_cast<const uint4*>(keys + i0)[0];
-            const uint4 b4 = reinterpret_cast<const uint4*>(keys + i1)[0];
-            k[0] = a4.x; k[1] = a4.y; k[2] = a4.z; k[3] = a4.w;
-            k[4] = b4.x; k[5] = b4.y; k[6] = b4.z; k[7] = b4.w;
+// ---- two-level partition of the keys by bucket (coarse = key >> 24, then the
+// 128 fine buckets inside each coarse one).  Order inside a bucket is
+// irrelevant (a histogram does not care), so each tile is sorted locally in
+// shared memory with warp-aggregated ranks and then written out as contiguous
+// per-bucket runs.  (A one-pass partition into ~8K buckets stored every key
+// separately and was bound by L2 store transactions: 0.7 ms for 2^26 keys.)
+constexpr int kCoarseShift = 24;
+constexpr int kFinePerCoarse = 1 << (kCoarseShift - kBucketShift);  // 128
+constexpr int kPartThreads = 512;
+constexpr int kPartPer = 8;                          // keys per thread per tile
+constexpr int kPartTile = kPartThreads * kPartPer;   // 4096 keys
+constexpr int kMaxCoarse = kMaxBuckets / kFinePerCoarse;
+
+// coarse cursors/bases and the per-coarse-bucket tile table for the fine pass
+__global__ void lat_coarse_kernel(const unsigned* __restrict__ base, int nbuckets, int ncoarse,
+                                  unsigned* __restrict__ ccur, unsigned* __restrict__ cbase,
+                                  unsigned* __restrict__ tbase) {
+    if (threadIdx.x != 0) return;
+    unsigned tiles = 0;
+    for (int c = 0; c < ncoarse; ++c) {
+        const unsigned lo = base[min(c * kFinePerCoarse, nbuckets)];
+        const unsigned hi = base[min((c + 1) * kFinePerCoarse, nbuckets)];
+        cbase[c] = lo;
+        ccur[c] = lo;
+        tbase[c] = tiles;
+        tiles += (hi - lo + kPartTile - 1) / kPartTile;
+    }
+    cbase[ncoarse] = base[nbuckets];
+    tbase[ncoarse] = tiles;
+}
+
+// Sort one tile [t0, t1) of `in` by digit(key) on chip and append each digit's
+// run at cursor[cur_base + digit] of `out`.
+template <typename DigitFn>
+__device__ void partition_tile(const unsigned* __restrict__ in, long long t0, long long t1,
+                               unsigned* __restrict__ cursor, int cur_base, int ndig, DigitFn digit,
+                               unsigned* __restrict__ out, unsigned* buf, unsigned* h, unsigned* lofs,
+                               unsigned* goff) {
+    const int lane = threadIdx.x & 31;
+    for (int d = threadIdx.x; d < ndig; d += blockDim.x) h[d] = 0u;
+    __syncthreads();
+    unsigned k[kPartPer], rank[kPartPer];
+    const bool vec = (reinterpret_cast<uintptr_t>(in + t0) & 15) == 0;  // fine-pass tiles start anywhere
+#pragma unroll
+    for (int q = 0; q < kPartPer / 4; ++q) {
+        const long long i = t0 + 4LL * (q * kPartThreads + threadIdx.x);
+        if (vec && i + 3 < t1) {
+            const uint4 v = *reinterpret_cast<const uint4*>(in + i);
+            k[4 * q] = v.x; k[4 * q + 1] = v.y; k[4 * q + 2] = v.z; k[4 * q + 3] = v.w;
         } else {
 #pragma unroll
-            for (int u = 0; u < kPer; ++u) {
-                const long long i = (u < 4 ? i0 : i1) + (u & 3);
-                k[u] = i < n ? keys[i] : 0xffffffffu;
-            }
+            for (int u = 0; u < 4; ++u) k[4 * q + u] = i + u < t1 ? in[i + u] : 0xffffffffu;
         }
+    }
 #pragma unroll
-        for (int u = 0; u < kPer; ++u)
-            rank[u] = k[u] != 0xffffffffu ? atomicAdd(&h[k[u] >> kBucketShift], 1u) : 0u;
-        __syncthreads();
-        for (int b = threadIdx.x; b < nbuckets; b += blockDim.x)
-            if (h[b]) off[b] = atomicAdd(&cursor[b], h[b]);
-        __syncthreads();
+    for (int u = 0; u < kPartPer; ++u) rank[u] = k[u] != 0xffffffffu ? atomicAdd(&h[digit(k[u])], 1u) : 0u;
+    __syncthreads();
+    // block-wide exclusive scan of h (ndig <= kPartThreads) and parallel run reservations
+    __shared__ unsigned s_wsum[kPartThreads / 32];
+    const int d = threadIdx.x;
+    const unsigned v = d < ndig ? h[d] : 0u;
+    unsigned x = v;
 #pragma unroll
-        for (int u = 0; u < kPer; ++u)
-            if (k[u] != 0xffffffffu) out[off[k[u] >> kBucketShift] + rank[u]] = k[u];
-        __syncthreads();
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[threadIdx.x >> 5] = x;
+    __syncthreads();
+    unsigned before = 0;
+    for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) before += s_wsum[w];
+    if (d < ndig) {
+        lofs[d] = before + x - v;
+        goff[d] = v ? atomicAdd(&cursor[cur_base + d], v) : 0u;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kPartPer; ++u)
+        if (k[u] != 0xffffffffu) buf[lofs[digit(k[u])] + rank[u]] = k[u];
+    __syncthreads();
+    const int cnt = (int)(t1 - t0);
+    for (int p = threadIdx.x; p < cnt; p += blockDim.x) {
+        const unsigned key = buf[p], d = digit(key);
+        out[goff[d] + (p - lofs[d])] = key;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kPartThreads, 2) lat_partition_coarse_kernel(
+    const unsigned* __restrict__ keys, long long n, unsigned* __restrict__ ccur, int ncoarse,
+    unsigned* __restrict__ out, const unsigned long long* __restrict__ bad) {
+    if (*bad != kNoBad) return;
+    __shared__ unsigned buf[kPartTile];
+    __shared__ unsigned h[kMaxCoarse], lofs[kMaxCoarse], goff[kMaxCoarse];
+    for (long long t0 = (long long)blockIdx.x * kPartTile; t0 < n; t0 += (long long)gridDim.x * kPartTile)
+        partition_tile(keys, t0, t0 + kPartTile < n ? t0 + kPartTile : n, ccur, 0, ncoarse,
+                       [](unsigned key) { return key >> kCoarseShift; }, out, buf, h, lofs, goff);
+}
+
+__global__ void __launch_bounds__(kPartThreads, 2) lat_partition_fine_kernel(
+    const unsigned* __restrict__ tmp, const unsigned* __restrict__ cbase, const unsigned* __restrict__ tbase,
+    int ncoarse, unsigned* __restrict__ fcur, unsigned* __restrict__ out,
+    const unsigned long long* __restrict__ bad) {
+    if (*bad != kNoBad) return;
+    __shared__ unsigned buf[kPartTile];
+    __shared__ unsigned h[kFinePerCoarse], lofs[kFinePerCoarse], goff[kFinePerCoarse];
+    const unsigned ntiles = tbase[ncoarse];
+    for (unsigned g = blockIdx.x; g < ntiles; g += gridDim.x) {
+        int c = 0;  // coarse bucket holding tile g (tbase is non-decreasing; <= 128 entries)
+        for (int lo = 0, hi = ncoarse; lo < hi;) {
+            const int mid = (lo + hi) >> 1;
+            if (tbase[mid + 1] <= g) lo = mid + 1;
+            else hi = mid;
+            c = lo;
+        }
+        const long long t0 = (long long)cbase[c] + (long long)(g - tbase[c]) * kPartTile;
+        const long long t1 = t0 + kPartTile < (long long)cbase[c + 1] ? t0 + kPartTile : (long long)cbase[c + 1];
+        partition_tile(tmp, t0, t1, fcur, c * kFinePerCoarse, kFinePerCoarse,
+                       [](unsigned key) { return (key >> kBucketShift) & (kFinePerCoarse - 1); }, out, buf, h,
+                       lofs, goff);
     }
 }
 

@@ -913,8 +913,8 @@ int lattice_run(const void* xyz_in, int dtype, int on_device, long long n, long 
                       n < (1LL << 32) - 1;
     const int nbuckets = (int)((cells + (1ull << kBucketShift) - 1) >> kBucketShift);
     const size_t kbytes = align_up((size_t)n * 4 + 64, 256);  // +16 keys: aligned staging windows may overrun
-    const size_t extra = slab ? 2 * kbytes + 3 * align_up((kMaxBuckets + 1) * 4, 256) +
-                                    align_up((size_t)nbuckets * sizeof(LatSlot), 256)
+    const size_t abytes = align_up((kMaxBuckets + 1) * 4, 256), cbytes4 = align_up((kMaxCoarse + 1) * 4, 256);
+    const size_t extra = slab ? 2 * kbytes + 3 * abytes + 3 * cbytes4 + align_up((size_t)nbuckets * sizeof(LatSlot), 256)
                               : 0;
     char* ex = nullptr;
     int rc = lat_prepare(xyz_in, dtype, on_device, n, &ar, &sc, &s, extra, &ex);
@@ -922,18 +922,20 @@ int lattice_run(const void* xyz_in, int dtype, int on_device, long long n, long 
     const int nb = sc.nslots;
     if (slab) {
         unsigned* sorted = (unsigned*)ex;
-        unsigned* scratch = (unsigned*)(ex + kbytes);
+        unsigned* scratch = (unsigned*)(ex + kbytes);  // coarse-partitioned keys, then the slab kernel's fallback
         unsigned* hist = (unsigned*)(ex + 2 * kbytes);
-        unsigned* base = hist + align_up((kMaxBuckets + 1) * 4, 256) / 4;
-        unsigned* cursor = base + align_up((kMaxBuckets + 1) * 4, 256) / 4;
-        LatSlot* bslots = (LatSlot*)(cursor + align_up((kMaxBuckets + 1) * 4, 256) / 4);
+        unsigned* base = (unsigned*)((char*)hist + abytes);
+        unsigned* cursor = (unsigned*)((char*)base + abytes);
+        unsigned* ccur = (unsigned*)((char*)cursor + abytes);
+        unsigned* cbase = (unsigned*)((char*)ccur + cbytes4);
+        unsigned* tbase = (unsigned*)((char*)cbase + cbytes4);
+        LatSlot* bslots = (LatSlot*)((char*)tbase + cbytes4);
+        const int ncoarse = (int)(((cells - 1) >> kCoarseShift) + 1);
         static thread_local bool attr_set[64] = {false};
         int dev = 0;
         CK(cudaGetDevice(&dev));
         if (!attr_set[dev & 63]) {
             CK(cudaFuncSetAttribute(lat_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSlabSmem));
-            CK(cudaFuncSetAttribute(lat_bucket_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    2 * kMaxBuckets * 4));
             attr_set[dev & 63] = true;
         }
         CK(cudaMemsetAsync(hist, 0, nbuckets * 4, s));
@@ -942,9 +944,14 @@ int lattice_run(const void* xyz_in, int dtype, int on_device, long long n, long 
         CK_LAUNCH("lat_keys_hist_kernel");
         lat_bucket_scan_kernel<<<1, 1024, 0, s>>>(hist, base, cursor, nbuckets);
         CK_LAUNCH("lat_bucket_scan_kernel");
-        lat_bucket_scatter_kernel<<<num_sms() * 3, 512, 2 * nbuckets * 4, s>>>((const unsigned*)keys, n, cursor,
-                                                                              sorted, nbuckets, sc.bad);
-        CK_LAUNCH("lat_bucket_scatter_kernel");
+        lat_coarse_kernel<<<1, 32, 0, s>>>(base, nbuckets, ncoarse, ccur, cbase, tbase);
+        CK_LAUNCH("lat_coarse_kernel");
+        lat_partition_coarse_kernel<<<num_sms() * 2, kPartThreads, 0, s>>>((const unsigned*)keys, n, ccur, ncoarse,
+                                                                          scratch, sc.bad);
+        CK_LAUNCH("lat_partition_coarse_kernel");
+        lat_partition_fine_kernel<<<num_sms() * 2, kPartThreads, 0, s>>>(scratch, cbase, tbase, ncoarse, cursor,
+                                                                        sorted, sc.bad);
+        CK_LAUNCH("lat_partition_fine_kernel");
         const int sgrid = std::min(num_sms(), nbuckets);
         lat_slab_kernel<<<sgrid, 1024, kSlabSmem, s>>>(sorted, scratch, base, nbuckets, grid, cells, sc.bad, bslots,
                                                        sc.overflow);
