@@ -41,7 +41,33 @@ __global__ void lat_keys_hist_kernel(const void* __restrict__ xyz, int dtype, lo
     extern __shared__ unsigned h_s[];
     for (int b = threadIdx.x; b < nbuckets; b += blockDim.x) h_s[b] = 0u;
     __syncthreads();
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+    long long i_scalar = 0;
+    if (dtype == PC_I32 && (reinterpret_cast<uintptr_t>(xyz) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(keys) & 15) == 0) {
+        // four beads (48 B of int32 coordinates) per thread: three 16-byte loads, one 16-byte key store
+        const int4* src = reinterpret_cast<const int4*>(xyz);
+        const long long groups = n / 4;
+        for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < groups;
+             g += (long long)gridDim.x * blockDim.x) {
+            const int4 p0 = src[3 * g], p1 = src[3 * g + 1], p2 = src[3 * g + 2];
+            const int c[12] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w, p2.x, p2.y, p2.z, p2.w};
+            unsigned kk[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const long long x = c[3 * u], y = c[3 * u + 1], z = c[3 * u + 2];
+                if (x < -a || x > a || y < -a || y > a || z < -a || z > a) {
+                    atomicMin(bad, (unsigned long long)(4 * g + u));
+                    kk[u] = 0u;
+                } else {
+                    kk[u] = (unsigned)(((x + a + 1) * side + (y + a + 1)) * side + (z + a + 1));
+                    atomicAdd(&h_s[kk[u] >> kBucketShift], 1u);
+                }
+            }
+            reinterpret_cast<uint4*>(keys)[g] = make_uint4(kk[0], kk[1], kk[2], kk[3]);
+        }
+        i_scalar = groups * 4;
+    }
+    for (long long i = i_scalar + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const long long x = coord_i64(xyz, dtype, i, 0), y = coord_i64(xyz, dtype, i, 1),
                         z = coord_i64(xyz, dtype, i, 2);

@@ -936,10 +936,12 @@ int lattice_run(const void* xyz_in, int dtype, int on_device, long long n, long 
         CK(cudaGetDevice(&dev));
         if (!attr_set[dev & 63]) {
             CK(cudaFuncSetAttribute(lat_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSlabSmem));
+            CK(cudaFuncSetAttribute(lat_keys_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kMaxBuckets * 4));
             attr_set[dev & 63] = true;
         }
         CK(cudaMemsetAsync(hist, 0, nbuckets * 4, s));
-        lat_keys_hist_kernel<<<nb, 256, nbuckets * 4, s>>>(sc.xyz, dtype, n, a, side, (unsigned*)keys, sc.bad, hist,
+        lat_keys_hist_kernel<<<2 * num_sms(), 1024, nbuckets * 4, s>>>(sc.xyz, dtype, n, a, side, (unsigned*)keys, sc.bad, hist,
                                                            nbuckets);
         CK_LAUNCH("lat_keys_hist_kernel");
         lat_bucket_scan_kernel<<<1, 1024, 0, s>>>(hist, base, cursor, nbuckets);
