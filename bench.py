@@ -47,6 +47,9 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-secondary", action="store_true", help="skip the config-2/5 side measurements")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                   help="gloo only to exercise the N>1 path with several ranks on one GPU (timings meaningless)")
+    p.add_argument("--shared-gpu", action="store_true", help="all ranks use cuda:0 (with --dist-backend gloo)")
     p.add_argument("--cpu-rows-per-core", type=int, default=160)
     p.add_argument("--ref-rows-per-core", type=int, default=32, help="reference arm: rows per core per step")
     return p.parse_args()
@@ -320,10 +323,15 @@ def run_ours(args):
     from paper_1901_11204_b200.distributed import row_slabs
 
     rank, world, local = dist_env()
+    if args.shared_gpu:
+        local = 0
     torch.cuda.set_device(local)
     os.environ["PAIRCOUNT_DEVICE"] = str(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     lib = _lib.load()
     stream = torch.cuda.current_stream()
 

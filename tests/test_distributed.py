@@ -91,3 +91,50 @@ def test_pack_roundtrip():
     s = D.pack_partial(12345, 0.1 + 0.2, 1, 3)
     counts, sums = D.unpack_partials(s, 3)
     assert counts == [0, 12345, 0] and sums[1] == 0.1 + 0.2 and sums[0] == 0.0
+
+
+def _gpu_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1901_11204_b200 import generators as gen
+        from paper_1901_11204_b200 import spi_engine as se
+
+        objs = gen.random_spheres(50_001, 30.0, 3).astype(np.float32)
+        out = {}
+        for sched in ("balanced", "standard"):
+            out[sched] = (D.spi_distributed(objs, se.collision_indicator, sched),
+                          D.spi_distributed(objs, se.inverse_square, sched))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_ranks_real_kernels_gloo():
+    """The N>1 path with the real kernels: 2 processes (gloo) share cuda:0, each
+    runs its row slab; the partials meet in the one all-reduce.  (Kernels of
+    different ranks never wait on each other, so sharing a GPU is safe.)"""
+    from oracle import c_oracle
+    from paper_1901_11204_b200 import generators as gen
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    objs = gen.random_spheres(50_001, 30.0, 3).astype(np.float32)
+    for sched in ("balanced", "standard"):
+        want_c, want_s, _ = c_oracle.rows(objs, 0, len(objs), sched)
+        (tc, parts, pairs), (ts, _, _) = results[0][sched]
+        assert tc == want_c and ts == pytest.approx(want_s, rel=1e-5)
+        for (lo, hi), part in zip(D.row_slabs(len(objs), world, sched), parts):
+            assert part == c_oracle.rows(objs, lo, hi, sched)[0]
+        assert results[1][sched][0] == results[0][sched][0]
