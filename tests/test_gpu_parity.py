@@ -337,3 +337,25 @@ def test_row_range_api_edges():
             assert (got, pairs) == (c, p)
     with pytest.raises(ValueError):
         se.spi_rows(objs, se.collision_indicator, (10, 5), "balanced")
+
+
+@pytest.mark.parametrize("trial", range(12))
+def test_boundary_stress_random_offsets(trial):
+    """Pairs planted at |d|^2 = 1 +- O(1e-7) inside clouds of random offset and
+    span (the Gram filter's error grows with the span; its band must too)."""
+    rng = np.random.default_rng(100 + trial)
+    offset = rng.choice([0.0, 1.0, 37.5, 1e3, 2.5e4, 1e6]) * rng.choice([-1, 1])
+    span = rng.choice([2.0, 50.0, 400.0, 3000.0])
+    n_bg, n_pair = int(rng.integers(500, 6000)), 400
+    bg = offset + rng.random((n_bg, 3)) * span
+    a = offset + rng.random((n_pair, 3)) * span
+    d = rng.normal(size=(n_pair, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    b = a + d * (1.0 + rng.normal(scale=2e-7, size=(n_pair, 1)))
+    pts = np.concatenate([bg, a, b])
+    rng.shuffle(pts)
+    for arr in (pts, pts.astype(np.float32)):
+        want_c, want_s, _ = c_oracle.rows(arr, 0, len(arr), "balanced")
+        assert se.spi_balanced(arr, se.collision_indicator).total == want_c
+        (r,) = _lib.pairs_host(np.ascontiguousarray(arr), _lib.PC_COLLISION_INVSQ, _lib.PC_STANDARD, [0, len(arr)])
+        assert r.count == want_c and _close(r.sum, want_s)
