@@ -214,6 +214,43 @@ def secondary(torch, lib, stream):
     out["cfg2_naive_vs_balanced_n65536"] = rows
     del d2, ws
 
+    # ---- config 3, count only: the metric's "collision-count wall time at N=2^20"
+    from paper_1901_11204_b200 import spi_engine as se
+
+    n3 = 2**20
+    obj3 = workload_input()
+    d3 = torch.from_numpy(obj3).cuda()
+    ws3 = torch.empty(_lib.workspace_bytes(n3), dtype=torch.uint8, device="cuda")
+    pairs3 = n3 * (n3 - 1) // 2
+    for _ in range(2):
+        _lib.pairs_async(d3.data_ptr(), _lib.PC_F32, n3, _lib.PC_COLLISION, _lib.PC_BALANCED, np.array([0, n3]),
+                         ws3.data_ptr(), ws3.numel(), res.data_ptr(), stream.cuda_stream, _lib.PC_TILE_FLAT)
+    torch.cuda.synchronize()
+    _lib.kernel_timing(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    e0.record(stream)
+    for _ in range(reps):
+        _lib.pairs_async(d3.data_ptr(), _lib.PC_F32, n3, _lib.PC_COLLISION, _lib.PC_BALANCED, np.array([0, n3]),
+                         ws3.data_ptr(), ws3.numel(), res.data_ptr(), stream.cuda_stream, _lib.PC_TILE_FLAT)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_k, cnt_k = _lib.kernel_timing_read()
+    _lib.kernel_timing(False)
+    dev_ms = e0.elapsed_time(e1) / reps
+    t0 = time.perf_counter()
+    r3 = se.spi_balanced(obj3, se.collision_indicator)
+    api_ms = (time.perf_counter() - t0) * 1e3
+    out["cfg3_collision_count_n2^20"] = {
+        "count": int(res[0].item()), "api_count": int(r3.total),
+        "kernel_ms": ms_k / cnt_k, "device_ms_per_call": dev_ms,
+        "Gpair_per_s_kernel": pairs3 / (ms_k / cnt_k * 1e-3) / 1e9,
+        "api_wall_ms": api_ms,
+        "api_path": "spi_balanced(points, collision_indicator): numpy (n,3) f32 -> ctypes pc_pairs_host "
+                    "(H2D, prep, Gram-filter kernel, finalize, D2H) -> SpiResult",
+        "kernel": "pairs_kernel<128,12,256,GRAM,FLAT>"}
+    del d3, ws3
+
     # ---- config 5: counting array, device-resident int32 coordinates
     n5, a5 = 2**26, 512
     pts = gen.grid_points(n5, a5)
