@@ -175,6 +175,15 @@ int pc_lattice_reset_keys(uint32_t* grid, int64_t half_extent, const void* keys,
  * a vector longer than 4096 beads, which the caller counts through a grid. */
 int pc_lattice_collisions_batch(const void* xyz, int32_t dtype, int32_t xyz_on_device, const int64_t* offsets,
                                 int32_t nvec, int64_t half_extent, pc_lattice_result* results, void* stream);
+/* Same as pc_lattice_collisions_batch for nvec separate HOST vectors
+ * (vectors[v] -> lengths[v] beads of (x,y,z), int32 or int64), as the
+ * reference's _linear_pass holds them (bench_cli.py:129-141): the library
+ * gathers them with host threads into pinned staging, narrowing int64 to
+ * int32 (a coordinate outside [-a,a] maps to INT32_MAX, still out of range,
+ * so PC_ERR_RANGE names the same first bad bead), then one H2D copy and one
+ * launch.  half_extent < INT32_MAX. */
+int pc_lattice_collisions_vectors(const void* const* vectors, const int64_t* lengths, int32_t dtype, int32_t nvec,
+                                  int64_t half_extent, pc_lattice_result* results, void* stream);
 
 /* Zero the whole grid with one streaming write (cudaMemsetAsync).  The
  * Python reset_sparse uses it in place of pc_lattice_reset_keys when the

@@ -47,6 +47,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -1236,33 +1237,18 @@ int pc_lattice_reset_keys(uint32_t* grid, int64_t half_extent, const void* keys,
     return PC_OK;
 }
 
-int pc_lattice_collisions_batch(const void* xyz, int32_t dtype, int32_t xyz_on_device, const int64_t* offsets,
-                                int32_t nvec, int64_t half_extent, pc_lattice_result* results, void* stream) {
-    g_launches = 0;
-    if (nvec < 0 || !offsets) return arg_fail("bad vector offsets");
-    if (half_extent < 0) return arg_fail("half_extent must be >= 0");
-    if (dtype != PC_I32 && dtype != PC_I64) return arg_fail("lattice beads must be int32 or int64");
-    for (int v = 0; v < nvec; ++v)
-        if (offsets[v] < 0 || offsets[v] > offsets[v + 1]) return arg_fail("vector offsets must be non-decreasing");
-    if (nvec == 0) return PC_OK;
-    const long long n = offsets[nvec];
-    const size_t cbytes = xyz_on_device ? 0 : align_up((size_t)n * 3 * dtype_bytes(dtype), 256);
-    const size_t obytes = align_up((size_t)(nvec + 1) * 8, 256), rbytes = align_up((size_t)nvec * 24, 256);
-    cudaStream_t s = (cudaStream_t)stream;
+}  // extern "C" (reopened below)
+
+namespace {
+// One lat_batch_kernel launch over device beads + host offsets; fills results.
+// Caller holds the device arena lock; `base` is arena memory past the beads.
+int lat_batch_run(const void* dxyz, int32_t dtype, const int64_t* offsets, int32_t nvec, int64_t half_extent,
+                  char* base, pc_lattice_result* results, cudaStream_t s) {
     int dev = 0;
     CK(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lock(g_arena[dev & 63].mu);
-    Arena* ar = nullptr;
-    int rc = arena_get(cbytes + obytes + rbytes, &ar);
-    if (rc) return rc;
-    char* base = (char*)ar->dev;
-    const void* dxyz = xyz;
-    if (!xyz_on_device) {
-        if (n > 0) CK(cudaMemcpyAsync(base, xyz, (size_t)n * 3 * dtype_bytes(dtype), cudaMemcpyHostToDevice, s));
-        dxyz = base;
-    }
-    long long* doffs = (long long*)(base + cbytes);
-    unsigned long long* dout = (unsigned long long*)(base + cbytes + obytes);
+    const size_t obytes = align_up((size_t)(nvec + 1) * 8, 256);
+    long long* doffs = (long long*)base;
+    unsigned long long* dout = (unsigned long long*)(base + obytes);
     CK(cudaMemcpyAsync(doffs, offsets, (size_t)(nvec + 1) * 8, cudaMemcpyHostToDevice, s));
     static thread_local bool attr_set[64] = {false};
     if (!attr_set[dev & 63]) {
@@ -1291,6 +1277,129 @@ int pc_lattice_collisions_batch(const void* xyz, int32_t dtype, int32_t xyz_on_d
         }
     }
     return PC_OK;
+}
+
+size_t batch_tail_bytes(int32_t nvec) {
+    return align_up((size_t)(nvec + 1) * 8, 256) + align_up((size_t)nvec * 24, 256);
+}
+
+// Pinned host staging for pc_lattice_collisions_vectors (per device, guarded by the arena lock).
+struct Pinned {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+Pinned g_pinned[64];
+
+int pinned_get(int dev, size_t bytes, void** out) {
+    Pinned& pn = g_pinned[dev & 63];
+    if (pn.cap < bytes) {
+        if (pn.p) CK(cudaFreeHost(pn.p));
+        pn.p = nullptr;
+        pn.cap = 0;
+        const size_t want = align_up(bytes + bytes / 4, 1 << 20);
+        CK(cudaHostAlloc(&pn.p, want, cudaHostAllocDefault));
+        pn.cap = want;
+    }
+    *out = pn.p;
+    return PC_OK;
+}
+
+// Gather vectors [v0, v1) into dst as int32, mapping any coordinate outside
+// [-a, a] to INT32_MAX (itself outside [-a, a], so the kernel still reports
+// the first bad bead of that vector -- narrowing can never wrap a bad bead
+// into range).
+void gather_narrow(const void* const* vecs, const int64_t* offs, int32_t dtype, int64_t a, int v0, int v1,
+                   int32_t* dst) {
+    for (int v = v0; v < v1; ++v) {
+        const long long m = 3 * (offs[v + 1] - offs[v]);
+        int32_t* d = dst + 3 * offs[v];
+        if (dtype == PC_I32) {
+            memcpy(d, vecs[v], (size_t)m * 4);
+        } else {
+            const long long* src = (const long long*)vecs[v];
+            for (long long k = 0; k < m; ++k) {
+                const long long x = src[k];
+                d[k] = (x < -a || x > a) ? INT32_MAX : (int32_t)x;
+            }
+        }
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int pc_lattice_collisions_batch(const void* xyz, int32_t dtype, int32_t xyz_on_device, const int64_t* offsets,
+                                int32_t nvec, int64_t half_extent, pc_lattice_result* results, void* stream) {
+    g_launches = 0;
+    if (nvec < 0 || !offsets) return arg_fail("bad vector offsets");
+    if (half_extent < 0) return arg_fail("half_extent must be >= 0");
+    if (dtype != PC_I32 && dtype != PC_I64) return arg_fail("lattice beads must be int32 or int64");
+    for (int v = 0; v < nvec; ++v)
+        if (offsets[v] < 0 || offsets[v] > offsets[v + 1]) return arg_fail("vector offsets must be non-decreasing");
+    if (nvec == 0) return PC_OK;
+    const long long n = offsets[nvec];
+    const size_t cbytes = xyz_on_device ? 0 : align_up((size_t)n * 3 * dtype_bytes(dtype), 256);
+    cudaStream_t s = (cudaStream_t)stream;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_arena[dev & 63].mu);
+    Arena* ar = nullptr;
+    int rc = arena_get(cbytes + batch_tail_bytes(nvec), &ar);
+    if (rc) return rc;
+    char* base = (char*)ar->dev;
+    const void* dxyz = xyz;
+    if (!xyz_on_device) {
+        if (n > 0) CK(cudaMemcpyAsync(base, xyz, (size_t)n * 3 * dtype_bytes(dtype), cudaMemcpyHostToDevice, s));
+        dxyz = base;
+    }
+    return lat_batch_run(dxyz, dtype, offsets, nvec, half_extent, base + cbytes, results, s);
+}
+
+int pc_lattice_collisions_vectors(const void* const* vectors, const int64_t* lengths, int32_t dtype, int32_t nvec,
+                                  int64_t half_extent, pc_lattice_result* results, void* stream) {
+    g_launches = 0;
+    if (nvec < 0 || (nvec > 0 && (!vectors || !lengths))) return arg_fail("bad vector list");
+    if (half_extent < 0 || half_extent >= INT32_MAX) return arg_fail("half_extent out of range");
+    if (dtype != PC_I32 && dtype != PC_I64) return arg_fail("lattice beads must be int32 or int64");
+    if (nvec == 0) return PC_OK;
+    std::vector<int64_t> offs((size_t)nvec + 1, 0);
+    for (int v = 0; v < nvec; ++v) {
+        if (lengths[v] < 0) return arg_fail("vector lengths must be >= 0");
+        if (lengths[v] > 0 && !vectors[v]) return arg_fail("null vector pointer");
+        offs[v + 1] = offs[v] + lengths[v];
+    }
+    const long long n = offs[nvec];
+    const size_t bbytes = (size_t)n * 3 * 4, cbytes = align_up(bbytes, 256);
+    cudaStream_t s = (cudaStream_t)stream;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_arena[dev & 63].mu);
+    Arena* ar = nullptr;
+    int rc = arena_get(cbytes + batch_tail_bytes(nvec), &ar);
+    if (rc) return rc;
+    char* base = (char*)ar->dev;
+    if (n > 0) {
+        void* stage = nullptr;
+        rc = pinned_get(dev, bbytes, &stage);
+        if (rc) return rc;
+        // split the gather over host threads by bead count (1 thread below ~1 MB)
+        const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+        const int nt = (int)std::min<long long>(std::min(hw, 16), std::max(1LL, (long long)(bbytes >> 20)));
+        std::vector<std::thread> pool;
+        int v0 = 0;
+        for (int t = 0; t < nt; ++t) {
+            const long long goal = n * (t + 1) / nt;
+            int v1 = v0;
+            while (v1 < nvec && (t == nt - 1 || offs[v1] < goal)) ++v1;
+            if (t == nt - 1) v1 = nvec;
+            if (v1 > v0) pool.emplace_back(gather_narrow, vectors, offs.data(), dtype, (int64_t)half_extent, v0, v1,
+                                           (int32_t*)stage);
+            v0 = v1;
+        }
+        for (auto& th : pool) th.join();
+        CK(cudaMemcpyAsync(base, stage, bbytes, cudaMemcpyHostToDevice, s));
+    }
+    return lat_batch_run(base, PC_I32, offs.data(), nvec, half_extent, base + cbytes, results, s);
 }
 
 int pc_lattice_clear(uint32_t* grid, int64_t half_extent, void* stream) {

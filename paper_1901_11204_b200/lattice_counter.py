@@ -258,17 +258,14 @@ def count_collisions_batch(vectors, space: LatticeSpace) -> list[CountReport]:
     arrays = [np.ascontiguousarray(as_bead_array(v)) for v in vectors]
     if not arrays:
         return []
-    offsets = np.zeros(len(arrays) + 1, dtype=np.int64)
-    np.cumsum([len(a) for a in arrays], out=offsets[1:])
-    allb = np.concatenate(arrays) if offsets[-1] else np.zeros((0, 3), dtype=np.int64)
-    if len(allb) and np.abs(allb).max() < 2**31 - 1:
-        allb = allb.astype(np.int32)
-    allb = np.ascontiguousarray(allb)
+    # the library gathers the separate host vectors itself (threads, pinned
+    # staging, int64 -> int32 narrowing): no host-side concatenation
+    ptrs = np.array([a.__array_interface__["data"][0] for a in arrays], dtype=np.uintp)
+    lengths = np.array([len(a) for a in arrays], dtype=np.int64)
     res = (_lib.LatticeResult * len(arrays))()
     lib = _lib.load()
-    _lib.check(lib.pc_lattice_collisions_batch(allb.ctypes.data, _lib.DTYPE_CODES[allb.dtype], 0,
-                                               offsets.ctypes.data, len(arrays), space.half_extent,
-                                               ctypes.addressof(res), None))
+    _lib.check(lib.pc_lattice_collisions_vectors(ptrs.ctypes.data, lengths.ctypes.data, _lib.PC_I64, len(arrays),
+                                                 space.half_extent, ctypes.addressof(res), None))
     reports = []
     for arr, r in zip(arrays, res):
         if r.error == _lib.PC_ERR_RANGE:

@@ -310,6 +310,39 @@ def test_batched_small_vectors():
         assert (rep.count, rep.beads_processed, rep.cells_touched) == (want, len(v), ref.cells_touched)
     with pytest.raises(lc.CoordinateRangeError, match="bead 1"):
         pc.count_collisions_batch([[(0, 0, 0)], [(0, 0, 0), (ext + 1, 0, 0)]], sp)
+    # int64 coordinates that would wrap into range if narrowed naively
+    for bad in (2**32, 2**32 + 1, -(2**32), 2**62, -(2**63)):
+        with pytest.raises(lc.CoordinateRangeError, match="bead 2"):
+            pc.count_collisions_batch([[(0, 0, 0)], [(1, 1, 1), (0, 0, 0), (0, bad, 0)]], sp)
+    assert sp.is_zero()
+
+
+def test_batch_entry_points_agree():
+    # pc_lattice_collisions_vectors (separate host vectors, int32 and int64) ==
+    # pc_lattice_collisions_batch (one packed array + offsets)
+    import ctypes
+
+    lib = _lib.load()
+    vectors = [np.zeros((0, 3), dtype=np.int64)] + [gen.random_chain(n, 800 + n)[0] for n in (1, 5, 300, 2000, 4096, 4097)]
+    a = max(int(np.abs(v).max()) for v in vectors if len(v))
+    lengths = np.array([len(v) for v in vectors], dtype=np.int64)
+    offsets = np.concatenate([[0], np.cumsum(lengths)]).astype(np.int64)
+    packed = np.ascontiguousarray(np.concatenate(vectors))
+    want = (_lib.LatticeResult * len(vectors))()
+    _lib.check(lib.pc_lattice_collisions_batch(packed.ctypes.data, _lib.PC_I64, 0, offsets.ctypes.data,
+                                               len(vectors), a, ctypes.addressof(want), None))
+    for dt, code in ((np.int64, _lib.PC_I64), (np.int32, _lib.PC_I32)):
+        arrs = [np.ascontiguousarray(v.astype(dt)) for v in vectors]
+        ptrs = np.array([x.__array_interface__["data"][0] for x in arrs], dtype=np.uintp)
+        got = (_lib.LatticeResult * len(vectors))()
+        _lib.check(lib.pc_lattice_collisions_vectors(ptrs.ctypes.data, lengths.ctypes.data, code, len(vectors), a,
+                                                     ctypes.addressof(got), None))
+        for v, g, w in zip(vectors, got, want):
+            assert (g.count, g.cells_touched, g.error, g.beads_processed) == \
+                (w.count, w.cells_touched, w.error, w.beads_processed)
+            if len(v) and len(v) <= 4096:
+                assert g.error == 0 and g.count == c_oracle.int_pairs(v)[0]
+        assert got[-1].error == _lib.PC_ERR_ARG  # > 4096 beads: the caller routes it through the grid
 
 
 def test_filter_bypass_for_huge_spans():
