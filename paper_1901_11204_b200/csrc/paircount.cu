@@ -281,10 +281,29 @@ __device__ __forceinline__ float4 staged_point(const void* xyz, int dtype, long 
     return make_float4(q[0], q[1], q[2], DIRECT ? 0.0f : (float)(-0.5 * nq));
 }
 
+// Compensated staging (direct formula, non-f32 input): the centred coordinate
+// q = p - c (exact int64 difference for integer input) as the unevaluated
+// fp32 sum hi + lo, so pair separations survive however far the points sit
+// from the centre (fp32 rounding of q alone would cost u*|q| absolute).
+__device__ __forceinline__ void staged_point_comp(const void* xyz, int dtype, long long i, const double c[3],
+                                                  const long long ci[3], float h[3], float l[3]) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double q;
+        if (is_int_dtype(dtype))
+            q = (double)(long long)((unsigned long long)coord_i64(xyz, dtype, i, k) - (unsigned long long)ci[k]);
+        else
+            q = coord_f64(xyz, dtype, i, k) - c[k];
+        h[k] = (float)q;
+        l[k] = (float)(q - (double)h[k]);
+    }
+}
+
 // Pair arrays for packed FP32: entry j>>1 of `even` (j even) / `odd` (j odd)
 // holds points j and (j+1) mod n interleaved as (x_j, x_j1, y_j, y_j1),
-// (z_j, z_j1, w_j, w_j1).  Thread per j; every point is staged twice.
-template <bool DIRECT>
+// (z_j, z_j1, w_j, w_j1) -- or, COMP, (xh, xh1, yh, yh1)(zh, zh1, xl, xl1)
+// (yl, yl1, zl, zl1).  Thread per j; every point is staged twice.
+template <bool DIRECT, bool COMP>
 __global__ void prep_stage_kernel(const void* __restrict__ xyz, int dtype, long long n,
                                   PrepStats* __restrict__ st, float4* __restrict__ even, float4* __restrict__ odd) {
     double c[3];
@@ -293,6 +312,16 @@ __global__ void prep_stage_kernel(const void* __restrict__ xyz, int dtype, long 
     double mnorm = 0.0;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
+        if (COMP) {
+            float h0[3], l0[3], h1[3], l1[3];
+            staged_point_comp(xyz, dtype, i, c, ci, h0, l0);
+            staged_point_comp(xyz, dtype, i + 1 == n ? 0 : i + 1, c, ci, h1, l1);
+            float4* dst = ((i & 1) ? odd : even) + 3 * (i >> 1);
+            dst[0] = make_float4(h0[0], h1[0], h0[1], h1[1]);
+            dst[1] = make_float4(h0[2], h1[2], l0[0], l1[0]);
+            dst[2] = make_float4(l0[1], l1[1], l0[2], l1[2]);
+            continue;
+        }
         double nq, nq1;
         const float4 p = staged_point<DIRECT>(xyz, dtype, i, c, ci, &nq);
         const float4 p1 = staged_point<DIRECT>(xyz, dtype, i + 1 == n ? 0 : i + 1, c, ci, &nq1);
@@ -382,6 +411,7 @@ struct KernelCfg {
 #endif
 constexpr KernelCfg kBig{4, PC_BIG_R, 256};  // direct (sum) kernel: warp tile 32*R rows (256 by default)
 constexpr KernelCfg kBigGram{4, 12, 256};    // count kernel: 384-row warp tiles measured 6% faster than 256
+constexpr KernelCfg kBigComp{4, 4, 256};     // compensated sum kernel (non-f32 input): 6 row registers per row
 constexpr KernelCfg kSmall{4, 2, 64};  // warp tile 64 rows, for n < kSmallN
 constexpr int kSmallN = 16384;
 
@@ -394,7 +424,7 @@ struct WsLayout {
 };
 WsLayout ws_layout(long long n) {
     WsLayout l;
-    const size_t pair_bytes = align_up((size_t)(n / 2 + 1) * 2 * sizeof(float4), 256);
+    const size_t pair_bytes = align_up((size_t)(n / 2 + 1) * 3 * sizeof(float4), 256);  // up to 3 float4 per pair
     l.pts = 0;  // even pairs, then odd pairs
     l.stats = 2 * pair_bytes;
     l.slots = l.stats + 256;
@@ -424,10 +454,10 @@ int num_sms() {
     return g_num_sms[dev];
 }
 
-template <int WARPS, int R, int W, bool DIRECT, bool FLAT>
+template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP>
 int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStream_t s) {
-    auto kern = pairs_kernel<WARPS, R, W, DIRECT, FLAT>;
-    constexpr int smem = WARPS * pairs_smem_per_warp<R, W>();
+    auto kern = pairs_kernel<WARPS, R, W, DIRECT, FLAT, COMP>;
+    constexpr int smem = WARPS * pairs_smem_per_warp<R, W, COMP>();
     {
         static thread_local bool attr_set[64] = {false};
         int dev = 0;
@@ -475,16 +505,16 @@ int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStr
     return PC_OK;
 }
 
-template <int WARPS, int R, int W, bool DIRECT>
+template <int WARPS, int R, int W, bool DIRECT, bool COMP = false>
 int dispatch_cfg(PairsArgs args, bool flat, long long cap, int* nslots, cudaStream_t s) {
     constexpr int T = 32 * R;
     args.n_tiles = (args.hi - args.lo + T - 1) / T;
     if (flat) {
         args.L = (long long)(T - 1) + (args.n >> 1);
         args.total = (long long)args.n_tiles * args.L;
-        return launch_pairs<WARPS, R, W, DIRECT, true>(args, cap, nslots, s);
+        return launch_pairs<WARPS, R, W, DIRECT, true, COMP>(args, cap, nslots, s);
     }
-    return launch_pairs<WARPS, R, W, DIRECT, false>(args, cap, nslots, s);
+    return launch_pairs<WARPS, R, W, DIRECT, false, COMP>(args, cap, nslots, s);
 }
 
 int run_pairs(const void* xyz, int dtype, long long n, int interaction, int schedule, int tiling,
@@ -512,6 +542,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     PrepStats* st = (PrepStats*)(ws + lay.stats);
     Slot* slots = (Slot*)(ws + lay.slots);
     const bool direct = interaction == PC_COLLISION_INVSQ;
+    const bool comp = direct && dtype != PC_F32;  // f32 coordinates are exact as staged
 
     // bbox init: minima to the largest ordered code, maxima to the smallest
     CK(cudaMemsetAsync(st, 0xff, offsetof(PrepStats, mx), s));
@@ -520,8 +551,9 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
         const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)num_sms() * 8);
         prep_bbox_kernel<<<blocks, 256, 0, s>>>(xyz, dtype, n, st);
         CK_LAUNCH("prep_bbox_kernel");
-        if (direct) prep_stage_kernel<true><<<blocks, 256, 0, s>>>(xyz, dtype, n, st, pts_even, pts_odd);
-        else prep_stage_kernel<false><<<blocks, 256, 0, s>>>(xyz, dtype, n, st, pts_even, pts_odd);
+        if (comp) prep_stage_kernel<true, true><<<blocks, 256, 0, s>>>(xyz, dtype, n, st, pts_even, pts_odd);
+        else if (direct) prep_stage_kernel<true, false><<<blocks, 256, 0, s>>>(xyz, dtype, n, st, pts_even, pts_odd);
+        else prep_stage_kernel<false, false><<<blocks, 256, 0, s>>>(xyz, dtype, n, st, pts_even, pts_odd);
         CK_LAUNCH("prep_stage_kernel");
     }
     PairsArgs args{};
@@ -546,11 +578,13 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
             const bool flat = tiling == PC_TILE_FLAT;
             int rc;
             if (n < kSmallN)
-                rc = direct ? dispatch_cfg<kSmall.warps, kSmall.r, kSmall.w, true>(args, flat, cap, &nslots, s)
-                            : dispatch_cfg<kSmall.warps, kSmall.r, kSmall.w, false>(args, flat, cap, &nslots, s);
+                rc = comp     ? dispatch_cfg<kSmall.warps, kSmall.r, kSmall.w, true, true>(args, flat, cap, &nslots, s)
+                     : direct ? dispatch_cfg<kSmall.warps, kSmall.r, kSmall.w, true>(args, flat, cap, &nslots, s)
+                              : dispatch_cfg<kSmall.warps, kSmall.r, kSmall.w, false>(args, flat, cap, &nslots, s);
             else
-                rc = direct ? dispatch_cfg<kBig.warps, kBig.r, kBig.w, true>(args, flat, cap, &nslots, s)
-                            : dispatch_cfg<kBigGram.warps, kBigGram.r, kBigGram.w, false>(args, flat, cap, &nslots, s);
+                rc = comp     ? dispatch_cfg<kBigComp.warps, kBigComp.r, kBigComp.w, true, true>(args, flat, cap, &nslots, s)
+                     : direct ? dispatch_cfg<kBig.warps, kBig.r, kBig.w, true>(args, flat, cap, &nslots, s)
+                              : dispatch_cfg<kBigGram.warps, kBigGram.r, kBigGram.w, false>(args, flat, cap, &nslots, s);
             if (rc) return rc;
         }
         finalize_kernel<<<1, 256, 0, s>>>(slots, nslots, st, row_pairs(n, lo, hi, schedule), direct ? 1 : 0, dres + k);

@@ -36,10 +36,22 @@ __device__ __forceinline__ float2 f2_rsub(float a, float2 b) {  // a - b, a broa
     return *reinterpret_cast<float2*>(&dd);
 }
 
-// element k of an interleaved pair buffer: (x, y, z, w)
-__device__ __forceinline__ float4 col_of(const float4* sp, int k) {
-    const float4 A = sp[k & ~1], B = sp[k | 1];
+// Pair-buffer layouts (one entry per column pair k, k+1):
+//   PS = 2 float4: (x, x', y, y')(z, z', w, w')                       Gram / direct
+//   PS = 3 float4: (x, x', y, y')(z, z', xl, xl')(yl, yl', zl, zl')   compensated direct:
+//   the centred coordinate is the unevaluated fp32 sum hi + lo (non-f32 inputs)
+template <bool COMP>
+__device__ __forceinline__ float4 col_hi(const float4* sp, int k) {  // (x, y, z, w) of element k
+    constexpr int PS = COMP ? 3 : 2;
+    const float4* b = sp + PS * (k >> 1);
+    const float4 A = b[0], B = b[1];
+    if (COMP) return (k & 1) ? make_float4(A.y, A.w, B.y, 0.f) : make_float4(A.x, A.z, B.x, 0.f);
     return (k & 1) ? make_float4(A.y, A.w, B.y, B.w) : make_float4(A.x, A.z, B.x, B.z);
+}
+__device__ __forceinline__ float4 col_lo(const float4* sp, int k) {  // (xl, yl, zl, 0), PS = 3 only
+    const float4* b = sp + 3 * (k >> 1);
+    const float4 B = b[1], C = b[2];
+    return (k & 1) ? make_float4(B.w, C.y, C.w, 0.f) : make_float4(B.z, C.x, C.z, 0.f);
 }
 
 #ifndef PC_MINB
@@ -50,15 +62,17 @@ __device__ __forceinline__ float4 col_of(const float4* sp, int k) {
 #endif
 constexpr int kDirectUnroll = PC_DIRECT_UNROLL;
 
-// dynamic shared memory per warp: 2 column buffers of W + one row buffer of T (float4 each)
-template <int R, int W>
+// dynamic shared memory per warp: 2 column buffers of W + one row buffer of T (PS/2 float4 per element)
+template <int R, int W, bool COMP = false>
 constexpr int pairs_smem_per_warp() {
-    return (2 * W + 32 * R) * (int)sizeof(float4);
+    return (2 * W + 32 * R) / 2 * (COMP ? 3 : 2) * (int)sizeof(float4);
 }
 
-template <int WARPS, int R, int W, bool DIRECT, bool FLAT>
+template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP = false>
 __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsArgs a) {
     constexpr int T = 32 * R;
+    constexpr int PS = COMP ? 3 : 2;  // float4 per column pair
+    static_assert(DIRECT || !COMP, "compensated staging is for the direct (sum) formula");
     static_assert(W % 64 == 0 && T % 64 == 0, "buffers must hold whole pairs for every lane");
     extern __shared__ __align__(16) float4 s_dyn[];
     __shared__ unsigned long long s_red[WARPS][2];
@@ -125,31 +139,37 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
         return j;
     };
     auto pair_src = [&](int j) -> const float4* {  // pair (j, (j+1) mod n)
-        return (j & 1 ? a.pts_odd : a.pts_even) + 2 * (j >> 1);
+        return (j & 1 ? a.pts_odd : a.pts_even) + PS * (j >> 1);
     };
 
-    float4* sp0 = s_dyn + (size_t)wid * (2 * W + T);  // column buffers [2][W]
-    float4* rowbuf = sp0 + 2 * W;                      // row buffer [T]
+    float4* sp0 = s_dyn + (size_t)wid * ((2 * W + T) / 2 * PS);  // column buffers [2][W elements]
+    float4* rowbuf = sp0 + W * PS;                                // row buffer [T elements]
     // a far column (0, 0, 0, fw): its Gram value is -inf, never a candidate
     const float fw = DIRECT ? 0.f : -INFINITY;
     auto stage_cols = [&](int buf, int t, int o, int wc) {
         const int j0 = a.lo + t * T + o + 1;  // column k sits at j0 + k (mod n when balanced)
-        float4* sp = sp0 + buf * W;
+        float4* sp = sp0 + buf * (W / 2 * PS);
 #pragma unroll
         for (int q = 0; q < W / 64; ++q) {
             const int k = 2 * (q * 32 + lane);  // columns k, k+1
+            float4* d = sp + PS * (k >> 1);
             if (k + 1 < wc) {
                 const float4* src = pair_src(bal ? wrap(j0 + k) : j0 + k);
-                cp_async16(&sp[k], src);
-                cp_async16(&sp[k + 1], src + 1);
+#pragma unroll
+                for (int p = 0; p < PS; ++p) cp_async16(&d[p], src + p);
             } else if (k < wc) {  // last column of an odd-width chunk: second half is a far point
                 const float4* src = pair_src(bal ? wrap(j0 + k) : j0 + k);
                 const float4 A = src[0], B = src[1];
-                sp[k] = make_float4(A.x, 0.f, A.z, 0.f);
-                sp[k + 1] = make_float4(B.x, 0.f, B.z, fw);
+                d[0] = make_float4(A.x, 0.f, A.z, 0.f);
+                d[1] = make_float4(B.x, 0.f, B.z, COMP ? 0.f : fw);
+                if (COMP) {
+                    const float4 C = src[2];
+                    d[PS - 1] = make_float4(C.x, 0.f, C.z, 0.f);
+                }
             } else {
-                sp[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-                sp[k + 1] = make_float4(0.f, 0.f, fw, fw);
+                d[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+                d[1] = make_float4(0.f, 0.f, COMP ? 0.f : fw, COMP ? 0.f : fw);
+                if (COMP) d[PS - 1] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
     };
@@ -160,13 +180,14 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             const int rl = 2 * (q * 32 + lane);  // rows rl, rl+1
             if (i0 + rl < n) {
                 const float4* src = pair_src(i0 + rl);
-                cp_async16(&rowbuf[rl], src);
-                cp_async16(&rowbuf[rl + 1], src + 1);
+#pragma unroll
+                for (int p = 0; p < PS; ++p) cp_async16(&rowbuf[PS * (rl >> 1) + p], src + p);
             }
         }
     };
 
     float rx[R], ry[R], rz[R], rc[R];
+    float rxl[R], ryl[R], rzl[R];  // COMP: low parts of the row coordinates
     int cur_tile = -1;
     unsigned valid_rows = 0;
     unsigned long long cnt = 0, checks = 0;
@@ -191,10 +212,16 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             for (int r = 0; r < R; ++r) {
                 const int rl = r * 32 + lane;
                 const bool ok = i0 + rl < a.hi;
-                const float4 v = col_of(rowbuf, rl);
+                const float4 v = col_hi<COMP>(rowbuf, rl);
                 rx[r] = ok ? v.x : 0.f;
                 ry[r] = ok ? v.y : 0.f;
                 rz[r] = ok ? v.z : 0.f;
+                if (COMP) {
+                    const float4 vl = col_lo(rowbuf, rl);
+                    rxl[r] = ok ? vl.x : 0.f;
+                    ryl[r] = ok ? vl.y : 0.f;
+                    rzl[r] = ok ? vl.z : 0.f;
+                }
                 rc[r] = ok ? (force ? -INFINITY : -v.w - half_tb) : INFINITY;
                 valid_rows |= (ok ? 1u : 0u) << r;
             }
@@ -219,7 +246,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             cp_async_commit();
         }
 
-        const float4* sp = sp0 + buf * W;
+        const float4* sp = sp0 + buf * (W / 2 * PS);
         const int j0 = i0 + off + 1;
         // every cell of the chunk owned by its row?  (see header comment)
         const bool dense = wc == W && i0 + T <= a.hi && off + 1 >= T && (!bal || off + W <= steps_min);
@@ -266,7 +293,29 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             float2 acc[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] = make_float2(0.f, 0.f);
-            if (dense) {
+            if (COMP && dense) {
+                // ---- compensated direct formula: dr = (hi_i - hi_j) + (lo_i - lo_j) keeps the
+                // separation to ~2u relative however far the points sit from the centre
+                const float2 one = make_float2(1.0f, 1.0f);
+#pragma unroll 1
+                for (int k = 0; k < W; k += 4) {
+                    const float4* P = sp + 3 * (k >> 1);
+                    const float4 A0 = P[0], B0 = P[1], C0 = P[2], A1 = P[3], B1 = P[4], C1 = P[5];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        float2 dx = __fadd2_rn(f2_rsub(rx[r], make_float2(A0.x, A0.y)), f2_rsub(rxl[r], make_float2(B0.z, B0.w)));
+                        float2 dy = __fadd2_rn(f2_rsub(ry[r], make_float2(A0.z, A0.w)), f2_rsub(ryl[r], make_float2(C0.x, C0.y)));
+                        float2 dz = __fadd2_rn(f2_rsub(rz[r], make_float2(B0.x, B0.y)), f2_rsub(rzl[r], make_float2(C0.z, C0.w)));
+                        const float2 p0 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __ffma2_rn(dx, dx, one)));
+                        dx = __fadd2_rn(f2_rsub(rx[r], make_float2(A1.x, A1.y)), f2_rsub(rxl[r], make_float2(B1.z, B1.w)));
+                        dy = __fadd2_rn(f2_rsub(ry[r], make_float2(A1.z, A1.w)), f2_rsub(ryl[r], make_float2(C1.x, C1.y)));
+                        dz = __fadd2_rn(f2_rsub(rz[r], make_float2(B1.x, B1.y)), f2_rsub(rzl[r], make_float2(C1.z, C1.w)));
+                        const float2 p1 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __ffma2_rn(dx, dx, one)));
+                        const float2 pr = __fmul2_rn(p0, p1), sm = __fadd2_rn(p0, p1);
+                        acc[r] = __ffma2_rn(sm, make_float2(rcp_approx(pr.x), rcp_approx(pr.y)), acc[r]);
+                    }
+                }
+            } else if (dense) {
                 // ---- direct formula, packed: p = 1 + |dr|^2 for two columns per FADD2/FFMA2;
                 // two column pairs share one FMUL2/FADD2/FFMA2 for 1/pa + 1/pc = (pa+pc)/(pa*pc)
                 const float2 one = make_float2(1.0f, 1.0f);
@@ -290,14 +339,20 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             } else {
                 // ---- edge chunk: per-pair ownership mask ----
                 for (int k = 0; k < W; ++k) {
-                    const float4 c0 = col_of(sp, k);
+                    const float4 c0 = col_hi<COMP>(sp, k);
+                    const float4 l0 = COMP ? col_lo(sp, k) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         const int rl = r * 32 + lane;
                         const int i = i0 + rl;
                         const int lim = i < a.hi ? (bal ? steps_for_dev(n, i) : n - 1 - i) : 0;
                         const bool ok = k < wc && (unsigned)(off + k - rl) < (unsigned)lim;
-                        const float dx = rx[r] - c0.x, dy = ry[r] - c0.y, dz = rz[r] - c0.z;
+                        float dx = rx[r] - c0.x, dy = ry[r] - c0.y, dz = rz[r] - c0.z;
+                        if (COMP) {
+                            dx += rxl[r] - l0.x;
+                            dy += ryl[r] - l0.y;
+                            dz += rzl[r] - l0.z;
+                        }
                         const float p = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1.0f)));
                         acc[r].x += ok ? rcp_approx(p) : 0.0f;
                     }
@@ -333,7 +388,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
 #pragma unroll 2
                     for (int q = 0; q < W / 32; ++q) {
                         const int k = q * 32 + lane;
-                        const float4 c0 = col_of(sp, k);
+                        const float4 c0 = col_hi<COMP>(sp, k);
                         bool cand;
                         if (DIRECT) {
                             const float dx = qx - c0.x, dy = qy - c0.y, dz = qz - c0.z;

@@ -345,6 +345,38 @@ def test_batch_entry_points_agree():
         assert got[-1].error == _lib.PC_ERR_ARG  # > 4096 beads: the caller routes it through the grid
 
 
+def _invsq_cases():
+    rng = np.random.default_rng(11)
+    a = rng.random((1500, 3)) * 6.0
+    yield "f64 cluster far from the origin", a + 1.0e4
+    two = np.concatenate([a, rng.random((1500, 3)) * 6.0 + np.array([1.0e5, 0.0, 0.0])])
+    yield "f64 two clusters 1e5 apart", two
+    yield "f64 default generator dtype", gen.random_spheres(3000, 80.0, 5)
+    yield "f64 huge offset, unit spacing", rng.random((1000, 3)) * 3.0 + 3.0e7
+    ints = rng.integers(0, 4, size=(1500, 3)) + np.int64(2**40)
+    yield "int64 near 2^40", ints
+    yield "int64 two clusters", np.concatenate([ints, ints[:700] - np.int64(2**41)])
+    yield "int32 spread", rng.integers(-2**30, 2**30, size=(800, 3)).astype(np.int32)
+
+
+@pytest.mark.parametrize("case", range(7))
+def test_inverse_square_sum_tight_for_non_f32_inputs(case):
+    # float64 / integer coordinates: the kernel must not lose the pair separation
+    # to fp32 rounding of large coordinates (compensated hi+lo staging, DESIGN.md
+    # §3).  Bar: 2e-6 relative, 5x tighter than the north_star's 1e-5.
+    name, pts = list(_invsq_cases())[case]
+    n = len(pts)
+    for sched in ("balanced", "standard"):
+        c_want, s_want, _ = c_oracle.rows(pts, 0, n, sched)
+        (r,) = _lib.pairs_host(np.ascontiguousarray(pts), _lib.PC_COLLISION_INVSQ,
+                               _lib.PC_BALANCED if sched == "balanced" else _lib.PC_STANDARD, [0, n])
+        assert r.count == c_want, name
+        assert r.sum == pytest.approx(s_want, rel=2e-6), name
+    r = se.spi_parallel(pts, se.inverse_square, 3, "balanced")
+    for b, got in zip(se._partition(n, 3), r.partials):
+        assert got == pytest.approx(c_oracle.rows(pts, b.start, b.stop, "balanced")[1], rel=2e-6), name
+
+
 def test_filter_bypass_for_huge_spans():
     # spans beyond ~1e15 make the fp32 Gram filter meaningless: every pair takes the exact path
     rng = np.random.default_rng(3)
