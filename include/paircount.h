@@ -126,6 +126,18 @@ int pc_pairs_host(const void* xyz_host, int32_t dtype, int64_t n, int32_t intera
                   int32_t schedule, int32_t tiling, int32_t nranges, const int64_t* bounds,
                   pc_pairs_result* results);
 
+/* Single-process multi-GPU all-pairs (SURVEY.md §8(b) pc_multi_pairs): device
+ * d computes the rows [bounds[d], bounds[d+1]) of the host input (bounds[0] = 0,
+ * bounds[ndev] = n; equal-work slabs as distributed.row_slabs) with
+ * pc_pairs_host on devices[d], one host thread per slab; per_device[d] is
+ * that slab's result and *total their sum in ascending d (count, float64 sum,
+ * pairs).  The exchange is host-side: the partials are 40 bytes each.  The
+ * same ordinal may repeat (slabs then run one after another).  For one
+ * process per GPU use distributed.spi_distributed (NCCL all-reduce). */
+int pc_pairs_multi(const void* xyz_host, int32_t dtype, int64_t n, int32_t interaction, int32_t schedule,
+                   int32_t tiling, int32_t ndev, const int32_t* devices, const int64_t* bounds,
+                   pc_pairs_result* per_device, pc_pairs_result* total);
+
 /* number of kernel launches the last pc_pairs* call on this thread issued */
 int32_t pc_last_launch_count(void);
 

@@ -39,7 +39,7 @@ DTYPE_CODES = {np.dtype(np.float32): PC_F32, np.dtype(np.float64): PC_F64,
 EXPORTED = (
     "pc_last_error", "pc_version", "pc_device_count", "pc_set_device", "pc_device_alloc",
     "pc_device_free", "pc_memcpy_h2d", "pc_memcpy_d2h", "pc_stream_sync",
-    "pc_pairs_workspace_bytes", "pc_pairs", "pc_pairs_async", "pc_pairs_host",
+    "pc_pairs_workspace_bytes", "pc_pairs", "pc_pairs_async", "pc_pairs_host", "pc_pairs_multi",
     "pc_last_launch_count", "pc_kernel_timing", "pc_kernel_timing_read", "pc_lattice_grid_cells", "pc_lattice_key_bytes",
     "pc_lattice_collisions", "pc_lattice_contacts", "pc_lattice_reset_keys", "pc_lattice_clear",
     "pc_lattice_collisions_batch", "pc_lattice_collisions_vectors",
@@ -81,6 +81,7 @@ _SIGS = {
     "pc_pairs": ([_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _sz, _vp, _vp], ctypes.c_int),
     "pc_pairs_async": ([_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _sz, _vp, _vp], ctypes.c_int),
     "pc_pairs_host": ([_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
+    "pc_pairs_multi": ([_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp], ctypes.c_int),
     "pc_last_launch_count": ([], _i32),
     "pc_kernel_timing": ([_i32], ctypes.c_int),
     "pc_kernel_timing_read": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i32)], ctypes.c_int),
@@ -160,6 +161,21 @@ def pairs_host(xyz: np.ndarray, interaction: int, schedule: int, bounds, tiling:
                            b.ctypes.data, ctypes.addressof(res))
     check(rc)
     return list(res)
+
+
+def pairs_multi(xyz: np.ndarray, interaction: int, schedule: int, devices, bounds, tiling: int = PC_TILE_AUTO):
+    """pc_pairs_multi: slab d of the rows on devices[d]; returns (per-device results, total)."""
+    lib = load()
+    arr = np.ascontiguousarray(xyz)
+    devs = np.ascontiguousarray(np.asarray(devices, dtype=np.int32))
+    b = np.ascontiguousarray(np.asarray(bounds, dtype=np.int64))
+    if len(b) != len(devs) + 1:
+        raise ValueError("need len(devices) + 1 slab bounds")
+    per = (PairsResult * len(devs))()
+    tot = PairsResult()
+    check(lib.pc_pairs_multi(arr.ctypes.data, DTYPE_CODES[arr.dtype], len(arr), interaction, schedule, tiling,
+                             len(devs), devs.ctypes.data, b.ctypes.data, ctypes.addressof(per), ctypes.byref(tot)))
+    return list(per), tot
 
 
 def pairs_async(xyz_ptr: int, dtype_code: int, n: int, interaction: int, schedule: int, bounds_host: np.ndarray,

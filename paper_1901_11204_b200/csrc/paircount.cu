@@ -1209,6 +1209,59 @@ int pc_pairs_host(const void* xyz_host, int32_t dtype, int64_t n, int32_t intera
     return rc;
 }
 
+int pc_pairs_multi(const void* xyz_host, int32_t dtype, int64_t n, int32_t interaction, int32_t schedule,
+                   int32_t tiling, int32_t ndev, const int32_t* devices, const int64_t* bounds,
+                   pc_pairs_result* per_device, pc_pairs_result* total) {
+    if (ndev < 1 || !devices || !bounds || !per_device || !total) return arg_fail("bad device list");
+    if (n < 0) return arg_fail("negative n");
+    if (bounds[0] != 0 || bounds[ndev] != n) return arg_fail("device slabs must cover rows [0, n)");
+    for (int d = 0; d < ndev; ++d)
+        if (bounds[d] > bounds[d + 1]) return arg_fail("device slab bounds must be non-decreasing");
+    int count = 0;
+    CK(cudaGetDeviceCount(&count));
+    for (int d = 0; d < ndev; ++d)
+        if (devices[d] < 0 || devices[d] >= count) return arg_fail("device ordinal out of range");
+    std::vector<int> rcs((size_t)ndev, PC_OK), launches((size_t)ndev, 0);
+    std::vector<std::string> errs((size_t)ndev);
+    auto work = [&](int d) {
+        int prev = 0;
+        cudaGetDevice(&prev);
+        if (cudaSetDevice(devices[d]) != cudaSuccess) {
+            rcs[d] = PC_ERR_CUDA;
+            errs[d] = "cudaSetDevice failed";
+            return;
+        }
+        rcs[d] = pc_pairs_host(xyz_host, dtype, n, interaction, schedule, tiling, 1, bounds + d, per_device + d);
+        launches[d] = g_launches;  // thread-local state of this worker thread
+        if (rcs[d] != PC_OK) errs[d] = g_err;
+        cudaSetDevice(prev);
+    };
+    // one host thread per slab; slabs on the same device serialise on its arena lock
+    std::vector<std::thread> pool;
+    for (int d = 1; d < ndev; ++d) pool.emplace_back(work, d);
+    work(0);
+    for (auto& th : pool) th.join();
+    g_launches = 0;
+    for (int d = 0; d < ndev; ++d) g_launches += launches[d];
+    for (int d = 0; d < ndev; ++d)
+        if (rcs[d] != PC_OK) {
+            g_err = errs[d];
+            return rcs[d];
+        }
+    // the exchange step: partials combined in ascending device order (deterministic float64 sum)
+    pc_pairs_result t;
+    memset(&t, 0, sizeof t);
+    for (int d = 0; d < ndev; ++d) {
+        t.count += per_device[d].count;
+        t.sum += per_device[d].sum;
+        t.pairs += per_device[d].pairs;
+        t.exact_checks += per_device[d].exact_checks;
+        if (!t.error) t.error = per_device[d].error;
+    }
+    *total = t;
+    return PC_OK;
+}
+
 int32_t pc_last_launch_count(void) { return g_launches; }
 
 int pc_kernel_timing(int32_t enable) {

@@ -99,3 +99,34 @@ def spi_distributed(objects, f, schedule: str = "balanced", group=None,
         total = total + p
     pairs = tuple(row_pairs(n, a, b, schedule) for a, b in row_slabs(n, world, schedule))
     return total, partials, pairs
+
+
+def spi_multi_gpu(objects, f, schedule: str = "balanced", devices=None):
+    """Total of f over all pairs with the rows split over several GPUs of ONE
+    process (``pc_pairs_multi``: a host thread per device, partials combined
+    in ascending device order).  ``devices`` defaults to every visible GPU;
+    an ordinal may repeat.  Returns (total, per-device partials, per-device
+    pair counts), like ``spi_distributed``."""
+    from . import _lib, spi_engine
+
+    if schedule not in spi_engine.SCHEDULES:
+        raise ValueError(f"schedule must be one of {spi_engine.SCHEDULES}, got {schedule!r}")
+    obj = spi_engine.as_object_array(objects)
+    n = len(obj)
+    if devices is None:
+        devices = list(range(int(_lib.load().pc_device_count())))
+    devices = [int(d) for d in devices]
+    if not devices:
+        raise ValueError("need at least one device")
+    slabs = row_slabs(n, len(devices), schedule)
+    pairs = tuple(row_pairs(n, a, b, schedule) for a, b in slabs)
+    if n < 2:
+        return 0, tuple(0 for _ in devices), pairs
+    code, xyz = spi_engine._prepare(obj, f, slabs, schedule)
+    bounds = [slabs[0][0]] + [b for _, b in slabs]
+    per, _ = _lib.pairs_multi(xyz, code, _lib.SCHEDULE_CODES[schedule], devices, bounds)
+    partials = tuple(spi_engine._partial_of(r, code, n, a, b, schedule)[0] for (a, b), r in zip(slabs, per))
+    total = partials[0]
+    for p in partials[1:]:
+        total = total + p
+    return total, partials, pairs

@@ -158,12 +158,9 @@ def _first_nonfinite_pair(obj: np.ndarray, f, schedule: str, lo: int, hi: int):
     return None
 
 
-def _run_ranges(obj: np.ndarray, f, ranges: list[tuple[int, int]], schedule: str):
-    """(partial, pairs) per row range -- the GPU counterpart of calling
-    _run_outer once per range (spi_engine.py:109-120)."""
-    n = len(obj)
-    if n < 2:
-        return [(0, 0) for _ in ranges]
+def _prepare(obj: np.ndarray, f, ranges: list[tuple[int, int]], schedule: str):
+    """(interaction code, device-ready coordinates) after the reference's
+    domain checks for the rows in ``ranges`` (spi_engine.py:84-99)."""
     code = _interaction_code(f)
     xyz = _device_coords(obj)
     if xyz.dtype.kind == "f" and not np.isfinite(xyz).all():
@@ -174,20 +171,32 @@ def _run_ranges(obj: np.ndarray, f, ranges: list[tuple[int, int]], schedule: str
             if hit:
                 raise AccumulationError(f"non-finite contribution for pair ({hit[0]}, {hit[1]})")
         raise InteractionDomainError("coordinates must be finite for the GPU inverse-square sum")
+    return code, xyz
+
+
+def _partial_of(r, code: int, n: int, lo: int, hi: int, schedule: str):
+    """Typed partial of one kernel result record (int count or float sum)."""
+    if r.error == _lib.PC_ERR_DOMAIN:
+        raise InteractionDomainError("sphere coordinates must be finite")
+    if r.error == _lib.PC_ERR_ARG:
+        raise ValueError("coordinates too large for the fp32 inverse-square kernel (|c| >= 1e18)")
+    pairs = row_pairs(n, lo, hi, schedule)
+    if int(r.pairs) != pairs:
+        raise RuntimeError(f"kernel pair count {r.pairs} != closed form {pairs}")
+    partial = float(r.sum) if code == _lib.PC_COLLISION_INVSQ else int(r.count)
+    return (partial if pairs else 0), pairs
+
+
+def _run_ranges(obj: np.ndarray, f, ranges: list[tuple[int, int]], schedule: str):
+    """(partial, pairs) per row range -- the GPU counterpart of calling
+    _run_outer once per range (spi_engine.py:109-120)."""
+    n = len(obj)
+    if n < 2:
+        return [(0, 0) for _ in ranges]
+    code, xyz = _prepare(obj, f, ranges, schedule)
     bounds = [ranges[0][0]] + [hi for _, hi in ranges]
     results = _lib.pairs_host(xyz, code, _lib.SCHEDULE_CODES[schedule], bounds)
-    out = []
-    for (lo, hi), r in zip(ranges, results):
-        if r.error == _lib.PC_ERR_DOMAIN:
-            raise InteractionDomainError("sphere coordinates must be finite")
-        if r.error == _lib.PC_ERR_ARG:
-            raise ValueError("coordinates too large for the fp32 inverse-square kernel (|c| >= 1e18)")
-        pairs = row_pairs(n, lo, hi, schedule)
-        if int(r.pairs) != pairs:
-            raise RuntimeError(f"kernel pair count {r.pairs} != closed form {pairs}")
-        partial = float(r.sum) if code == _lib.PC_COLLISION_INVSQ else int(r.count)
-        out.append((partial if pairs else 0, pairs))
-    return out
+    return [_partial_of(r, code, n, lo, hi, schedule) for (lo, hi), r in zip(ranges, results)]
 
 
 def _audit_symmetry(obj: np.ndarray, f, rng_seed: int = 0, samples: int = 16) -> None:

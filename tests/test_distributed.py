@@ -5,6 +5,8 @@ the compute callback."""
 
 from __future__ import annotations
 
+import functools
+import operator
 import os
 import socket
 
@@ -138,3 +140,31 @@ def test_two_ranks_real_kernels_gloo():
         for (lo, hi), part in zip(D.row_slabs(len(objs), world, sched), parts):
             assert part == c_oracle.rows(objs, lo, hi, sched)[0]
         assert results[1][sched][0] == results[0][sched][0]
+
+
+@pytest.mark.gpu
+def test_single_process_multi_gpu_entry():
+    """pc_pairs_multi (SURVEY.md §8(b) pc_multi_pairs): slabs on a device list,
+    partials combined host-side in device order.  The box has one GPU, so the
+    list repeats ordinal 0 -- the slabs are independent, nothing waits."""
+    from oracle import c_oracle
+    from paper_1901_11204_b200 import _lib
+    from paper_1901_11204_b200 import generators as gen
+    from paper_1901_11204_b200 import spi_engine as se
+
+    objs = gen.random_spheres(30_001, 24.0, 8).astype(np.float32)
+    n = len(objs)
+    for sched in ("balanced", "standard"):
+        want_c, want_s, _ = c_oracle.rows(objs, 0, n, sched)
+        for devs in ([0], [0, 0], [0, 0, 0, 0]):
+            tc, parts, pairs = D.spi_multi_gpu(objs, se.collision_indicator, sched, devs)
+            assert tc == want_c and sum(pairs) == n * (n - 1) // 2
+            for (lo, hi), part in zip(D.row_slabs(n, len(devs), sched), parts):
+                assert part == c_oracle.rows(objs, lo, hi, sched)[0]
+            ts, sparts, _ = D.spi_multi_gpu(objs, se.inverse_square, sched, devs)
+            assert ts == pytest.approx(want_s, rel=1e-5)
+            assert ts == functools.reduce(operator.add, sparts)  # left fold, as spi_engine.py:221-223
+        if sched == "balanced":  # equal slabs == the reference's worker partition
+            assert parts == se.spi_parallel(objs, se.collision_indicator, 4, "balanced").partials
+    with pytest.raises(ValueError):
+        _lib.pairs_multi(objs, _lib.PC_COLLISION, _lib.PC_BALANCED, [0, 99], [0, 5, n])
