@@ -33,7 +33,7 @@ def nvcc() -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
-    newest = max(SRC.stat().st_mtime, HDR.stat().st_mtime)
+    newest = max([HDR.stat().st_mtime] + [f.stat().st_mtime for f in SRC.parent.iterdir() if f.is_file()])
     if not force and OUT.exists() and OUT.stat().st_mtime >= newest:
         return OUT
     tmp = OUT.with_suffix(".so.tmp")

@@ -32,7 +32,11 @@ constexpr int kSlabCells = 1 << kSlabShift;
 constexpr int kSubSlabs = 1 << (kBucketShift - kSlabShift);  // 16
 constexpr int kMaxBuckets = 16384;                             // grids below 2^32 cells
 constexpr int kKeyCap = 16384;    // keys of one bucket staged on chip (2x the uniform mean)
-constexpr int kSlabSmem = (kKeyCap + 8 + kKeyCap + 2 * kSlabCells + 3 * kSubSlabs) * 4;
+#ifndef PC_SLAB_BUFS
+#define PC_SLAB_BUFS 3
+#endif
+constexpr int kSlabBufs = PC_SLAB_BUFS;  // counting-array ring: up to kSlabBufs-1 bulk stores in flight per SM
+constexpr int kSlabSmem = (kKeyCap + 8 + kKeyCap + kSlabBufs * kSlabCells + 3 * kSubSlabs) * 4;
 
 __global__ void lat_keys_hist_kernel(const void* __restrict__ xyz, int dtype, long long n, long long a,
                                      long long side, unsigned* __restrict__ keys,
@@ -246,7 +250,8 @@ __device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uns
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
-__device__ __forceinline__ void bulk_wait_read_le1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read_le() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -263,8 +268,8 @@ __global__ void __launch_bounds__(1024, 1)
     extern __shared__ __align__(128) unsigned smem[];
     unsigned* keys_in = smem;                           // [kKeyCap + 8] staged keys (16 B aligned window)
     unsigned* keys_s = keys_in + kKeyCap + 8;           // [kKeyCap] keys grouped by slab
-    unsigned* cbuf0 = keys_s + kKeyCap;                 // [2][kSlabCells] double-buffered counting arrays
-    unsigned* sub_n = cbuf0 + 2 * kSlabCells;           // [kSubSlabs] keys per slab
+    unsigned* cbuf0 = keys_s + kKeyCap;                 // [kSlabBufs][kSlabCells] ring of counting arrays
+    unsigned* sub_n = cbuf0 + kSlabBufs * kSlabCells;   // [kSubSlabs] keys per slab
     unsigned* sub_cur = sub_n + kSubSlabs;              // [kSubSlabs] scatter cursors
     unsigned* sub_start = sub_cur + kSubSlabs;          // [kSubSlabs] slab start offsets
     __shared__ unsigned long long s_a[32], s_b[32];
@@ -291,8 +296,8 @@ __global__ void __launch_bounds__(1024, 1)
             const unsigned ncell =
                 (unsigned)(cells - cell0 < (unsigned long long)kSlabCells ? cells - cell0 : kSlabCells);
             unsigned* cnt = cbuf0 + flip * kSlabCells;
-            // the bulk store issued two slabs ago read this buffer: wait for it
-            if (threadIdx.x == 0) bulk_wait_read_le1();
+            // the bulk store issued kSlabBufs slabs ago read this buffer: wait for it
+            if (threadIdx.x == 0) bulk_wait_read_le<kSlabBufs - 1>();
             __syncthreads();
             uint4* cnt4 = reinterpret_cast<uint4*>(cnt);
             for (int q = threadIdx.x; q < kSlabCells / 4; q += blockDim.x) cnt4[q] = make_uint4(0u, 0u, 0u, 0u);
@@ -310,7 +315,7 @@ __global__ void __launch_bounds__(1024, 1)
             const unsigned vec_bytes = (ncell * 4u) & ~15u;
             if (threadIdx.x == 0 && vec_bytes) bulk_store_s2g(grid + cell0, cnt, vec_bytes);
             for (unsigned q = vec_bytes / 4 + threadIdx.x; q < ncell; q += blockDim.x) grid[cell0 + q] = cnt[q];
-            flip ^= 1;
+            flip = flip + 1 == kSlabBufs ? 0 : flip + 1;
         }
     };
 

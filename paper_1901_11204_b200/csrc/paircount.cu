@@ -114,11 +114,6 @@ __device__ __forceinline__ float max3f(float a, float b, float c) {
     asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
     return d;
 }
-__device__ __forceinline__ float min3f(float a, float b, float c) {
-    float d;
-    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-    return d;
-}
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -410,8 +405,17 @@ struct KernelCfg {
 #define PC_BIG_R 8
 #endif
 constexpr KernelCfg kBig{4, PC_BIG_R, 256};  // direct (sum) kernel: warp tile 32*R rows (256 by default)
-constexpr KernelCfg kBigGram{4, 12, 256};    // count kernel: 384-row warp tiles measured 6% faster than 256
-constexpr KernelCfg kBigComp{4, 4, 256};     // compensated sum kernel (non-f32 input): 6 row registers per row
+#ifndef PC_GRAM_R
+#define PC_GRAM_R 12
+#endif
+#ifndef PC_GRAM_W
+#define PC_GRAM_W 192  // 4 CTAs per SM fit in shared memory (256: 3); +4% at N = 65,536
+#endif
+#ifndef PC_COMP_W
+#define PC_COMP_W 192
+#endif
+constexpr KernelCfg kBigGram{4, PC_GRAM_R, PC_GRAM_W};  // count kernel: 384-row warp tiles measured 6% faster than 256
+constexpr KernelCfg kBigComp{4, 4, PC_COMP_W};          // compensated sum kernel (non-f32 input): 6 row registers per row
 constexpr KernelCfg kSmall{4, 2, 64};  // warp tile 64 rows, for n < kSmallN
 constexpr int kSmallN = 16384;
 
