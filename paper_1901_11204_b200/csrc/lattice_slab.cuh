@@ -152,28 +152,42 @@ __global__ void lat_coarse_kernel(const unsigned* __restrict__ base, int nbucket
     tbase[ncoarse] = tiles;
 }
 
-// Sort one tile [t0, t1) of `in` by digit(key) on chip and append each digit's
-// run at cursor[cur_base + digit] of `out`.
+// Stage keys [t0, t1) of `in` into shared `dst` at index p - (t0 & ~3): a
+// 16-byte cp.async per aligned quad, 4-byte ones for the ragged head and
+// tail (fine-pass tiles start anywhere; the last tile may end anywhere).
+// One commit group per call.
+constexpr int kStage = kPartTile + 8;  // staged keys per buffer (tile + alignment slack)
+__device__ __forceinline__ void stage_keys(const unsigned* __restrict__ in, long long t0, long long t1,
+                                           unsigned* dst) {
+    // 32-bit offsets from the aligned base a0 (a tile spans <= kPartTile keys)
+    const unsigned* src = in + (t0 & ~3LL);
+    const int h0 = (int)(t0 & 3), e = (int)(t1 - (t0 & ~3LL));  // keys live at [h0, e)
+    const int b0 = (h0 + 3) & ~3, b1 = e & ~3;                    // 16-byte body [b0, b1)
+    const int tid = threadIdx.x;
+    if (b0 >= b1) {
+        for (int p = h0 + tid; p < e; p += blockDim.x) cp_async4(&dst[p], &src[p]);
+    } else {
+        if (h0 + tid < b0) cp_async4(&dst[h0 + tid], &src[h0 + tid]);
+        for (int q = b0 + 4 * tid; q < b1; q += 4 * blockDim.x) cp_async16(&dst[q], &src[q]);
+        if (b1 + tid < e) cp_async4(&dst[b1 + tid], &src[b1 + tid]);
+    }
+    cp_async_commit();
+}
+
+// Sort one staged tile (kin[0 .. cnt)) by digit(key) on chip and append each
+// digit's run at cursor[cur_base + digit] of `out`.
 template <typename DigitFn>
-__device__ void partition_tile(const unsigned* __restrict__ in, long long t0, long long t1,
-                               unsigned* __restrict__ cursor, int cur_base, int ndig, DigitFn digit,
-                               unsigned* __restrict__ out, unsigned* buf, unsigned* h, unsigned* lofs,
-                               unsigned* goff) {
+__device__ void partition_tile(const unsigned* kin, int cnt, unsigned* __restrict__ cursor, int cur_base, int ndig,
+                               DigitFn digit, unsigned* __restrict__ out, unsigned* buf, unsigned* h,
+                               unsigned* lofs, unsigned* goff) {
     const int lane = threadIdx.x & 31;
     for (int d = threadIdx.x; d < ndig; d += blockDim.x) h[d] = 0u;
     __syncthreads();
     unsigned k[kPartPer], rank[kPartPer];
-    const bool vec = (reinterpret_cast<uintptr_t>(in + t0) & 15) == 0;  // fine-pass tiles start anywhere
 #pragma unroll
-    for (int q = 0; q < kPartPer / 4; ++q) {
-        const long long i = t0 + 4LL * (q * kPartThreads + threadIdx.x);
-        if (vec && i + 3 < t1) {
-            const uint4 v = *reinterpret_cast<const uint4*>(in + i);
-            k[4 * q] = v.x; k[4 * q + 1] = v.y; k[4 * q + 2] = v.z; k[4 * q + 3] = v.w;
-        } else {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) k[4 * q + u] = i + u < t1 ? in[i + u] : 0xffffffffu;
-        }
+    for (int u = 0; u < kPartPer; ++u) {
+        const int p = u * kPartThreads + threadIdx.x;
+        k[u] = p < cnt ? kin[p] : 0xffffffffu;
     }
 #pragma unroll
     for (int u = 0; u < kPartPer; ++u) rank[u] = k[u] != 0xffffffffu ? atomicAdd(&h[digit(k[u])], 1u) : 0u;
@@ -193,31 +207,49 @@ __device__ void partition_tile(const unsigned* __restrict__ in, long long t0, lo
     unsigned before = 0;
     for (int w = 0; w < (int)(threadIdx.x >> 5); ++w) before += s_wsum[w];
     if (d < ndig) {
-        lofs[d] = before + x - v;
-        goff[d] = v ? atomicAdd(&cursor[cur_base + d], v) : 0u;
+        const unsigned lo = before + x - v;
+        lofs[d] = lo;
+        goff[d] = (v ? atomicAdd(&cursor[cur_base + d], v) : 0u) - lo;  // out index = goff[d] + tile position
     }
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < kPartPer; ++u)
         if (k[u] != 0xffffffffu) buf[lofs[digit(k[u])] + rank[u]] = k[u];
     __syncthreads();
-    const int cnt = (int)(t1 - t0);
     for (int p = threadIdx.x; p < cnt; p += blockDim.x) {
-        const unsigned key = buf[p], d = digit(key);
-        out[goff[d] + (p - lofs[d])] = key;
+        const unsigned key = buf[p];
+        out[goff[digit(key)] + p] = key;
     }
     __syncthreads();
 }
+
+// Both passes walk their tiles with the next tile's keys in flight (cp.async
+// double buffer in dynamic shared memory): the partition itself is a chain of
+// barriers, so without the prefetch every tile paid a full DRAM round trip.
+constexpr int kPartSmem = 2 * kStage * 4;
 
 __global__ void __launch_bounds__(kPartThreads, 2) lat_partition_coarse_kernel(
     const unsigned* __restrict__ keys, long long n, unsigned* __restrict__ ccur, int ncoarse,
     unsigned* __restrict__ out, const unsigned long long* __restrict__ bad) {
     if (*bad != kNoBad) return;
+    extern __shared__ __align__(16) unsigned part_in[];  // [2][kStage]
     __shared__ unsigned buf[kPartTile];
     __shared__ unsigned h[kMaxCoarse], lofs[kMaxCoarse], goff[kMaxCoarse];
-    for (long long t0 = (long long)blockIdx.x * kPartTile; t0 < n; t0 += (long long)gridDim.x * kPartTile)
-        partition_tile(keys, t0, t0 + kPartTile < n ? t0 + kPartTile : n, ccur, 0, ncoarse,
+    const long long stride = (long long)gridDim.x * kPartTile;
+    long long t0 = (long long)blockIdx.x * kPartTile;
+    if (t0 < n) stage_keys(keys, t0, min(t0 + kPartTile, n), part_in);
+    for (int cur = 0; t0 < n; t0 += stride, cur ^= 1) {
+        const long long nx = t0 + stride;
+        if (nx < n) {
+            stage_keys(keys, nx, min(nx + kPartTile, n), part_in + (cur ^ 1) * kStage);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        partition_tile(part_in + cur * kStage, (int)(min(t0 + kPartTile, n) - t0), ccur, 0, ncoarse,
                        [](unsigned key) { return key >> kCoarseShift; }, out, buf, h, lofs, goff);
+    }
 }
 
 __global__ void __launch_bounds__(kPartThreads, 2) lat_partition_fine_kernel(
@@ -225,22 +257,46 @@ __global__ void __launch_bounds__(kPartThreads, 2) lat_partition_fine_kernel(
     int ncoarse, unsigned* __restrict__ fcur, unsigned* __restrict__ out,
     const unsigned long long* __restrict__ bad) {
     if (*bad != kNoBad) return;
+    extern __shared__ __align__(16) unsigned part_in[];  // [2][kStage]
     __shared__ unsigned buf[kPartTile];
     __shared__ unsigned h[kFinePerCoarse], lofs[kFinePerCoarse], goff[kFinePerCoarse];
-    const unsigned ntiles = tbase[ncoarse];
-    for (unsigned g = blockIdx.x; g < ntiles; g += gridDim.x) {
-        int c = 0;  // coarse bucket holding tile g (tbase is non-decreasing; <= 128 entries)
-        for (int lo = 0, hi = ncoarse; lo < hi;) {
-            const int mid = (lo + hi) >> 1;
-            if (tbase[mid + 1] <= g) lo = mid + 1;
-            else hi = mid;
-            c = lo;
+    __shared__ unsigned s_tb[kMaxCoarse + 1], s_cb[kMaxCoarse + 1];
+    for (int q = threadIdx.x; q <= ncoarse; q += blockDim.x) {
+        s_tb[q] = tbase[q];
+        s_cb[q] = cbase[q];
+    }
+    __syncthreads();
+    const unsigned ntiles = s_tb[ncoarse];
+    auto tile_of = [&](unsigned g, int& c, long long& t0, long long& t1) {
+        while (s_tb[c + 1] <= g) ++c;  // coarse bucket holding tile g (g only grows; c starts at the last one)
+        t0 = (long long)s_cb[c] + (long long)(g - s_tb[c]) * kPartTile;
+        t1 = t0 + kPartTile < (long long)s_cb[c + 1] ? t0 + kPartTile : (long long)s_cb[c + 1];
+    };
+    unsigned g = blockIdx.x;
+    int c = 0;
+    long long t0 = 0, t1 = 0;
+    if (g < ntiles) {
+        tile_of(g, c, t0, t1);
+        stage_keys(tmp, t0, t1, part_in);
+    }
+    for (int cur = 0; g < ntiles; g += gridDim.x, cur ^= 1) {
+        const unsigned gn = g + gridDim.x;
+        int cn = c;
+        long long n0 = 0, n1 = 0;
+        if (gn < ntiles) {
+            tile_of(gn, cn, n0, n1);
+            stage_keys(tmp, n0, n1, part_in + (cur ^ 1) * kStage);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
-        const long long t0 = (long long)cbase[c] + (long long)(g - tbase[c]) * kPartTile;
-        const long long t1 = t0 + kPartTile < (long long)cbase[c + 1] ? t0 + kPartTile : (long long)cbase[c + 1];
-        partition_tile(tmp, t0, t1, fcur, c * kFinePerCoarse, kFinePerCoarse,
+        __syncthreads();
+        partition_tile(part_in + cur * kStage + (t0 & 3), (int)(t1 - t0), fcur, c * kFinePerCoarse, kFinePerCoarse,
                        [](unsigned key) { return (key >> kBucketShift) & (kFinePerCoarse - 1); }, out, buf, h,
                        lofs, goff);
+        c = cn;
+        t0 = n0;
+        t1 = n1;
     }
 }
 

@@ -123,6 +123,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
@@ -984,6 +988,10 @@ int lattice_run(const void* xyz_in, int dtype, int on_device, long long n, long 
             CK(cudaFuncSetAttribute(lat_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSlabSmem));
             CK(cudaFuncSetAttribute(lat_keys_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kMaxBuckets * 4));
+            CK(cudaFuncSetAttribute(lat_partition_coarse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kPartSmem));
+            CK(cudaFuncSetAttribute(lat_partition_fine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kPartSmem));
             attr_set[dev & 63] = true;
         }
         CK(cudaMemsetAsync(hist, 0, nbuckets * 4, s));
@@ -994,10 +1002,10 @@ int lattice_run(const void* xyz_in, int dtype, int on_device, long long n, long 
         CK_LAUNCH("lat_bucket_scan_kernel");
         lat_coarse_kernel<<<1, 32, 0, s>>>(base, nbuckets, ncoarse, ccur, cbase, tbase);
         CK_LAUNCH("lat_coarse_kernel");
-        lat_partition_coarse_kernel<<<num_sms() * 2, kPartThreads, 0, s>>>((const unsigned*)keys, n, ccur, ncoarse,
+        lat_partition_coarse_kernel<<<num_sms() * 2, kPartThreads, kPartSmem, s>>>((const unsigned*)keys, n, ccur, ncoarse,
                                                                           scratch, sc.bad);
         CK_LAUNCH("lat_partition_coarse_kernel");
-        lat_partition_fine_kernel<<<num_sms() * 2, kPartThreads, 0, s>>>(scratch, cbase, tbase, ncoarse, cursor,
+        lat_partition_fine_kernel<<<num_sms() * 2, kPartThreads, kPartSmem, s>>>(scratch, cbase, tbase, ncoarse, cursor,
                                                                         sorted, sc.bad);
         CK_LAUNCH("lat_partition_fine_kernel");
         const int sgrid = std::min(num_sms(), nbuckets);

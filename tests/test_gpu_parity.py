@@ -197,6 +197,57 @@ def test_config5_counting_array(golden_configs):
     assert rep.count == pc.oracle_collisions(part)
 
 
+def _dense_cases():
+    rng = np.random.default_rng(21)
+    yield 64, rng.integers(-64, 65, size=(2_000_003, 3))                       # uniform, n % 4 != 0
+    yield 64, rng.integers(-5, 5, size=(600_000, 3))                            # one heavy region
+    yield 64, np.zeros((100_000, 3), dtype=np.int64) + 7                        # a single cell
+    yield 150, np.concatenate([rng.integers(-150, -140, size=(300_000, 3)),      # two far clusters
+                               rng.integers(140, 151, size=(300_000, 3))])
+    yield 64, rng.integers(-64, 65, size=(1_000_000, 3)).astype(np.int32)       # vectorised int32 path
+    yield 64, rng.integers(-64, 65, size=(1_000_001, 3)).astype(np.int32)[1:]   # int32, unaligned start
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_dense_regime_counting_array(case):
+    # beads > cells/64 on a clean grid: keys + tile sort + segment partition +
+    # shared-memory slabs.  Oracle: keys histogram on the host (Alg. 1 result).
+    a, beads = list(_dense_cases())[case]
+    side = 2 * a + 3
+    b64 = beads.astype(np.int64)
+    keys = ((b64[:, 0] + a + 1) * side + (b64[:, 1] + a + 1)) * side + (b64[:, 2] + a + 1)
+    occ = np.bincount(keys, minlength=side**3)
+    sp = pc.new_space(a)
+    assert len(beads) * 64 > side**3  # the dense regime
+    if beads.dtype == np.int32:  # device-resident int32 beads (bench's layout), aligned or not
+        import ctypes
+
+        import torch
+
+        lib = _lib.load()
+        full = torch.from_numpy(np.ascontiguousarray(np.concatenate([beads[:1], beads]))).cuda()
+        dev = full[1:] if case % 2 else full[:-1]  # 12-byte offset (scalar loads) or 16-byte aligned
+        if not case % 2:
+            dev.copy_(torch.from_numpy(beads).cuda())
+        kbuf = torch.empty(len(beads), dtype=torch.int32, device="cuda")
+        r = _lib.LatticeResult()
+        _lib.check(lib.pc_lattice_collisions(dev.data_ptr(), _lib.PC_I32, 1, len(beads), a, sp.grid_ptr,
+                                             kbuf.data_ptr(), 1, ctypes.byref(r), None))
+        assert r.error == 0
+        count, touched = int(r.count), int(r.cells_touched)
+        torch.cuda.synchronize()
+        assert np.array_equal(np.asarray(sp.cells).ravel(), occ.astype(np.uint32))
+        _lib.check(lib.pc_lattice_clear(sp.grid_ptr, a, None))
+    else:
+        rep = pc.count_collisions(beads, sp)
+        count, touched = rep.count, rep.cells_touched
+        assert np.array_equal(np.asarray(sp.cells).ravel(), occ.astype(np.uint32))
+        pc.reset_sparse(sp)
+    assert count == int((occ * (occ - 1) // 2).sum())
+    assert touched == int(np.count_nonzero(occ))
+    assert sp.is_zero()
+
+
 # ------------------------------------------------------------- lattice --
 
 def test_lattice_golden(golden_small):
