@@ -408,9 +408,11 @@ def _invsq_cases():
     yield "int64 near 2^40", ints
     yield "int64 two clusters", np.concatenate([ints, ints[:700] - np.int64(2**41)])
     yield "int32 spread", rng.integers(-2**30, 2**30, size=(800, 3)).astype(np.int32)
+    # n >= 16384: the big-tile compensated configuration
+    yield "f64 big config, offset cluster", rng.random((40_000, 3)) * 34.0 + np.array([5.0e3, -2.0e4, 7.0e2])
 
 
-@pytest.mark.parametrize("case", range(7))
+@pytest.mark.parametrize("case", range(8))
 def test_inverse_square_sum_tight_for_non_f32_inputs(case):
     # float64 / integer coordinates: the kernel must not lose the pair separation
     # to fp32 rounding of large coordinates (compensated hi+lo staging, DESIGN.md
