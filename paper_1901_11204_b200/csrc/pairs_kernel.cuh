@@ -57,10 +57,15 @@ __device__ __forceinline__ float4 col_lo(const float4* sp, int k) {  // (xl, yl,
 #ifndef PC_MINB
 #define PC_MINB 4
 #endif
+#ifndef PC_GRAM_UNROLL
+#define PC_GRAM_UNROLL 8
+#endif
 #ifndef PC_DIRECT_UNROLL
 #define PC_DIRECT_UNROLL 2
 #endif
 constexpr int kDirectUnroll = PC_DIRECT_UNROLL;
+constexpr int kGramUnroll = PC_GRAM_UNROLL;
+
 
 // dynamic shared memory per warp: 2 column buffers of W + one row buffer of T (PS/2 float4 per element)
 template <int R, int W, bool COMP = false>
@@ -68,11 +73,17 @@ constexpr int pairs_smem_per_warp() {
     return (2 * W + 32 * R) / 2 * (COMP ? 3 : 2) * (int)sizeof(float4);
 }
 
-template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP = false>
+// SLIM: one out-of-line copy of the slow path (rescan + exact re-check) instead
+// of one inlined copy per row.  Measured: the sum kernel is 2% faster slim; the
+// count kernel is 6% faster slim at N = 65,536 (most chunks flag a row, and the
+// unrolled slow path made the kernel 178 KB of SASS) but 2% slower at 2^20
+// (rare flags; the hot loop schedules better without the call).
+template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP = false, bool SLIM = true>
 __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsArgs a) {
     constexpr int T = 32 * R;
     constexpr int PS = COMP ? 3 : 2;  // float4 per column pair
     static_assert(DIRECT || !COMP, "compensated staging is for the direct (sum) formula");
+    constexpr bool kSingleRescan = SLIM;
     static_assert(W % 64 == 0 && T % 64 == 0, "buffers must hold whole pairs for every lane");
     extern __shared__ __align__(16) float4 s_dyn[];
     __shared__ unsigned long long s_red[WARPS][2];
@@ -259,7 +270,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             if (off + 1 >= T) {
                 // ---- Gram filter, packed: 3 FFMA2 + 1 FMNMX3 per two pairs.  Unowned
                 // cells past a row's window only cost a rescan if they are contacts.
-#pragma unroll 4
+#pragma unroll kGramUnroll
                 for (int k = 0; k < W; k += 2) {
                     const float4 A = sp[k], B = sp[k + 1];
                     const float2 cx = make_float2(A.x, A.y), cy = make_float2(A.z, A.w);
@@ -372,16 +383,14 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
         // (A lane-serial rescan cost ~800 instructions per flagged row and, 8x
         // unrolled, thrashed the I-cache at N = 65,536 where ~1 chunk in 1 flags.)
         if (__any_sync(0xffffffffu, fl != 0)) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                unsigned owners = __ballot_sync(0xffffffffu, (fl >> r) & 1u);
+            auto rescan = [&](float vx, float vy, float vz, float vc, int r, unsigned owners) {
                 while (owners) {
                     const int src = __ffs(owners) - 1;
                     owners &= owners - 1;
-                    const float qx = __shfl_sync(0xffffffffu, rx[r], src);
-                    const float qy = __shfl_sync(0xffffffffu, ry[r], src);
-                    const float qz = __shfl_sync(0xffffffffu, rz[r], src);
-                    const float qc = __shfl_sync(0xffffffffu, rc[r], src);
+                    const float qx = __shfl_sync(0xffffffffu, vx, src);
+                    const float qy = __shfl_sync(0xffffffffu, vy, src);
+                    const float qz = __shfl_sync(0xffffffffu, vz, src);
+                    const float qc = __shfl_sync(0xffffffffu, vc, src);
                     const int rl = r * 32 + src;
                     const int i = i0 + rl;
                     const int lim = bal ? steps_for_dev(n, i) : n - 1 - i;  // flagged rows are valid rows
@@ -399,7 +408,61 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                         }
                         if (cand && k < wc && (unsigned)(off + k - rl) < (unsigned)lim) {
                             ++checks;
-                            cnt += exact_pair(a.xyz, a.dtype, a.pred, i, bal ? wrap(j0 + k) : j0 + k) ? 1ull : 0ull;
+                            const int j = bal ? wrap(j0 + k) : j0 + k;
+                            cnt += (SLIM ? exact_pair_call(a.xyz, a.dtype, a.pred, i, j)
+                                         : exact_pair(a.xyz, a.dtype, a.pred, i, j)) ? 1ull : 0ull;
+                        }
+                    }
+                }
+            };
+            if (kSingleRescan) {
+                // one copy of the rescan for all R rows, the row's registers picked by
+                // an unrolled select (no dynamic register indexing)
+#pragma unroll 1
+                for (int r = 0; r < R; ++r) {
+                    const unsigned owners = __ballot_sync(0xffffffffu, (fl >> r) & 1u);
+                    if (!owners) continue;
+                    float vx = 0.f, vy = 0.f, vz = 0.f, vc = 0.f;
+#pragma unroll
+                    for (int rr = 0; rr < R; ++rr)
+                        if (rr == r) {
+                            vx = rx[rr];
+                            vy = ry[rr];
+                            vz = rz[rr];
+                            vc = rc[rr];
+                        }
+                    rescan(vx, vy, vz, vc, r, owners);
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    unsigned owners = __ballot_sync(0xffffffffu, (fl >> r) & 1u);
+                    while (owners) {
+                        const int src = __ffs(owners) - 1;
+                        owners &= owners - 1;
+                        const float qx = __shfl_sync(0xffffffffu, rx[r], src);
+                        const float qy = __shfl_sync(0xffffffffu, ry[r], src);
+                        const float qz = __shfl_sync(0xffffffffu, rz[r], src);
+                        const float qc = __shfl_sync(0xffffffffu, rc[r], src);
+                        const int rl = r * 32 + src;
+                        const int i = i0 + rl;
+                        const int lim = bal ? steps_for_dev(n, i) : n - 1 - i;  // flagged rows are valid rows
+#pragma unroll 2
+                        for (int q = 0; q < W / 32; ++q) {
+                            const int k = q * 32 + lane;
+                            const float4 c0 = col_hi<COMP>(sp, k);
+                            bool cand;
+                            if (DIRECT) {
+                                const float dx = qx - c0.x, dy = qy - c0.y, dz = qz - c0.z;
+                                cand = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1.0f))) < thr2;
+                            } else {
+                                const float tt = fmaf(qz, c0.z, fmaf(qy, c0.y, fmaf(qx, c0.x, c0.w)));
+                                cand = force || tt > qc;
+                            }
+                            if (cand && k < wc && (unsigned)(off + k - rl) < (unsigned)lim) {
+                                ++checks;
+                                cnt += exact_pair(a.xyz, a.dtype, a.pred, i, bal ? wrap(j0 + k) : j0 + k) ? 1ull : 0ull;
+                            }
                         }
                     }
                 }
