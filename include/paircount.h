@@ -138,6 +138,19 @@ int pc_pairs_multi(const void* xyz_host, int32_t dtype, int64_t n, int32_t inter
                    int32_t tiling, int32_t ndev, const int32_t* devices, const int64_t* bounds,
                    pc_pairs_result* per_device, pc_pairs_result* total);
 
+/* All pairs of each of nvec small HOST vectors (vectors[v] -> lengths[v]
+ * points, dtype as pc_pairs) in one launch: the quadratic side of the
+ * reference's linear-vs-quadratic harness (bench_cli.py:129-179, one
+ * oracle_collisions call per vector there).  One CTA per vector with the
+ * vector in shared memory; the reference predicate in the reference's own
+ * arithmetic (float64 for collision_indicator and the inverse-square sum,
+ * int64 with wrap-around for the integer ones), so counts are exact.
+ * results[v]: count, sum (PC_COLLISION_INVSQ), pairs = n(n-1)/2; error
+ * PC_ERR_DOMAIN for non-finite coordinates, PC_ERR_ARG for a vector of more
+ * than 4096 points (run it through pc_pairs_host). */
+int pc_pairs_batch(const void* const* vectors, const int64_t* lengths, int32_t dtype, int32_t nvec,
+                   int32_t interaction, pc_pairs_result* results, void* stream);
+
 /* number of kernel launches the last pc_pairs* call on this thread issued */
 int32_t pc_last_launch_count(void);
 

@@ -39,7 +39,7 @@ DTYPE_CODES = {np.dtype(np.float32): PC_F32, np.dtype(np.float64): PC_F64,
 EXPORTED = (
     "pc_last_error", "pc_version", "pc_device_count", "pc_set_device", "pc_device_alloc",
     "pc_device_free", "pc_memcpy_h2d", "pc_memcpy_d2h", "pc_stream_sync",
-    "pc_pairs_workspace_bytes", "pc_pairs", "pc_pairs_async", "pc_pairs_host", "pc_pairs_multi",
+    "pc_pairs_workspace_bytes", "pc_pairs", "pc_pairs_async", "pc_pairs_host", "pc_pairs_multi", "pc_pairs_batch",
     "pc_last_launch_count", "pc_kernel_timing", "pc_kernel_timing_read", "pc_lattice_grid_cells", "pc_lattice_key_bytes",
     "pc_lattice_collisions", "pc_lattice_contacts", "pc_lattice_reset_keys", "pc_lattice_clear",
     "pc_lattice_collisions_batch", "pc_lattice_collisions_vectors",
@@ -82,6 +82,7 @@ _SIGS = {
     "pc_pairs_async": ([_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _sz, _vp, _vp], ctypes.c_int),
     "pc_pairs_host": ([_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
     "pc_pairs_multi": ([_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "pc_pairs_batch": ([_vp, _vp, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
     "pc_last_launch_count": ([], _i32),
     "pc_kernel_timing": ([_i32], ctypes.c_int),
     "pc_kernel_timing_read": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i32)], ctypes.c_int),
@@ -176,6 +177,22 @@ def pairs_multi(xyz: np.ndarray, interaction: int, schedule: int, devices, bound
     check(lib.pc_pairs_multi(arr.ctypes.data, DTYPE_CODES[arr.dtype], len(arr), interaction, schedule, tiling,
                              len(devs), devs.ctypes.data, b.ctypes.data, ctypes.addressof(per), ctypes.byref(tot)))
     return list(per), tot
+
+
+def pairs_batch(arrays, interaction: int):
+    """pc_pairs_batch over a list of C-contiguous (n, 3) arrays of one dtype; returns PairsResult[]."""
+    lib = load()
+    if not arrays:
+        return []
+    dt = arrays[0].dtype
+    if any(a.dtype != dt for a in arrays):
+        raise ValueError("pairs_batch needs one dtype for all vectors")
+    ptrs = np.array([a.__array_interface__["data"][0] for a in arrays], dtype=np.uintp)
+    lengths = np.array([len(a) for a in arrays], dtype=np.int64)
+    res = (PairsResult * len(arrays))()
+    check(lib.pc_pairs_batch(ptrs.ctypes.data, lengths.ctypes.data, DTYPE_CODES[dt], len(arrays), interaction,
+                             ctypes.addressof(res), None))
+    return list(res)
 
 
 def pairs_async(xyz_ptr: int, dtype_code: int, n: int, interaction: int, schedule: int, bounds_host: np.ndarray,

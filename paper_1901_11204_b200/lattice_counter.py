@@ -299,3 +299,26 @@ def oracle_collisions(beads) -> int:
 def oracle_contacts(beads) -> int:
     """Pairs at Manhattan distance exactly 1 (lattice_counter.py:244-255)."""
     return _integer_pairs(beads, _lib.PC_MANHATTAN1)
+
+
+def _integer_pairs_batch(vectors, interaction: int) -> list[int]:
+    arrays = [np.ascontiguousarray(as_bead_array(v)) for v in vectors]
+    out = []
+    for arr, r in zip(arrays, _lib.pairs_batch(arrays, interaction)):
+        if r.error == _lib.PC_ERR_ARG:  # too long for one CTA's shared memory: the full all-pairs path
+            out.append(_integer_pairs(arr, interaction))
+        else:
+            out.append(int(r.count))
+    return out
+
+
+def oracle_collisions_batch(vectors) -> list[int]:
+    """``[oracle_collisions(v) for v in vectors]`` in one GPU launch (one CTA
+    per vector, exact int64 compare) -- the quadratic side of the reference's
+    linear-vs-quadratic harness (bench_cli.py:129-179)."""
+    return _integer_pairs_batch(vectors, _lib.PC_COINCIDE)
+
+
+def oracle_contacts_batch(vectors) -> list[int]:
+    """``[oracle_contacts(v) for v in vectors]`` in one GPU launch."""
+    return _integer_pairs_batch(vectors, _lib.PC_MANHATTAN1)

@@ -72,7 +72,7 @@ def test_verify_quick_passes_and_is_deterministic(tmp_path, capsys):
 
 @pytest.mark.gpu
 def test_mismatch_exit_code(tmp_path, monkeypatch):
-    monkeypatch.setattr(bench_cli, "oracle_collisions", lambda beads: -1)
+    monkeypatch.setattr(bench_cli, "oracle_collisions_batch", lambda vectors: [-1 for _ in vectors])
     rc = main(["bench", "linear-vs-quadratic", "--sizes", "8", "--vectors", "1", "--reps", "1",
                "--out", str(tmp_path / "raw.csv")])
     assert rc == bench_cli.EXIT_MISMATCH

@@ -368,6 +368,32 @@ def test_batched_small_vectors():
     assert sp.is_zero()
 
 
+def test_batched_all_pairs_oracles():
+    # oracle_collisions_batch / oracle_contacts_batch == per-vector oracles (C oracle)
+    vectors = [gen.random_chain(n, 9000 + n + v)[0] for n in (1, 2, 3, 16, 64, 257, 1024, 4096) for v in range(6)]
+    vectors += [np.zeros((0, 3), dtype=np.int64), np.zeros((40, 3), dtype=np.int64),
+                np.array([[2**62, 0, 0], [-(2**62), 0, 0], [1, 0, 0], [0, 0, 0]], dtype=np.int64),  # wrap-around
+                gen.random_chain(5000, 3)[0]]                                                    # > 4096: fallback
+    cols = pc.oracle_collisions_batch(vectors)
+    cons = pc.oracle_contacts_batch(vectors)
+    for v, c, m in zip(vectors, cols, cons):
+        assert (c, m) == c_oracle.int_pairs(v), len(v)
+    # float predicates through the C ABI: exact count, float64 sum
+    rng = np.random.default_rng(4)
+    objs = [np.ascontiguousarray(rng.random((k, 3)) * (k ** (1 / 3)) * 1.2) for k in (2, 5, 100, 777, 4096)]
+    objs.append(np.array([[0.0, 0.0, 0.0], [np.nan, 0.0, 0.0]]))
+    for code in (_lib.PC_COLLISION, _lib.PC_COLLISION_INVSQ):
+        res = _lib.pairs_batch(objs, code)
+        for o, r in zip(objs, res):
+            if not np.isfinite(o).all():
+                assert r.error == _lib.PC_ERR_DOMAIN
+                continue
+            want_c, want_s, pairs = c_oracle.rows(o, 0, len(o), "balanced")
+            assert (r.error, r.count, r.pairs) == (0, want_c, pairs)
+            if code == _lib.PC_COLLISION_INVSQ:
+                assert r.sum == pytest.approx(want_s, rel=1e-12)
+
+
 def test_batch_entry_points_agree():
     # pc_lattice_collisions_vectors (separate host vectors, int32 and int64) ==
     # pc_lattice_collisions_batch (one packed array + offsets)
