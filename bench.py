@@ -336,6 +336,11 @@ def secondary(torch, lib, stream):
     for _ in range(reps):
         got = lc.count_collisions_batch(chains, sp)
     gpu_ms = (time.perf_counter() - t0) / reps * 1e3
+    lc.oracle_collisions_batch(chains[:8])
+    t0 = time.perf_counter()
+    quad = lc.oracle_collisions_batch(chains)
+    quad_ms = (time.perf_counter() - t0) * 1e3
+    assert quad == [r.count for r in got]
     cells_np = npo.new_dense_space(ext)
     t0 = time.perf_counter()
     cpu = [npo.count_collisions_dense(c, cells_np, ext)[0] for c in chains[:100]]  # reference _linear_pass step
@@ -343,6 +348,9 @@ def secondary(torch, lib, stream):
     assert [r.count for r in got[:100]] == cpu
     out["many_vectors_1000x1024_chains"] = {
         "gpu_ms_per_execution": gpu_ms, "path": "count_collisions_batch from host arrays (H2D + 1 launch + D2H)",
+        "gpu_quadratic_ms_per_execution": quad_ms,
+        "quadratic_path": "oracle_collisions_batch: all 1000 x C(1024,2) pairs, one launch (the linear-vs-quadratic "
+                          "harness's other side; counts equal)",
         "cpu_baseline_ms_per_execution": cpu_ms, "cpu_baseline": "oracle numpy port of the reference's dense-grid "
         "count_collisions + reset_sparse, 100 of the 1000 vectors timed on 1 core, x10",
         "collisions_total": int(sum(r.count for r in got))}
