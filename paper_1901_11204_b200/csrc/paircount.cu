@@ -425,7 +425,7 @@ constexpr KernelCfg kBigGram{4, PC_GRAM_R, PC_GRAM_W};  // count kernel: 384-row
 constexpr KernelCfg kBigComp{4, 4, PC_COMP_W};          // compensated sum kernel (non-f32 input): 6 row registers per row
 constexpr KernelCfg kSmall{4, 2, 64};  // warp tile 64 rows, for n < kSmallN
 constexpr int kSmallN = 16384;
-constexpr long long kSlimGramN = 1LL << 18;  // count kernel: slim slow path below (pairs_kernel.cuh, SLIM)
+
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -466,9 +466,9 @@ int num_sms() {
     return g_num_sms[dev];
 }
 
-template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP, bool SLIM>
+template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP>
 int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStream_t s) {
-    auto kern = pairs_kernel<WARPS, R, W, DIRECT, FLAT, COMP, SLIM>;
+    auto kern = pairs_kernel<WARPS, R, W, DIRECT, FLAT, COMP>;
     constexpr int smem = WARPS * pairs_smem_per_warp<R, W, COMP>();
     {
         static thread_local bool attr_set[64] = {false};
@@ -517,16 +517,16 @@ int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStr
     return PC_OK;
 }
 
-template <int WARPS, int R, int W, bool DIRECT, bool COMP = false, bool SLIM = true>
+template <int WARPS, int R, int W, bool DIRECT, bool COMP = false>
 int dispatch_cfg(PairsArgs args, bool flat, long long cap, int* nslots, cudaStream_t s) {
     constexpr int T = 32 * R;
     args.n_tiles = (args.hi - args.lo + T - 1) / T;
     if (flat) {
         args.L = (long long)(T - 1) + (args.n >> 1);
         args.total = (long long)args.n_tiles * args.L;
-        return launch_pairs<WARPS, R, W, DIRECT, true, COMP, SLIM>(args, cap, nslots, s);
+        return launch_pairs<WARPS, R, W, DIRECT, true, COMP>(args, cap, nslots, s);
     }
-    return launch_pairs<WARPS, R, W, DIRECT, false, COMP, SLIM>(args, cap, nslots, s);
+    return launch_pairs<WARPS, R, W, DIRECT, false, COMP>(args, cap, nslots, s);
 }
 
 int run_pairs(const void* xyz, int dtype, long long n, int interaction, int schedule, int tiling,
@@ -596,9 +596,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
             else
                 rc = comp     ? dispatch_cfg<kBigComp.warps, kBigComp.r, kBigComp.w, true, true>(args, flat, cap, &nslots, s)
                      : direct ? dispatch_cfg<kBig.warps, kBig.r, kBig.w, true>(args, flat, cap, &nslots, s)
-                     : n < kSlimGramN
-                         ? dispatch_cfg<kBigGram.warps, kBigGram.r, kBigGram.w, false, false, true>(args, flat, cap, &nslots, s)
-                         : dispatch_cfg<kBigGram.warps, kBigGram.r, kBigGram.w, false, false, false>(args, flat, cap, &nslots, s);
+                              : dispatch_cfg<kBigGram.warps, kBigGram.r, kBigGram.w, false>(args, flat, cap, &nslots, s);
             if (rc) return rc;
         }
         finalize_kernel<<<1, 256, 0, s>>>(slots, nslots, st, row_pairs(n, lo, hi, schedule), direct ? 1 : 0, dres + k);

@@ -73,17 +73,11 @@ constexpr int pairs_smem_per_warp() {
     return (2 * W + 32 * R) / 2 * (COMP ? 3 : 2) * (int)sizeof(float4);
 }
 
-// SLIM: one out-of-line copy of the slow path (rescan + exact re-check) instead
-// of one inlined copy per row.  Measured: the sum kernel is 2% faster slim; the
-// count kernel is 6% faster slim at N = 65,536 (most chunks flag a row, and the
-// unrolled slow path made the kernel 178 KB of SASS) but 2% slower at 2^20
-// (rare flags; the hot loop schedules better without the call).
-template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP = false, bool SLIM = true>
+template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP = false>
 __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsArgs a) {
     constexpr int T = 32 * R;
     constexpr int PS = COMP ? 3 : 2;  // float4 per column pair
     static_assert(DIRECT || !COMP, "compensated staging is for the direct (sum) formula");
-    constexpr bool kSingleRescan = SLIM;
     static_assert(W % 64 == 0 && T % 64 == 0, "buffers must hold whole pairs for every lane");
     extern __shared__ __align__(16) float4 s_dyn[];
     __shared__ unsigned long long s_red[WARPS][2];
@@ -409,63 +403,30 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                         if (cand && k < wc && (unsigned)(off + k - rl) < (unsigned)lim) {
                             ++checks;
                             const int j = bal ? wrap(j0 + k) : j0 + k;
-                            cnt += (SLIM ? exact_pair_call(a.xyz, a.dtype, a.pred, i, j)
-                                         : exact_pair(a.xyz, a.dtype, a.pred, i, j)) ? 1ull : 0ull;
+                            cnt += exact_pair_call(a.xyz, a.dtype, a.pred, i, j) ? 1ull : 0ull;
                         }
                     }
                 }
             };
-            if (kSingleRescan) {
-                // one copy of the rescan for all R rows, the row's registers picked by
-                // an unrolled select (no dynamic register indexing)
+            // One out-of-line copy of the rescan and the exact re-check for all R
+            // rows, the row's registers picked by an unrolled select (no dynamic
+            // register indexing).  Inlined once per row the kernel was 178 KB of
+            // SASS; slim it is 1.4% faster for the sum, 8% for the count at
+            // N = 65,536 and 7% on the clustered 2^22 set (most chunks flag a row).
 #pragma unroll 1
-                for (int r = 0; r < R; ++r) {
-                    const unsigned owners = __ballot_sync(0xffffffffu, (fl >> r) & 1u);
-                    if (!owners) continue;
-                    float vx = 0.f, vy = 0.f, vz = 0.f, vc = 0.f;
+            for (int r = 0; r < R; ++r) {
+                const unsigned owners = __ballot_sync(0xffffffffu, (fl >> r) & 1u);
+                if (!owners) continue;
+                float vx = 0.f, vy = 0.f, vz = 0.f, vc = 0.f;
 #pragma unroll
-                    for (int rr = 0; rr < R; ++rr)
-                        if (rr == r) {
-                            vx = rx[rr];
-                            vy = ry[rr];
-                            vz = rz[rr];
-                            vc = rc[rr];
-                        }
-                    rescan(vx, vy, vz, vc, r, owners);
-                }
-            } else {
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    unsigned owners = __ballot_sync(0xffffffffu, (fl >> r) & 1u);
-                    while (owners) {
-                        const int src = __ffs(owners) - 1;
-                        owners &= owners - 1;
-                        const float qx = __shfl_sync(0xffffffffu, rx[r], src);
-                        const float qy = __shfl_sync(0xffffffffu, ry[r], src);
-                        const float qz = __shfl_sync(0xffffffffu, rz[r], src);
-                        const float qc = __shfl_sync(0xffffffffu, rc[r], src);
-                        const int rl = r * 32 + src;
-                        const int i = i0 + rl;
-                        const int lim = bal ? steps_for_dev(n, i) : n - 1 - i;  // flagged rows are valid rows
-#pragma unroll 2
-                        for (int q = 0; q < W / 32; ++q) {
-                            const int k = q * 32 + lane;
-                            const float4 c0 = col_hi<COMP>(sp, k);
-                            bool cand;
-                            if (DIRECT) {
-                                const float dx = qx - c0.x, dy = qy - c0.y, dz = qz - c0.z;
-                                cand = fmaf(dz, dz, fmaf(dy, dy, fmaf(dx, dx, 1.0f))) < thr2;
-                            } else {
-                                const float tt = fmaf(qz, c0.z, fmaf(qy, c0.y, fmaf(qx, c0.x, c0.w)));
-                                cand = force || tt > qc;
-                            }
-                            if (cand && k < wc && (unsigned)(off + k - rl) < (unsigned)lim) {
-                                ++checks;
-                                cnt += exact_pair(a.xyz, a.dtype, a.pred, i, bal ? wrap(j0 + k) : j0 + k) ? 1ull : 0ull;
-                            }
-                        }
+                for (int rr = 0; rr < R; ++rr)
+                    if (rr == r) {
+                        vx = rx[rr];
+                        vy = ry[rr];
+                        vz = rz[rr];
+                        vc = rc[rr];
                     }
-                }
+                rescan(vx, vy, vz, vc, r, owners);
             }
         }
         __syncwarp();  // the buffer just read is restaged next iteration

@@ -1,6 +1,6 @@
 """Run each hot kernel a few times on its benchmark size, for ncu captures.
 
-    python scripts/profile_kernels.py [direct|gram|gram_std|cfg2|lattice|all] [--reps R]
+    python scripts/profile_kernels.py [direct|gram|gram_std|cfg2|cfg4|lattice|all] [--reps R]
 
 Prints one timing line per case (CUDA events around the main kernel via
 pc_kernel_timing); the numbers under ncu are not bench values.
@@ -25,8 +25,9 @@ from paper_1901_11204_b200 import _lib  # noqa: E402
 from paper_1901_11204_b200 import generators as gen  # noqa: E402
 
 
-def pairs_case(name, n, interaction, schedule, tiling, reps, seed=1):
-    obj = gen.random_spheres(n, gen.contact_box_edge(n), seed).astype(np.float32)
+def pairs_case(name, n, interaction, schedule, tiling, reps, seed=1, obj=None):
+    if obj is None:
+        obj = gen.random_spheres(n, gen.contact_box_edge(n), seed).astype(np.float32)
     d = torch.from_numpy(obj).cuda()
     ws = torch.empty(_lib.workspace_bytes(n), dtype=torch.uint8, device="cuda")
     res = torch.zeros(8, dtype=torch.int64, device="cuda")
@@ -84,6 +85,9 @@ def main():
         pairs_case("gram_naive_2^20", 2**20, _lib.PC_COLLISION, _lib.PC_STANDARD, _lib.PC_TILE_PER_ROW_TILE, a.reps)
     if w in ("cfg2", "all"):
         pairs_case("gram_flat_65536", 65536, _lib.PC_COLLISION, _lib.PC_BALANCED, _lib.PC_TILE_FLAT, a.reps, seed=0)
+    if w in ("cfg4", "all"):
+        pairs_case("gram_flat_clustered_2^22", 2**22, _lib.PC_COLLISION, _lib.PC_BALANCED, _lib.PC_TILE_FLAT, a.reps,
+                   obj=gen.clustered_spheres(2**22).astype(np.float32))
     if w in ("lattice", "all"):
         lattice_case(a.reps)
     if w in ("micro", "all"):
