@@ -290,6 +290,20 @@ def secondary(torch, lib, stream):
         "hbm_frac_of_measured": b_alg / (ms * 1e-3) / 1e9 / hbm,
         "note": "scattered global atomics would cap this at ~21 G beads/s (scripts/microbench_l2atomic.cu)"}
     del d5, grid, keys
+    # the same step through the drop-in API from host int64 beads (the reference's own input)
+    from paper_1901_11204_b200 import lattice_counter as lc
+
+    pts64 = np.ascontiguousarray(pts.astype(np.int64))
+    sp5 = lc.new_space(a5)
+    for rep in range(2):
+        t0 = time.perf_counter()
+        rep5 = lc.count_collisions(pts64, sp5)
+        lc.reset_sparse(sp5)
+        api_ms = (time.perf_counter() - t0) * 1e3
+    out["cfg5_counting_array_n2^26"].update({
+        "api_wall_ms": api_ms, "api_count": rep5.count,
+        "api_path": "count_collisions(int64 host beads, space) + reset_sparse: H2D of 1.61 GB + the device step"})
+    del sp5, pts64
 
     # ---- config 4: 2^22 clustered points, count; the per-rank slabs of a 2/4/8-GPU split timed
     # one after another on this GPU (ranks never wait on each other: the only exchange is the final

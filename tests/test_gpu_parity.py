@@ -503,3 +503,22 @@ def test_boundary_stress_random_offsets(trial):
         assert se.spi_balanced(arr, se.collision_indicator).total == want_c
         (r,) = _lib.pairs_host(np.ascontiguousarray(arr), _lib.PC_COLLISION_INVSQ, _lib.PC_STANDARD, [0, len(arr)])
         assert r.count == want_c and _close(r.sum, want_s)
+
+
+def test_large_host_int64_beads_narrowed_exactly():
+    # a large int64 host vector (dense regime, 9.6 MB): counts exact, and a bead
+    # beyond int32 or just outside the cube is still reported by its index
+    rng = np.random.default_rng(8)
+    beads = rng.integers(-40, 41, size=(400_000, 3))
+    sp = pc.new_space(40)
+    rep = pc.count_collisions(beads, sp)
+    keys = np.ravel_multi_index(tuple((beads + 41).T), (83, 83, 83))
+    occ = np.bincount(keys)
+    assert rep.count == int((occ * (occ - 1) // 2).sum()) and rep.cells_touched == np.count_nonzero(occ)
+    pc.reset_sparse(sp)
+    for bad in (2**32 + 5, -(2**40), 41):
+        b2 = beads.copy()
+        b2[250_001, 1] = bad
+        with pytest.raises(lc.CoordinateRangeError, match="bead 250001"):
+            pc.count_collisions(b2, sp)
+        assert sp.is_zero()
