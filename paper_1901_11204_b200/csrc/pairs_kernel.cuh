@@ -54,6 +54,38 @@ __device__ __forceinline__ float4 col_lo(const float4* sp, int k) {  // (xl, yl,
     return (k & 1) ? make_float4(B.w, C.y, C.w, 0.f) : make_float4(B.z, C.x, C.z, 0.f);
 }
 
+// ---- TMA bulk staging (cp.async.bulk global -> shared, completion on an mbarrier)
+#ifndef PC_TMA_STAGE
+#define PC_TMA_STAGE 1
+#endif
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+    unsigned spins = 0;
+    while (!mbar_try_wait(bar, parity))
+        if (++spins == (1u << 28)) __trap();  // a lost transaction must fail loudly, never hang the GPU
+}
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned bytes, unsigned bar) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(d), "l"(gsrc), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_shared() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 #ifndef PC_MINB
 #define PC_MINB 4
 #endif
@@ -81,6 +113,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     static_assert(W % 64 == 0 && T % 64 == 0, "buffers must hold whole pairs for every lane");
     extern __shared__ __align__(16) float4 s_dyn[];
     __shared__ unsigned long long s_red[WARPS][2];
+    __shared__ __align__(8) unsigned long long s_bar[WARPS][2];  // per-warp TMA completion, one per column buffer
     __shared__ double s_sum[WARPS];
 
     const int lane = threadIdx.x & 31;
@@ -198,16 +231,76 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     unsigned long long cnt = 0, checks = 0;
     double sum = 0.0;
 
+    // Staging of chunk (t, o, wcn) into column buffer b, with the tile's rows when asked.  A full
+    // chunk whose window does not wrap is ONE contiguous run of pair entries, and a whole row tile
+    // is one too: lane 0 hands each to a TMA bulk copy that completes on the buffer's mbarrier.
+    // Ragged chunks (partial, wrapping, odd width) and the last row tile take per-lane cp.async.
+    // TMA staging is on for the sum kernel (+1.0 %); the count kernel keeps per-lane cp.async, where
+    // the extra live state cost 1.5 % (it runs at 128 registers).
+    constexpr bool kTma = PC_TMA_STAGE && DIRECT;
+    const unsigned bar_base = (unsigned)__cvta_generic_to_shared(&s_bar[wid][0]);
+    if (kTma) {
+        if (lane == 0) {
+            mbar_init(bar_base, 1);
+            mbar_init(bar_base + 8, 1);
+            mbar_init_fence();
+        }
+        __syncwarp();
+    }
+    unsigned pend = 0;  // bit b: TMA in flight into buffer b; bit 2: a cp.async group in flight
+    unsigned phase = 0; // bit b: parity of buffer b's next mbarrier phase
+    auto stage = [&](int b, int t, int o, int wcn, bool rows) {
+        const int i0n = a.lo + t * T;
+        int jw = i0n + o + 1;
+        if (bal) jw = wrap(jw);
+        const bool cols_tma = kTma && wcn == W && jw + W - 1 < n;
+        const bool rows_tma = kTma && rows && i0n + T <= n;
+        if (cols_tma || rows_tma) {
+            if (lane == 0) {
+                fence_proxy_async_shared();  // this warp's earlier generic reads of the buffers come first
+                const unsigned cb = cols_tma ? W / 2 * PS * 16 : 0u, rb = rows_tma ? T / 2 * PS * 16 : 0u;
+                const unsigned bar = bar_base + 8u * b;
+                mbar_expect_tx(bar, cb + rb);
+                if (cols_tma) bulk_g2s(sp0 + b * (W / 2 * PS), pair_src(jw), cb, bar);
+                if (rows_tma) bulk_g2s(rowbuf, pair_src(i0n), rb, bar);
+            }
+            pend |= 1u << b;
+        }
+        if (!cols_tma || (rows && !rows_tma)) {
+            if (!cols_tma) stage_cols(b, t, o, wcn);
+            if (rows && !rows_tma) stage_rows(t);
+            cp_async_commit();
+            pend |= 4u;
+        }
+    };
+
     int wc = left > 0 ? width(off, left) : 0;
     if (left > 0) {
-        stage_rows(tile);
-        stage_cols(0, tile, off, wc);
-        cp_async_commit();
+        if (kTma) {
+            stage(0, tile, off, wc, true);
+        } else {
+            stage_rows(tile);
+            stage_cols(0, tile, off, wc);
+            cp_async_commit();
+        }
     }
     int buf = 0;
     int staged_tile = tile;  // tile whose rows the row buffer receives / holds
     while (left > 0) {
-        cp_async_wait<0>();  // chunk `buf` (and, on a switch, its tile's rows) landed
+        // chunk `buf` (and, on a switch, its tile's rows) landed
+        if (kTma) {
+            if (pend & 4u) {
+                cp_async_wait<0>();
+                pend &= ~4u;
+            }
+            if (pend & (1u << buf)) {
+                mbar_wait(bar_base + 8u * buf, (phase >> buf) & 1u);
+                phase ^= 1u << buf;
+                pend &= ~(1u << buf);
+            }
+        } else {
+            cp_async_wait<0>();
+        }
         __syncwarp();
         const int i0 = a.lo + tile * T;
         if (tile != cur_tile) {
@@ -243,12 +336,18 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
         if (FLAT && nleft == 0) claim(ntile, noff, nleft);
         const int nwc = nleft > 0 ? width(noff, nleft) : 0;
         if (nleft > 0) {
-            if (ntile != staged_tile) {
-                stage_rows(ntile);
+            if (kTma) {
+                const bool new_rows = ntile != staged_tile;
                 staged_tile = ntile;
+                stage(buf ^ 1, ntile, noff, nwc, new_rows);
+            } else {
+                if (ntile != staged_tile) {
+                    stage_rows(ntile);
+                    staged_tile = ntile;
+                }
+                stage_cols(buf ^ 1, ntile, noff, nwc);
+                cp_async_commit();
             }
-            stage_cols(buf ^ 1, ntile, noff, nwc);
-            cp_async_commit();
         }
 
         const float4* sp = sp0 + buf * (W / 2 * PS);
