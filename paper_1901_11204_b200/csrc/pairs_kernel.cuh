@@ -55,6 +55,9 @@ __device__ __forceinline__ float4 col_lo(const float4* sp, int k) {  // (xl, yl,
 }
 
 // ---- TMA bulk staging (cp.async.bulk global -> shared, completion on an mbarrier)
+#ifndef PC_TMA_GRAM
+#define PC_TMA_GRAM 0
+#endif
 #ifndef PC_TMA_STAGE
 #define PC_TMA_STAGE 1
 #endif
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     // Ragged chunks (partial, wrapping, odd width) and the last row tile take per-lane cp.async.
     // TMA staging is on for the sum kernel (+1.0 %); the count kernel keeps per-lane cp.async, where
     // the extra live state cost 1.5 % (it runs at 128 registers).
-    constexpr bool kTma = PC_TMA_STAGE && DIRECT;
+    constexpr bool kTma = PC_TMA_STAGE && (DIRECT || PC_TMA_GRAM);
     const unsigned bar_base = (unsigned)__cvta_generic_to_shared(&s_bar[wid][0]);
     if (kTma) {
         if (lane == 0) {
