@@ -489,9 +489,11 @@ def run_ours(args):
     peak_tflops = 2.0 * ffma_rate / 1e12
     traffic = None
     tfile = ROOT / "profiles" / "kernel_traffic.json"
+    tinfo = {}
     if tfile.exists():
         try:
-            traffic = json.loads(tfile.read_text()).get("pairs_kernel_direct_flat_n2^20")
+            tinfo = json.loads(tfile.read_text())
+            traffic = tinfo.get("pairs_kernel_direct_flat_n2^20")
         except (ValueError, OSError):
             traffic = None
     clocks = clk.summary()
@@ -500,7 +502,12 @@ def run_ours(args):
                 "kernel": "pairs_kernel<128,8,256,DIRECT,FLAT>", "kernel_ms": kern_ms_avg,
                 "flops_per_pair": FLOPS_PER_PAIR,
                 "peak_source": "measured live: pc_microbench FFMA stream x 2 flop (no FP32 entry in MEASURED_PEAKS.json)",
-                "pairs_per_s_kernel": rank_pairs / (kern_ms_avg * 1e-3)}
+                "pairs_per_s_kernel": rank_pairs / (kern_ms_avg * 1e-3),
+                # the same kernel against the pipe it is bound by: FMA-pipe lane operations it issues per pair
+                # (15 FFMA2-class per 4 pairs = 7.5) x pairs/s / the live FFMA lane rate; DESIGN.md §3
+                "fma_pipe": {"lane_ops_per_pair": 7.5,
+                             "frac": 7.5 * rank_pairs / (kern_ms_avg * 1e-3) / ffma_rate,
+                             "ncu_fma_pipe_active": tinfo.get("pairs_kernel_direct_fma_pipe_active")}}
 
     line = {
         "metric": "G pair-tests/s at N=2^20 (contact count + inverse-square sum)",
