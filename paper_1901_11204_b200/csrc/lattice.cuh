@@ -1,0 +1,451 @@
+// Counting array (Alg. 1 / Alg. 2): lattice kernels and the host driver.
+// Included by paircount.cu inside its anonymous namespace.
+
+// ------------------------------------------------------------------------
+// counting array (Alg. 1 / Alg. 2)
+// ------------------------------------------------------------------------
+struct LatSlot {
+    unsigned long long a, b;
+};
+constexpr unsigned long long kNoBad = ~0ull;
+
+template <typename KT>
+__global__ void lat_keys_kernel(const void* __restrict__ xyz, int dtype, long long n, long long a, long long side,
+                                KT* __restrict__ keys, unsigned long long* __restrict__ bad) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long x = coord_i64(xyz, dtype, i, 0), y = coord_i64(xyz, dtype, i, 1),
+                        z = coord_i64(xyz, dtype, i, 2);
+        if (x < -a || x > a || y < -a || y > a || z < -a || z > a) {  // _validate, lattice_counter.py:98-105
+            atomicMin(bad, (unsigned long long)i);
+        } else if (keys) {
+            keys[i] = (KT)(((x + a + 1) * side + (y + a + 1)) * side + (z + a + 1));  // _flatten, :107-111
+        }
+    }
+}
+
+// Alg. 1 on a clean grid: collisions += space[b]; space[b]++  
+template <typename KT>
+__global__ void lat_place_clean_kernel(const KT* __restrict__ keys, long long n, unsigned* __restrict__ grid,
+                                       const unsigned long long* __restrict__ bad, LatSlot* __restrict__ slots,
+                                       int* __restrict__ overflow) {
+    __shared__ unsigned long long s_a[8], s_b[8];
+    unsigned long long cnt = 0, first = 0;
+    int ovf = 0;
+    if (*bad == kNoBad) {
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+             i += (long long)gridDim.x * blockDim.x) {
+            const unsigned old = atomicAdd(grid + keys[i], 1u);
+            cnt += old;
+            first += old == 0u;
+            ovf |= old >= 0xfffffffeu;
+        }
+    }
+    cnt = warp_sum(cnt);
+    first = warp_sum(first);
+    if (__any_sync(0xffffffffu, ovf) && (threadIdx.x & 31) == 0) atomicOr(overflow, 1);
+    if ((threadIdx.x & 31) == 0) { s_a[threadIdx.x >> 5] = cnt; s_b[threadIdx.x >> 5] = first; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        LatSlot sl{0, 0};
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { sl.a += s_a[q]; sl.b += s_b[q]; }
+        slots[blockIdx.x] = sl;
+    }
+}
+
+template <typename KT>
+__global__ void lat_place_kernel(const KT* __restrict__ keys, long long n, unsigned* __restrict__ grid,
+                                 const unsigned long long* __restrict__ bad) {
+    if (*bad != kNoBad) return;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        atomicAdd(grid + keys[i], 1u);
+}
+
+// sum over beads of (final occupancy - 1) (lattice_counter.py:151-153); b = overflow flag
+template <typename KT>
+__global__ void lat_gather_kernel(const KT* __restrict__ keys, long long n, const unsigned* __restrict__ grid,
+                                  const unsigned long long* __restrict__ bad, LatSlot* __restrict__ slots,
+                                  int* __restrict__ overflow) {
+    __shared__ unsigned long long s_a[8];
+    unsigned long long acc = 0;
+    int ovf = 0;
+    if (*bad == kNoBad) {
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+             i += (long long)gridDim.x * blockDim.x) {
+            const unsigned occ = grid[keys[i]];
+            acc += (unsigned long long)occ - 1ull;
+            ovf |= occ >= 0xffffffffu;
+        }
+    }
+    acc = warp_sum(acc);
+    if (__any_sync(0xffffffffu, ovf) && (threadIdx.x & 31) == 0) atomicOr(overflow, 1);
+    if ((threadIdx.x & 31) == 0) s_a[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        LatSlot sl{0, 0};
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) sl.a += s_a[q];
+        slots[blockIdx.x] = sl;
+    }
+}
+
+// Alg. 2 second loop: six axial neighbour occupancies per bead
+template <typename KT>
+__global__ void lat_neighbours_kernel(const KT* __restrict__ keys, long long n, long long side,
+                                      const unsigned* __restrict__ grid, const unsigned long long* __restrict__ bad,
+                                      LatSlot* __restrict__ slots) {
+    __shared__ unsigned long long s_a[8];
+    unsigned long long acc = 0;
+    if (*bad == kNoBad) {
+        const long long d2 = side * side;
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+             i += (long long)gridDim.x * blockDim.x) {
+            const long long k = (long long)keys[i];
+            acc += (unsigned long long)grid[k + d2] + grid[k - d2] + grid[k + side] + grid[k - side] +
+                   grid[k + 1] + grid[k - 1];
+        }
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) s_a[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        LatSlot sl{0, 0};
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) sl.a += s_a[q];
+        slots[blockIdx.x] = sl;
+    }
+}
+
+// Distinct-cell count by marking bit 31 of every read cell (own cell, and the
+// six neighbours when `with_neighbours`), counting first markers; a second
+// call with unmark=1 clears the marks.  Occupancies never reach 2^31 here
+// (overflow is reported first).
+template <typename KT>
+__global__ void lat_mark_kernel(const KT* __restrict__ keys, long long n, long long side, int with_neighbours,
+                                int unmark, unsigned* __restrict__ grid, const unsigned long long* __restrict__ bad,
+                                LatSlot* __restrict__ slots) {
+    __shared__ unsigned long long s_a[8];
+    unsigned long long firsts = 0;
+    if (*bad == kNoBad) {
+        const long long d2 = side * side;
+        const long long offs[7] = {0, d2, -d2, side, -side, 1, -1};
+        const int m = with_neighbours ? 7 : 1;
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+             i += (long long)gridDim.x * blockDim.x) {
+            const long long k = (long long)keys[i];
+            for (int q = 0; q < m; ++q) {
+                if (unmark) atomicAnd(grid + k + offs[q], 0x7fffffffu);
+                else firsts += (atomicOr(grid + k + offs[q], 0x80000000u) & 0x80000000u) ? 0ull : 1ull;
+            }
+        }
+    }
+    firsts = warp_sum(firsts);
+    if ((threadIdx.x & 31) == 0) s_a[threadIdx.x >> 5] = firsts;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        LatSlot sl{0, 0};
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) sl.a += s_a[q];
+        slots[blockIdx.x] = sl;
+    }
+}
+
+template <typename KT>
+__global__ void lat_zero_keys_kernel(const KT* __restrict__ keys, long long n, unsigned* __restrict__ grid) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        grid[keys[i]] = 0u;
+}
+
+__global__ void lat_zero_beads_kernel(const void* __restrict__ xyz, int dtype, long long n, long long a, long long side,
+                                      unsigned* __restrict__ grid, const unsigned long long* __restrict__ bad) {
+    if (*bad != kNoBad) return;
+    const long long d2 = side * side;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long k = ((coord_i64(xyz, dtype, i, 0) + a + 1) * side + (coord_i64(xyz, dtype, i, 1) + a + 1)) * side +
+                            (coord_i64(xyz, dtype, i, 2) + a + 1);
+        grid[k] = 0u; grid[k + d2] = 0u; grid[k - d2] = 0u; grid[k + side] = 0u;
+        grid[k - side] = 0u; grid[k + 1] = 0u; grid[k - 1] = 0u;
+    }
+}
+
+__global__ void lat_sum_slots_kernel(const LatSlot* __restrict__ slots, int nslots, unsigned long long* __restrict__ out) {
+    __shared__ unsigned long long sa[256], sb[256];
+    unsigned long long x = 0, y = 0;
+    for (int q = threadIdx.x; q < nslots; q += blockDim.x) { x += slots[q].a; y += slots[q].b; }
+    sa[threadIdx.x] = x; sb[threadIdx.x] = y;
+    __syncthreads();
+    for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h) { sa[threadIdx.x] += sa[threadIdx.x + h]; sb[threadIdx.x] += sb[threadIdx.x + h]; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) { out[0] = sa[0]; out[1] = sb[0]; }
+}
+
+__global__ void count_nonzero_kernel(const uint4* __restrict__ grid4, long long n4, const unsigned* __restrict__ tail,
+                                     int ntail, unsigned long long* __restrict__ out) {
+    unsigned long long c = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+        const uint4 v = grid4[i];
+        c += (v.x != 0u) + (v.y != 0u) + (v.z != 0u) + (v.w != 0u);
+    }
+    if (blockIdx.x == 0 && (int)threadIdx.x < ntail) c += tail[threadIdx.x] != 0u;
+    c = warp_sum(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+// Scratch layout for one lattice call: [coords copy][bad u64][overflow int][slots][sums]
+#include "lattice_slab.cuh"
+
+// ---- batched small vectors (the paper's 100-1000 vectors per execution) ----
+// One CTA per vector; Alg. 1 (collisions += space[b]; space[b]++) on a
+// shared-memory counting array addressed by an open-addressing hash of the
+// cell key (the dense (2a+3)^3 grid does not fit on chip).  Equivalent to
+// count_collisions + reset_sparse per vector on a clean space.
+constexpr int kBatchSlots = 8192;  // vectors up to kBatchSlots/2 beads; larger ones go through the grid
+constexpr unsigned long long kEmptyKey = ~0ull;
+constexpr int kBatchSmem = kBatchSlots * 12;
+
+__global__ void __launch_bounds__(256) lat_batch_kernel(const void* __restrict__ xyz, int dtype,
+                                                        const long long* __restrict__ offs, int nvec, long long a,
+                                                        long long side, unsigned long long* __restrict__ out) {
+    extern __shared__ unsigned long long tkey[];  // [kBatchSlots] keys, then [kBatchSlots] uint32 counts
+    unsigned* tcnt = reinterpret_cast<unsigned*>(tkey + kBatchSlots);
+    __shared__ unsigned long long s_acc[8], s_first[8];
+    __shared__ long long s_bad;
+    for (int v = blockIdx.x; v < nvec; v += gridDim.x) {
+        const long long lo = offs[v], hi = offs[v + 1];
+        for (int q = threadIdx.x; q < kBatchSlots; q += blockDim.x) {
+            tkey[q] = kEmptyKey;
+            tcnt[q] = 0u;
+        }
+        if (threadIdx.x == 0) s_bad = -1;
+        __syncthreads();
+        unsigned long long acc = 0, first = 0;
+        if (hi - lo <= kBatchSlots / 2) {
+            for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+                const long long x = coord_i64(xyz, dtype, i, 0), y = coord_i64(xyz, dtype, i, 1),
+                                z = coord_i64(xyz, dtype, i, 2);
+                if (x < -a || x > a || y < -a || y > a || z < -a || z > a) {
+                    atomicMin((unsigned long long*)&s_bad, (unsigned long long)(i - lo));
+                    continue;
+                }
+                const unsigned long long key = (unsigned long long)(((x + a + 1) * side + (y + a + 1)) * side + (z + a + 1));
+                unsigned h = (unsigned)((key * 0x9E3779B97F4A7C15ull) >> 51) & (kBatchSlots - 1);
+                for (;;) {
+                    const unsigned long long prev = atomicCAS(&tkey[h], kEmptyKey, key);
+                    if (prev == kEmptyKey || prev == key) {
+                        const unsigned old = atomicAdd(&tcnt[h], 1u);  // Alg. 1
+                        acc += old;
+                        first += old == 0u;
+                        break;
+                    }
+                    h = (h + 1) & (kBatchSlots - 1);
+                }
+            }
+        }
+        acc = warp_sum(acc);
+        first = warp_sum(first);
+        if ((threadIdx.x & 31) == 0) {
+            s_acc[threadIdx.x >> 5] = acc;
+            s_first[threadIdx.x >> 5] = first;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long c = 0, f = 0;
+            for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+                c += s_acc[q];
+                f += s_first[q];
+            }
+            const bool big = hi - lo > kBatchSlots / 2;
+            out[3 * v] = c;
+            out[3 * v + 1] = f;
+            // first out-of-range bead (vector-relative), ~0 if none, ~1 if the vector was too long
+            out[3 * v + 2] = big ? ~1ull : (unsigned long long)s_bad;
+        }
+        __syncthreads();
+    }
+}
+
+struct LatScratch {
+    const void* xyz;
+    unsigned long long* bad;
+    int* overflow;
+    LatSlot* slots;
+    unsigned long long* sums;  // 8 pairs of (a, b)
+    int nslots;
+};
+
+int lattice_blocks(long long n) {
+    return (int)std::max(1LL, std::min<long long>((n + 255) / 256, (long long)num_sms() * 8));
+}
+
+int lat_prepare(const void* xyz, int dtype, int on_device, long long n, Arena** ar_out, LatScratch* sc,
+                cudaStream_t* s_inout, size_t extra = 0, char** extra_out = nullptr) {
+    if (dtype != PC_I32 && dtype != PC_I64) return arg_fail("lattice beads must be int32 or int64");
+    const int nb = lattice_blocks(n);
+    const size_t cbytes = on_device ? 0 : align_up((size_t)n * 3 * dtype_bytes(dtype), 256);
+    const size_t need = cbytes + 256 + align_up((size_t)nb * sizeof(LatSlot), 256) + 256 + align_up(extra, 256);
+    Arena* ar = nullptr;
+    int rc = arena_get(need, &ar);
+    if (rc) return rc;
+    char* base = (char*)ar->dev;
+    cudaStream_t s = *s_inout;
+    if (!on_device) {
+        if (n > 0) CK(cudaMemcpyAsync(base, xyz, (size_t)n * 3 * dtype_bytes(dtype), cudaMemcpyHostToDevice, s));
+        sc->xyz = base;
+    } else {
+        sc->xyz = xyz;
+    }
+    sc->bad = (unsigned long long*)(base + cbytes);
+    sc->overflow = (int*)(base + cbytes + 8);
+    sc->slots = (LatSlot*)(base + cbytes + 256);
+    sc->sums = (unsigned long long*)(base + cbytes + 256 + align_up((size_t)nb * sizeof(LatSlot), 256));
+    sc->nslots = nb;
+    if (extra_out) *extra_out = (char*)sc->sums + 256;
+    CK(cudaMemsetAsync(sc->bad, 0xff, 8, s));
+    CK(cudaMemsetAsync(sc->overflow, 0, 4, s));
+    *ar_out = ar;
+    return PC_OK;
+}
+
+template <typename KT>
+int lattice_run(const void* xyz_in, int dtype, int on_device, long long n, long long a, unsigned* grid, void* keys_v,
+                int clean, int contacts, pc_lattice_result* res, cudaStream_t s) {
+    g_launches = 0;
+    memset(res, 0, sizeof *res);
+    res->beads_processed = n;
+    if (n == 0) return PC_OK;
+    if (!grid || !keys_v) return arg_fail("grid and keys buffers are required");
+    KT* keys = (KT*)keys_v;
+    const long long side = 2 * a + 3;
+    Arena* ar = nullptr;
+    LatScratch sc;
+    std::unique_lock<std::mutex> lock;
+    {
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        lock = std::unique_lock<std::mutex>(g_arena[dev & 63].mu);
+    }
+    const unsigned long long cells = (unsigned long long)side * side * side;
+    // dense regime on a clean grid: shared-memory slab histogram (lattice_slab.cuh)
+    // crossover: n scattered atomics at ~21 G/s vs streaming 4 B/cell + ~40 B/bead at HBM rate -> n > cells/67
+    const bool slab = clean && !contacts && sizeof(KT) == 4 && (unsigned long long)n * 64 > cells &&
+                      n < (1LL << 32) - 1;
+    const int nbuckets = (int)((cells + (1ull << kBucketShift) - 1) >> kBucketShift);
+    const size_t kbytes = align_up((size_t)n * 4 + 64, 256);  // +16 keys: aligned staging windows may overrun
+    const size_t abytes = align_up((kMaxBuckets + 1) * 4, 256), cbytes4 = align_up((kMaxCoarse + 1) * 4, 256);
+    const size_t extra = slab ? 2 * kbytes + 3 * abytes + 3 * cbytes4 + align_up((size_t)nbuckets * sizeof(LatSlot), 256)
+                              : 0;
+    char* ex = nullptr;
+    int rc = lat_prepare(xyz_in, dtype, on_device, n, &ar, &sc, &s, extra, &ex);
+    if (rc) return rc;
+    const int nb = sc.nslots;
+    if (slab) {
+        unsigned* sorted = (unsigned*)ex;
+        unsigned* scratch = (unsigned*)(ex + kbytes);  // coarse-partitioned keys, then the slab kernel's fallback
+        unsigned* hist = (unsigned*)(ex + 2 * kbytes);
+        unsigned* base = (unsigned*)((char*)hist + abytes);
+        unsigned* cursor = (unsigned*)((char*)base + abytes);
+        unsigned* ccur = (unsigned*)((char*)cursor + abytes);
+        unsigned* cbase = (unsigned*)((char*)ccur + cbytes4);
+        unsigned* tbase = (unsigned*)((char*)cbase + cbytes4);
+        LatSlot* bslots = (LatSlot*)((char*)tbase + cbytes4);
+        const int ncoarse = (int)(((cells - 1) >> kCoarseShift) + 1);
+        static thread_local bool attr_set[64] = {false};
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        if (!attr_set[dev & 63]) {
+            CK(cudaFuncSetAttribute(lat_slab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSlabSmem));
+            CK(cudaFuncSetAttribute(lat_keys_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kMaxBuckets * 4));
+            CK(cudaFuncSetAttribute(lat_partition_coarse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kPartSmem));
+            CK(cudaFuncSetAttribute(lat_partition_fine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kPartSmem));
+            attr_set[dev & 63] = true;
+        }
+        CK(cudaMemsetAsync(hist, 0, nbuckets * 4, s));
+        lat_keys_hist_kernel<<<2 * num_sms(), 1024, nbuckets * 4, s>>>(sc.xyz, dtype, n, a, side, (unsigned*)keys, sc.bad, hist,
+                                                           nbuckets);
+        CK_LAUNCH("lat_keys_hist_kernel");
+        lat_bucket_scan_kernel<<<1, 1024, 0, s>>>(hist, base, cursor, nbuckets);
+        CK_LAUNCH("lat_bucket_scan_kernel");
+        lat_coarse_kernel<<<1, 32, 0, s>>>(base, nbuckets, ncoarse, ccur, cbase, tbase);
+        CK_LAUNCH("lat_coarse_kernel");
+        lat_partition_coarse_kernel<<<num_sms() * 2, kPartThreads, kPartSmem, s>>>((const unsigned*)keys, n, ccur, ncoarse,
+                                                                          scratch, sc.bad);
+        CK_LAUNCH("lat_partition_coarse_kernel");
+        lat_partition_fine_kernel<<<num_sms() * 2, kPartThreads, kPartSmem, s>>>(scratch, cbase, tbase, ncoarse, cursor,
+                                                                        sorted, sc.bad);
+        CK_LAUNCH("lat_partition_fine_kernel");
+        const int sgrid = std::min(num_sms(), nbuckets);
+        lat_slab_kernel<<<sgrid, 1024, kSlabSmem, s>>>(sorted, scratch, base, nbuckets, grid, cells, sc.bad, bslots,
+                                                       sc.overflow);
+        CK_LAUNCH("lat_slab_kernel");
+        lat_sum_slots_kernel<<<1, 256, 0, s>>>(bslots, sgrid, sc.sums);
+        CK_LAUNCH("lat_sum_slots_kernel");
+    } else {
+        lat_keys_kernel<KT><<<nb, 256, 0, s>>>(sc.xyz, dtype, n, a, side, keys, sc.bad);
+        CK_LAUNCH("lat_keys_kernel");
+    }
+    if (slab) {
+        // count / cells_touched are in sums[0], sums[1], as for the atomic path
+    } else if (clean && !contacts) {
+        lat_place_clean_kernel<KT><<<nb, 256, 0, s>>>(keys, n, grid, sc.bad, sc.slots, sc.overflow);
+        CK_LAUNCH("lat_place_clean_kernel");
+        lat_sum_slots_kernel<<<1, 256, 0, s>>>(sc.slots, nb, sc.sums);
+        CK_LAUNCH("lat_sum_slots_kernel");
+    } else {
+        lat_place_kernel<KT><<<nb, 256, 0, s>>>(keys, n, grid, sc.bad);
+        CK_LAUNCH("lat_place_kernel");
+        lat_gather_kernel<KT><<<nb, 256, 0, s>>>(keys, n, grid, sc.bad, sc.slots, sc.overflow);
+        CK_LAUNCH("lat_gather_kernel");
+        lat_sum_slots_kernel<<<1, 256, 0, s>>>(sc.slots, nb, sc.sums);  // sums[0] = sum(occ - 1)
+        CK_LAUNCH("lat_sum_slots_kernel");
+        if (contacts) {
+            lat_neighbours_kernel<KT><<<nb, 256, 0, s>>>(keys, n, side, grid, sc.bad, sc.slots);
+            CK_LAUNCH("lat_neighbours_kernel");
+            lat_sum_slots_kernel<<<1, 256, 0, s>>>(sc.slots, nb, sc.sums + 2);  // sums[2] = doubled
+            CK_LAUNCH("lat_sum_slots_kernel");
+        }
+        lat_mark_kernel<KT><<<nb, 256, 0, s>>>(keys, n, side, contacts, 0, grid, sc.bad, sc.slots);
+        CK_LAUNCH("lat_mark_kernel");
+        lat_sum_slots_kernel<<<1, 256, 0, s>>>(sc.slots, nb, sc.sums + 4);  // sums[4] = distinct cells
+        CK_LAUNCH("lat_sum_slots_kernel");
+        lat_mark_kernel<KT><<<nb, 256, 0, s>>>(keys, n, side, contacts, 1, grid, sc.bad, sc.slots);
+        CK_LAUNCH("lat_mark_kernel");
+    }
+    unsigned long long host[8] = {0};
+    unsigned long long bad = 0;
+    int ovf = 0;
+    CK(cudaMemcpyAsync(host, sc.sums, sizeof host, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&bad, sc.bad, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&ovf, sc.overflow, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (bad != kNoBad) {
+        res->error = PC_ERR_RANGE;
+        res->detail = (long long)bad;
+        return PC_ERR_RANGE;
+    }
+    if (ovf) {
+        res->error = PC_ERR_OVERFLOW;
+        return PC_ERR_OVERFLOW;
+    }
+    if (clean && !contacts) {
+        res->count = (long long)host[0];
+        res->cells_touched = (long long)host[1];
+    } else if (!contacts) {
+        res->count = (long long)(host[0] / 2);
+        res->cells_touched = (long long)host[4];
+    } else {
+        res->doubled = (long long)host[2];
+        res->count = res->doubled / 2;
+        res->cells_touched = (long long)host[4];
+        if (res->doubled & 1) {
+            res->error = PC_ERR_ODD;
+            return PC_ERR_ODD;
+        }
+    }
+    return PC_OK;
+}
+
