@@ -210,6 +210,18 @@ int pc_lattice_collisions_batch(const void* xyz, int32_t dtype, int32_t xyz_on_d
 int pc_lattice_collisions_vectors(const void* const* vectors, const int64_t* lengths, int32_t dtype, int32_t nvec,
                                   int64_t half_extent, pc_lattice_result* results, void* stream);
 
+/* count_collisions over several GPUs of one process (the
+ * counting array split by key range).  Device d owns the x-planes
+ * [-a + P*d/ndev, -a + P*(d+1)/ndev), P = 2a+1, on a private slab grid of
+ * (planes+2) x (2a+3)^2 cells; it copies all host beads in, validates every
+ * bead (PC_ERR_RANGE, detail = first bad bead, identical on every device),
+ * compacts its own beads and runs Alg. 1 on them.  Cells of different
+ * devices are disjoint, so *total = the sums of count and cells_touched =
+ * count_collisions(beads, new_space(a)) on one grid.  The slab grids are left
+ * zero; no LatticeSpace is involved.  The same ordinal may repeat. */
+int pc_lattice_collisions_multi(const void* xyz_host, int32_t dtype, int64_t n, int64_t half_extent, int32_t ndev,
+                                const int32_t* devices, pc_lattice_result* per_device, pc_lattice_result* total);
+
 /* Zero the whole grid with one streaming write (cudaMemsetAsync).  The
  * Python reset_sparse uses it in place of pc_lattice_reset_keys when the
  * touched keys number more than 1/32 of the cells AND every other cell is

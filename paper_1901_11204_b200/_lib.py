@@ -42,7 +42,7 @@ EXPORTED = (
     "pc_pairs_workspace_bytes", "pc_pairs", "pc_pairs_async", "pc_pairs_host", "pc_pairs_multi", "pc_pairs_batch",
     "pc_last_launch_count", "pc_kernel_timing", "pc_kernel_timing_read", "pc_lattice_grid_cells", "pc_lattice_key_bytes",
     "pc_lattice_collisions", "pc_lattice_contacts", "pc_lattice_reset_keys", "pc_lattice_clear",
-    "pc_lattice_collisions_batch", "pc_lattice_collisions_vectors",
+    "pc_lattice_collisions_batch", "pc_lattice_collisions_vectors", "pc_lattice_collisions_multi",
     "pc_lattice_reset_beads", "pc_grid_count_nonzero", "pc_microbench",
 )
 
@@ -95,6 +95,7 @@ _SIGS = {
     "pc_lattice_clear": ([_vp, _i64, _vp], ctypes.c_int),
     "pc_lattice_collisions_batch": ([_vp, _i32, _i32, _vp, _i32, _i64, _vp, _vp], ctypes.c_int),
     "pc_lattice_collisions_vectors": ([_vp, _vp, _i32, _i32, _i64, _vp, _vp], ctypes.c_int),
+    "pc_lattice_collisions_multi": ([_vp, _i32, _i64, _i64, _i32, _vp, _vp, _vp], ctypes.c_int),
     "pc_grid_count_nonzero": ([_vp, _i64, ctypes.POINTER(_i64), _vp], ctypes.c_int),
     "pc_microbench": ([_i32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
 }

@@ -308,9 +308,12 @@ int lat_prepare(const void* xyz, int dtype, int on_device, long long n, Arena** 
     return PC_OK;
 }
 
+// cells_limit: the grid holds only keys [0, cells_limit) (an x-slab of the cube, see
+// pc_lattice_collisions_multi); 0 = the whole (2a+3)^3 cube.
 template <typename KT>
 int lattice_run(const void* xyz_in, int dtype, int on_device, long long n, long long a, unsigned* grid, void* keys_v,
-                int clean, int contacts, pc_lattice_result* res, cudaStream_t s) {
+                int clean, int contacts, pc_lattice_result* res, cudaStream_t s,
+                unsigned long long cells_limit = 0) {
     g_launches = 0;
     memset(res, 0, sizeof *res);
     res->beads_processed = n;
@@ -326,7 +329,7 @@ int lattice_run(const void* xyz_in, int dtype, int on_device, long long n, long 
         CK(cudaGetDevice(&dev));
         lock = std::unique_lock<std::mutex>(g_arena[dev & 63].mu);
     }
-    const unsigned long long cells = (unsigned long long)side * side * side;
+    const unsigned long long cells = cells_limit ? cells_limit : (unsigned long long)side * side * side;
     // dense regime on a clean grid: shared-memory slab histogram (lattice_slab.cuh)
     // crossover: n scattered atomics at ~21 G/s vs streaming 4 B/cell + ~40 B/bead at HBM rate -> n > cells/67
     const bool slab = clean && !contacts && sizeof(KT) == 4 && (unsigned long long)n * 64 > cells &&
@@ -449,3 +452,49 @@ int lattice_run(const void* xyz_in, int dtype, int on_device, long long n, long 
     return PC_OK;
 }
 
+
+// ---- multi-GPU counting array (x-slab split; pc_lattice_collisions_multi) ----
+// Validate every bead (first bad index, as lat_keys_kernel) and append the beads
+// with x in [xlo, xhi) to `out` as int32 (x - xlo - a, y, z): in a cube of the
+// same half-extent those land on planes 1 .. xhi-xlo, so the keys of the slab's
+// (xhi-xlo+2) x side x side grid are the cube formula unchanged.  Order is
+// irrelevant to a histogram, so slots come from one warp-aggregated atomic.
+__global__ void lat_compact_slab_kernel(const void* __restrict__ xyz, int dtype, long long n, long long a,
+                                        long long xlo, long long xhi, int* __restrict__ out,
+                                        unsigned long long* __restrict__ count, unsigned long long* __restrict__ bad) {
+    const int lane = threadIdx.x & 31;
+    for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += (long long)gridDim.x * blockDim.x) {
+        const long long i = base + threadIdx.x;
+        bool keep = false;
+        long long x = 0, y = 0, z = 0;
+        if (i < n) {
+            x = coord_i64(xyz, dtype, i, 0);
+            y = coord_i64(xyz, dtype, i, 1);
+            z = coord_i64(xyz, dtype, i, 2);
+            if (x < -a || x > a || y < -a || y > a || z < -a || z > a) atomicMin(bad, (unsigned long long)i);
+            else keep = x >= xlo && x < xhi;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        unsigned long long pos = 0;
+        if (lane == 0 && m) pos = atomicAdd(count, (unsigned long long)__popc(m));
+        pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(m & ((1u << lane) - 1u));
+        if (keep) {
+            out[3 * pos] = (int)(x - xlo - a);
+            out[3 * pos + 1] = (int)y;
+            out[3 * pos + 2] = (int)z;
+        }
+    }
+}
+
+// Per-device state of pc_lattice_collisions_multi: input copy, compacted beads,
+// keys and the slab grid (kept all-zero between calls), guarded by its own lock
+// (lattice_run takes the arena lock).
+struct MultiLat {
+    std::mutex mu;
+    void* buf = nullptr;
+    size_t cap = 0;
+    unsigned* grid = nullptr;
+    unsigned long long grid_cells = 0;
+    cudaStream_t stream = nullptr;
+};
+MultiLat g_multilat[64];

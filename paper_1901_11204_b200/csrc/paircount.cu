@@ -819,6 +819,118 @@ int pc_pairs_multi(const void* xyz_host, int32_t dtype, int64_t n, int32_t inter
     return PC_OK;
 }
 
+int pc_lattice_collisions_multi(const void* xyz_host, int32_t dtype, int64_t n, int64_t half_extent, int32_t ndev,
+                                const int32_t* devices, pc_lattice_result* per_device, pc_lattice_result* total) {
+    if (ndev < 1 || !devices || !per_device || !total) return arg_fail("bad device list");
+    if (n < 0 || (n > 0 && !xyz_host)) return arg_fail("bad bead array");
+    if (half_extent < 0 || half_extent >= (1LL << 30)) return arg_fail("half_extent out of range");
+    if (dtype != PC_I32 && dtype != PC_I64) return arg_fail("lattice beads must be int32 or int64");
+    int count = 0;
+    CK(cudaGetDeviceCount(&count));
+    for (int d = 0; d < ndev; ++d)
+        if (devices[d] < 0 || devices[d] >= count) return arg_fail("device ordinal out of range");
+    const long long a = half_extent, side = 2 * a + 3, planes = 2 * a + 1;
+    std::vector<int> rcs((size_t)ndev, PC_OK);
+    std::vector<std::string> errs((size_t)ndev);
+    auto work = [&](int d) {
+        pc_lattice_result& r = per_device[d];
+        memset(&r, 0, sizeof r);
+        const long long xlo = -a + planes * d / ndev, xhi = -a + planes * (d + 1) / ndev;
+        auto fail = [&](int rc) {
+            rcs[d] = rc;
+            errs[d] = g_err;
+        };
+        int prev = 0;
+        cudaGetDevice(&prev);
+        if (cudaSetDevice(devices[d]) != cudaSuccess) return fail(cuda_fail("cudaSetDevice", cudaGetLastError()));
+        MultiLat& ml = g_multilat[devices[d] & 63];
+        std::lock_guard<std::mutex> lock(ml.mu);
+        auto body = [&]() -> int {
+            if (!ml.stream) CK(cudaStreamCreateWithFlags(&ml.stream, cudaStreamNonBlocking));
+            cudaStream_t s = ml.stream;
+            const size_t in_b = align_up((size_t)n * 3 * dtype_bytes(dtype), 256);
+            const size_t cmp_b = align_up((size_t)n * 12 + 16, 256), key_b = align_up((size_t)n * 4 + 64, 256);
+            const size_t need = in_b + cmp_b + key_b + 256;
+            if (ml.cap < need) {
+                if (ml.buf) CK(cudaFree(ml.buf));
+                ml.buf = nullptr;
+                ml.cap = 0;
+                CK(cudaMalloc(&ml.buf, need + need / 8));
+                ml.cap = need + need / 8;
+            }
+            const unsigned long long cells = (unsigned long long)(xhi - xlo + 2) * side * side;
+            if (ml.grid_cells < cells) {
+                if (ml.grid) CK(cudaFree(ml.grid));
+                ml.grid = nullptr;
+                ml.grid_cells = 0;
+                CK(cudaMalloc(&ml.grid, cells * 4));
+                CK(cudaMemsetAsync(ml.grid, 0, cells * 4, s));
+                ml.grid_cells = cells;
+            }
+            char* base = (char*)ml.buf;
+            int* cmp = (int*)(base + in_b);
+            unsigned* keys = (unsigned*)(base + in_b + cmp_b);
+            unsigned long long* ctr = (unsigned long long*)(base + in_b + cmp_b + key_b);  // [0] kept, [1] bad
+            if (n > 0) CK(cudaMemcpyAsync(base, xyz_host, (size_t)n * 3 * dtype_bytes(dtype), cudaMemcpyHostToDevice, s));
+            CK(cudaMemsetAsync(ctr, 0, 8, s));
+            CK(cudaMemsetAsync(ctr + 1, 0xff, 8, s));
+            if (n > 0) {
+                const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)num_sms() * 8);
+                lat_compact_slab_kernel<<<blocks, 256, 0, s>>>(base, dtype, n, a, xlo, xhi, cmp, ctr, ctr + 1);
+                CK_LAUNCH("lat_compact_slab_kernel");
+            }
+            unsigned long long hc[2] = {0, kNoBad};
+            CK(cudaMemcpyAsync(hc, ctr, 16, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            r.beads_processed = n;
+            if (hc[1] != kNoBad) {
+                r.error = PC_ERR_RANGE;
+                r.detail = (long long)hc[1];
+                return PC_OK;
+            }
+            pc_lattice_result sub;
+            const int rc = lattice_run<unsigned>(cmp, PC_I32, 1, (long long)hc[0], a, ml.grid, keys, 1, 0, &sub, s,
+                                                 cells);
+            CK(cudaMemsetAsync(ml.grid, 0, cells * 4, s));  // keep the slab grid clean for the next call
+            CK(cudaStreamSynchronize(s));
+            if (rc == PC_ERR_OVERFLOW) {
+                r.error = PC_ERR_OVERFLOW;
+                return PC_OK;
+            }
+            if (rc != PC_OK) return rc;
+            r.count = sub.count;
+            r.cells_touched = sub.cells_touched;
+            return PC_OK;
+        };
+        const int rc = body();
+        if (rc != PC_OK) fail(rc);
+        cudaSetDevice(prev);
+    };
+    std::vector<std::thread> pool;
+    for (int d = 1; d < ndev; ++d) pool.emplace_back(work, d);
+    work(0);
+    for (auto& th : pool) th.join();
+    for (int d = 0; d < ndev; ++d)
+        if (rcs[d] != PC_OK) {
+            g_err = errs[d];
+            return rcs[d];
+        }
+    pc_lattice_result t;
+    memset(&t, 0, sizeof t);
+    t.beads_processed = n;
+    for (int d = 0; d < ndev; ++d) {
+        const pc_lattice_result& r = per_device[d];
+        if (r.error && !t.error) {
+            t.error = r.error;
+            t.detail = r.detail;
+        }
+        t.count += r.count;
+        t.cells_touched += r.cells_touched;
+    }
+    *total = t;
+    return PC_OK;
+}
+
 int32_t pc_last_launch_count(void) { return g_launches; }
 
 int pc_kernel_timing(int32_t enable) {

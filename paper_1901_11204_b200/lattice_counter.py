@@ -322,3 +322,31 @@ def oracle_collisions_batch(vectors) -> list[int]:
 def oracle_contacts_batch(vectors) -> list[int]:
     """``[oracle_contacts(v) for v in vectors]`` in one GPU launch."""
     return _integer_pairs_batch(vectors, _lib.PC_MANHATTAN1)
+
+
+def count_collisions_multi_gpu(beads, half_extent: int, devices=None) -> CountReport:
+    """``count_collisions(beads, new_space(half_extent))`` with the grid split
+    over several GPUs of this process by x-planes (``pc_lattice_collisions_multi``):
+    each device validates all beads, keeps its planes' beads and runs Alg. 1 on
+    a private slab grid; the counts and touched cells of the disjoint slabs
+    add up.  No space is left populated.  ``devices`` defaults to every visible
+    GPU; an ordinal may repeat."""
+    arr = np.ascontiguousarray(as_bead_array(beads))
+    if half_extent < 0:
+        raise ValueError(f"half_extent must be >= 0, got {half_extent}")
+    lib = _lib.load()
+    if devices is None:
+        devices = list(range(int(lib.pc_device_count())))
+    devs = np.ascontiguousarray(np.asarray(list(devices), dtype=np.int32))
+    if len(devs) == 0:
+        raise ValueError("need at least one device")
+    per = (_lib.LatticeResult * len(devs))()
+    tot = _lib.LatticeResult()
+    _lib.check(lib.pc_lattice_collisions_multi(arr.ctypes.data, _lib.PC_I64, len(arr), half_extent, len(devs),
+                                               devs.ctypes.data, ctypes.addressof(per), ctypes.byref(tot)))
+    if tot.error == _lib.PC_ERR_RANGE:
+        idx = int(tot.detail)
+        raise CoordinateRangeError(f"bead {idx} at {tuple(arr[idx])} outside [-{half_extent}, {half_extent}]^3")
+    if tot.error == _lib.PC_ERR_OVERFLOW:
+        raise OccupancyOverflowError(f"cell occupancy exceeds {_CELL_MAX} (counter width)")
+    return CountReport(count=int(tot.count), beads_processed=len(arr), cells_touched=int(tot.cells_touched))

@@ -522,3 +522,24 @@ def test_large_host_int64_beads_narrowed_exactly():
         with pytest.raises(lc.CoordinateRangeError, match="bead 250001"):
             pc.count_collisions(b2, sp)
         assert sp.is_zero()
+
+
+@pytest.mark.parametrize("devs", [[0], [0, 0], [0, 0, 0, 0, 0]])
+def test_counting_array_multi_gpu_slabs(devs):
+    # pc_lattice_collisions_multi: x-slab split over a device list (ordinal 0 repeated on
+    # the one-GPU box) == the single-grid counting array, dense and sparse regimes
+    rng = np.random.default_rng(len(devs))
+    for a, n in ((30, 2_000_000), (30, 5_000), (200, 300_000)):
+        beads = rng.integers(-a, a + 1, size=(n, 3))
+        beads[: n // 10] = beads[0]  # one heavy cell
+        side = 2 * a + 3
+        keys = np.ravel_multi_index(tuple((beads + a + 1).T), (side,) * 3)
+        occ = np.bincount(keys)
+        rep = lc.count_collisions_multi_gpu(beads, a, devs)
+        assert (rep.count, rep.cells_touched, rep.beads_processed) == \
+            (int((occ * (occ - 1) // 2).sum()), int(np.count_nonzero(occ)), n)
+    bad = rng.integers(-5, 6, size=(1000, 3))
+    bad[777, 2] = 6
+    with pytest.raises(lc.CoordinateRangeError, match="bead 777"):
+        lc.count_collisions_multi_gpu(bad, 5, devs)
+    assert lc.count_collisions_multi_gpu(np.zeros((0, 3), dtype=np.int64), 5, devs).count == 0
