@@ -295,11 +295,13 @@ def secondary(torch, lib, stream):
 
     pts64 = np.ascontiguousarray(pts.astype(np.int64))
     sp5 = lc.new_space(a5)
-    for rep in range(2):
+    api_times = []
+    for rep in range(3):
         t0 = time.perf_counter()
         rep5 = lc.count_collisions(pts64, sp5)
         lc.reset_sparse(sp5)
-        api_ms = (time.perf_counter() - t0) * 1e3
+        api_times.append((time.perf_counter() - t0) * 1e3)
+    api_ms = min(api_times[1:])  # first call pays the host pages' first touch
     out["cfg5_counting_array_n2^26"].update({
         "api_wall_ms": api_ms, "api_count": rep5.count,
         "api_path": "count_collisions(int64 host beads, space) + reset_sparse: H2D of 1.61 GB + the device step"})
