@@ -515,10 +515,12 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             // register indexing).  Inlined once per row the kernel was 178 KB of
             // SASS; slim it is 1.4% faster for the sum, 8% for the count at
             // N = 65,536 and 7% on the clustered 2^22 set (most chunks flag a row).
-#pragma unroll 1
-            for (int r = 0; r < R; ++r) {
+            // rows flagged by any lane, one REDUX; visit only those
+            unsigned rows_any = __reduce_or_sync(0xffffffffu, fl);
+            while (rows_any) {
+                const int r = __ffs(rows_any) - 1;
+                rows_any &= rows_any - 1;
                 const unsigned owners = __ballot_sync(0xffffffffu, (fl >> r) & 1u);
-                if (!owners) continue;
                 float vx = 0.f, vy = 0.f, vz = 0.f, vc = 0.f;
 #pragma unroll
                 for (int rr = 0; rr < R; ++rr)
