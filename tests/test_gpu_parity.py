@@ -246,6 +246,15 @@ def test_dense_regime_counting_array(case):
     assert count == int((occ * (occ - 1) // 2).sum())
     assert touched == int(np.count_nonzero(occ))
     assert sp.is_zero()
+    # Alg. 2 on the same beads (dense regime: slab histogram + one stencil pass)
+    offs = np.array([1, -1, side, -side, side * side, -side * side], dtype=np.int64)
+    doubled = int(sum(occ[keys + o].sum(dtype=np.int64) for o in offs))
+    touched7 = len(np.unique(np.concatenate([keys] + [keys + o for o in offs])))
+    rep = pc.count_contacts(b64, sp)
+    assert (rep.count, rep.cells_touched) == (doubled // 2, touched7)
+    assert np.array_equal(np.asarray(sp.cells).ravel(), occ.astype(np.uint32))  # left populated
+    pc.reset_sparse(sp)
+    assert sp.is_zero()
 
 
 # ------------------------------------------------------------- lattice --
