@@ -184,6 +184,26 @@ def secondary(torch, lib, stream):
     from paper_1901_11204_b200 import generators as gen
 
     out = {}
+    # ---- config 1: N=4,096 integer points, exact-coincidence count (the reference's naive oracle)
+    from oracle import numpy_port as npo1
+    from paper_1901_11204_b200 import lattice_counter as lc1
+
+    cloud = gen.normal_cloud(4096, 8.0, 64, 0)
+    for _ in range(20):
+        got1 = lc1.oracle_collisions(cloud)
+    t0 = time.perf_counter()
+    for _ in range(200):
+        got1 = lc1.oracle_collisions(cloud)
+    api_us = (time.perf_counter() - t0) / 200 * 1e6
+    t0 = time.perf_counter()
+    want1 = npo1.oracle_collisions(cloud)
+    cpu_ms = (time.perf_counter() - t0) * 1e3
+    out["cfg1_integer_coincidence_n4096"] = {
+        "count": got1, "expected": 356, "api_us_per_call": api_us,
+        "api_path": "oracle_collisions(int64 host points): H2D, prep, all-pairs kernel with the exact int64 predicate, D2H",
+        "cpu_oracle_ms": cpu_ms, "cpu": "numpy port of the reference's N x N coincidence matrix (1 core)",
+        "matches_cpu": got1 == want1}
+
     # ---- config 2
     n2 = 65536
     obj2 = gen.random_spheres(n2, gen.contact_box_edge(n2), 0).astype(np.float32)
