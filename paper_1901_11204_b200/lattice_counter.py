@@ -2,11 +2,14 @@
 
 Drop-in for the reference module ``pkg/src/paircount/lattice_counter.py``.
 The space is a device-resident dense uint32 grid of side 2a+3 (one zero
-padding cell per face, index (x+a+1, y+a+1, z+a+1)); beads are placed with
-one atomic increment each (Alg. 1: collisions += old occupancy) by
-libpaircount.so, which also evaluates Alg. 2's neighbour sums and the
-sparse reset.  The O(N^2) oracles run on the GPU all-pairs kernel with the
-reference's exact integer predicates.
+padding cell per face, index (x+a+1, y+a+1, z+a+1)).  libpaircount.so places
+the beads -- one atomic increment each when beads are few relative to cells
+(Alg. 1: collisions += old occupancy), shared-memory slabs streamed out by
+TMA when they are many -- and evaluates Alg. 2's neighbour sums (per bead,
+or one stencil pass over the grid in the dense regime) and the sparse reset.
+The O(N^2) oracles run on the GPU all-pairs kernel with the reference's
+exact integer predicates; ``*_batch`` and ``*_multi_gpu`` variants count many
+small vectors in one launch / one grid over several GPUs.
 
 Differences of representation (not of results):
   * ``LatticeSpace.cells`` is a read-only host snapshot of the device grid

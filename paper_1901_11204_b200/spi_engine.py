@@ -11,8 +11,10 @@ Python callable, and there is no CPU fallback):
   * ``collision_indicator``  -- integer contact count, bit-exact (the fp32
     filter + exact float64 re-check of csrc/paircount.cu);
   * ``inverse_square``       -- softened inverse square 1/(1+|a-b|^2) summed
-    in fp32 per chunk and float64 across chunks; agrees with the float64
-    reference within 1e-5 relative (tests/test_gpu_parity.py).
+    in fp32 per chunk and float64 across chunks (float64/integer coordinates
+    enter as hi+lo fp32 pairs so separations keep ~2u relative accuracy);
+    agrees with the float64 reference within 1e-5 relative
+    (tests/test_gpu_parity.py).
 Any other callable raises ``TypeError`` -- after the same argument checks the
 reference performs and after the n < 2 short-circuit, where the reference
 never calls ``f`` either.
