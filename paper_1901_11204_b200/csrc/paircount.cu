@@ -247,6 +247,21 @@ __device__ __forceinline__ void bbox_centre(const PrepStats& st, int dtype, doub
     }
 }
 
+// Largest per-axis extent of the bounding box (float64).
+__device__ __forceinline__ double bbox_span(const PrepStats& st, int dtype) {
+    double e = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double d = is_int_dtype(dtype) ? (double)dec_i64(st.mx[k]) - (double)dec_i64(st.mn[k])
+                                             : dec_f64(st.mx[k]) - dec_f64(st.mn[k]);
+        e = fmax(e, d);
+    }
+    return e;
+}
+// The compensated (hi + lo) sum keeps each term within 4u + 2u^2*E relative; beyond
+// this span that passes 1e-7 and the sum takes pairs_f64_kernel instead.
+constexpr double kCompMaxSpan = 67108864.0;  // 2^26
+
 // Staged value of point i: centred fp32 q and w = -|q|^2/2 (Gram), or the
 // raw fp32 coordinates (direct formula).
 template <bool DIRECT>
@@ -386,6 +401,54 @@ __global__ void finalize_kernel(const Slot* __restrict__ slots, int nslots, cons
         if (direct && r.error == PC_OK && !(dec_f64_or0(st->maxabs) < 1e18)) r.error = PC_ERR_ARG;
         r.reserved = 0;
         *out = r;
+    }
+}
+
+// Sum + count for float64/integer input whose span defeats the compensated fp32
+// staging (bbox_span > kCompMaxSpan): every owned pair in float64, the count with
+// the reference's own arithmetic (spi_engine.py:68-73) and the term 1/(1+d2) in
+// float64.  Always launched after the compensated kernel; exactly one of the two
+// does the work (each checks the span), the other writes zero slots.
+__global__ void __launch_bounds__(256) pairs_f64_kernel(const PairsArgs a, Slot* __restrict__ slots) {
+    __shared__ unsigned long long s_c[8];
+    __shared__ double s_s[8];
+    const bool wide = bbox_span(*a.st, a.dtype) > kCompMaxSpan;
+    unsigned long long cnt = 0;
+    double sum = 0.0;
+    if (wide) {
+        const bool bal = a.sched == PC_BALANCED;
+        for (long long i = a.lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.hi;
+             i += (long long)gridDim.x * blockDim.x) {
+            const long long m = bal ? steps_for_dev(a.n, (int)i) : (long long)a.n - 1 - i;
+            const double xi = coord_f64(a.xyz, a.dtype, i, 0), yi = coord_f64(a.xyz, a.dtype, i, 1),
+                         zi = coord_f64(a.xyz, a.dtype, i, 2);
+            for (long long s = 1; s <= m; ++s) {
+                long long j = i + s;
+                if (j >= a.n) j -= a.n;
+                const double dx = __dsub_rn(xi, coord_f64(a.xyz, a.dtype, j, 0));
+                const double dy = __dsub_rn(yi, coord_f64(a.xyz, a.dtype, j, 1));
+                const double dz = __dsub_rn(zi, coord_f64(a.xyz, a.dtype, j, 2));
+                const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+                cnt += d2 < 1.0 ? 1ull : 0ull;
+                sum += 1.0 / (1.0 + d2);
+            }
+        }
+    }
+    cnt = warp_sum(cnt);
+    sum = warp_sum(sum);
+    if ((threadIdx.x & 31) == 0) {
+        s_c[threadIdx.x >> 5] = cnt;
+        s_s[threadIdx.x >> 5] = sum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Slot sl{0ull, 0ull, 0.0, 0ull};
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            sl.count += s_c[w];
+            sl.sum += s_s[w];
+        }
+        sl.checks = sl.count;
+        slots[blockIdx.x] = sl;
     }
 }
 
@@ -585,6 +648,13 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
                      : direct ? dispatch_cfg<kBig.warps, kBig.r, kBig.w, true>(args, flat, cap, &nslots, s)
                               : dispatch_cfg<kBigGram.warps, kBigGram.r, kBigGram.w, false>(args, flat, cap, &nslots, s);
             if (rc) return rc;
+            if (comp) {  // the wide-span float64 path (does nothing unless the span needs it)
+                const int g2 = (int)std::min<long long>((hi - lo + 255) / 256, (long long)num_sms() * 4);
+                if (nslots + g2 > cap) return arg_fail("workspace too small for the CTA slots");
+                pairs_f64_kernel<<<g2, 256, 0, s>>>(args, slots + nslots);
+                CK_LAUNCH("pairs_f64_kernel");
+                nslots += g2;
+            }
         }
         finalize_kernel<<<1, 256, 0, s>>>(slots, nslots, st, row_pairs(n, lo, hi, schedule), direct ? 1 : 0, dres + k);
         CK_LAUNCH("finalize_kernel");

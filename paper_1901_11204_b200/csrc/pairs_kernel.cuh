@@ -122,6 +122,10 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const long long gw = (long long)blockIdx.x * WARPS + wid;
+    if (COMP && bbox_span(*a.st, a.dtype) > kCompMaxSpan) {  // pairs_f64_kernel takes this call
+        if (threadIdx.x == 0) a.slots[blockIdx.x] = Slot{0ull, 0ull, 0.0, 0ull};
+        return;
+    }
     const int n = a.n;
     const bool bal = a.sched == PC_BALANCED;
 

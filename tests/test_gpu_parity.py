@@ -445,9 +445,19 @@ def _invsq_cases():
     yield "int32 spread", rng.integers(-2**30, 2**30, size=(800, 3)).astype(np.int32)
     # n >= 16384: the big-tile compensated configuration
     yield "f64 big config, offset cluster", rng.random((40_000, 3)) * 34.0 + np.array([5.0e3, -2.0e4, 7.0e2])
+    # spans beyond 2^26: the float64 path (pairs_f64_kernel)
+    far = rng.random((1200, 3)) * 5.0
+    far[600:] += np.array([1.0e10, -3.0e9, 0.0])
+    yield "f64 two clusters 1e10 apart", far
+    ifar = rng.integers(0, 5, size=(1000, 3)).astype(np.int64)
+    ifar[500:] += np.int64(2**50)
+    yield "int64 two clusters 2^50 apart", ifar
+    big = rng.random((20_000, 3)) * 40.0
+    big[::2] += 4.0e8
+    yield "f64 big config, span 4e8", big
 
 
-@pytest.mark.parametrize("case", range(8))
+@pytest.mark.parametrize("case", range(11))
 def test_inverse_square_sum_tight_for_non_f32_inputs(case):
     # float64 / integer coordinates: the kernel must not lose the pair separation
     # to fp32 rounding of large coordinates (compensated hi+lo staging, DESIGN.md
