@@ -12,10 +12,12 @@
 // y_j+1)(z_j, z_j+1, w_j, w_j+1), so one FFMA2/FADD2 (sm_100 f32x2) with the
 // row value broadcast evaluates two pairs.  The prep kernel writes the pair
 // arrays E (pairs starting at even j) and O (odd j), each pair holding point
-// j and point (j+1) mod n, so any window position is two 16-byte cp.async.
-// A tile's rows are staged the same way (cp.async into a warp-private row
-// buffer, issued with the chunk that first needs them) so a tile switch
-// never stalls on a global load.
+// j and point (j+1) mod n, so any window position is two 16-byte copies and a
+// window of consecutive columns is one contiguous run.  The sum kernel moves
+// full chunks and whole row tiles with one TMA bulk copy each (lane 0, per-warp
+// mbarrier per buffer); the count kernel and ragged chunks use per-lane
+// cp.async.  A tile's rows are staged into a warp-private row buffer with the
+// chunk that first needs them, so a tile switch never stalls on a global load.
 //
 // Column space: a warp tile starting at row i0 walks offsets s' = 1..L
 // (partner j = i0 + s', mod n for the balanced schedule); row rl owns offset
