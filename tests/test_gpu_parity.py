@@ -562,3 +562,36 @@ def test_counting_array_multi_gpu_slabs(devs):
     with pytest.raises(lc.CoordinateRangeError, match="bead 777"):
         lc.count_collisions_multi_gpu(bad, 5, devs)
     assert lc.count_collisions_multi_gpu(np.zeros((0, 3), dtype=np.int64), 5, devs).count == 0
+
+
+def test_abi_argument_errors():
+    # every C entry rejects malformed arguments with PC_ERR_ARG (ValueError) and a message
+    import ctypes
+
+    lib = _lib.load()
+    pts = gen.random_spheres(1000, 10.0, 1).astype(np.float32)
+    n = len(pts)
+    with pytest.raises(ValueError, match="row range"):
+        _lib.pairs_host(pts, _lib.PC_COLLISION, _lib.PC_BALANCED, [0, n + 1])
+    with pytest.raises(ValueError, match="row range"):
+        _lib.pairs_host(pts, _lib.PC_COLLISION, _lib.PC_BALANCED, [5, 3])
+    with pytest.raises(ValueError, match="integer interactions"):
+        _lib.pairs_host(pts, _lib.PC_COINCIDE, _lib.PC_BALANCED, [0, n])
+    with pytest.raises(ValueError, match="schedule"):
+        _lib.pairs_host(pts, _lib.PC_COLLISION, 7, [0, n])
+    res = (_lib.PairsResult * 1)()
+    b = np.array([0, n], dtype=np.int64)
+    ws = _lib.DeviceBuffer(1024)
+    d = _lib.DeviceBuffer(pts.nbytes)
+    _lib.check(lib.pc_memcpy_h2d(d.ptr, pts.ctypes.data, pts.nbytes, None))
+    rc = lib.pc_pairs(d.ptr, _lib.PC_F32, n, _lib.PC_COLLISION, _lib.PC_BALANCED, 0, 1, b.ctypes.data, ws.ptr, 1024,
+                      ctypes.addressof(res), None)
+    assert rc == _lib.PC_ERR_ARG and b"workspace" in lib.pc_last_error()
+    with pytest.raises(ValueError, match="device"):
+        _lib.pairs_multi(pts, _lib.PC_COLLISION, _lib.PC_BALANCED, [0, 1000], [0, 500, n])
+    with pytest.raises(ValueError, match="cover"):
+        _lib.pairs_multi(pts, _lib.PC_COLLISION, _lib.PC_BALANCED, [0, 0], [0, 500, n - 1])
+    with pytest.raises(ValueError):
+        lc.count_collisions_multi_gpu(np.zeros((4, 3), dtype=np.int64), 5, [1000])
+    with pytest.raises(ValueError, match="integer"):
+        _lib.pairs_batch([pts], _lib.PC_MANHATTAN1)
