@@ -268,7 +268,18 @@ def secondary(torch, lib, stream):
         "api_wall_ms": api_ms,
         "api_path": "spi_balanced(points, collision_indicator): numpy (n,3) f32 -> ctypes pc_pairs_host "
                     "(H2D, prep, Gram-filter kernel, finalize, D2H) -> SpiResult",
-        "kernel": "pairs_kernel<128,12,256,GRAM,FLAT>"}
+        "kernel": "pairs_kernel<128,12,192,GRAM,FLAT>"}
+    # the paper's comparison in its large-N regime (N > 525,000): the straightforward
+    # scheme (standard schedule, one warp per row tile) on the same inner code
+    _lib.kernel_timing(True)
+    _lib.pairs_async(d3.data_ptr(), _lib.PC_F32, n3, _lib.PC_COLLISION, _lib.PC_STANDARD, np.array([0, n3]),
+                     ws3.data_ptr(), ws3.numel(), res.data_ptr(), stream.cuda_stream, _lib.PC_TILE_PER_ROW_TILE)
+    ms_n, cnt_n = _lib.kernel_timing_read()
+    _lib.kernel_timing(False)
+    torch.cuda.synchronize()
+    out["cfg3_collision_count_n2^20"].update({
+        "naive_standard_per_row_tile_ms": ms_n / cnt_n, "naive_count": int(res[0].item()),
+        "naive_over_balanced_time": (ms_n / cnt_n) / (ms_k / cnt_k)})
     del d3, ws3
 
     # ---- config 5: counting array, device-resident int32 coordinates
