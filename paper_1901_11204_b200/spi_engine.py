@@ -290,3 +290,35 @@ def spi_rows(objects, f: Callable, rows: range | tuple, schedule: str = "balance
         raise ValueError(f"row range [{lo}, {hi}) outside [0, {len(obj)}]")
     ((partial, pairs),) = _run_ranges(obj, f, [(lo, hi)], schedule)
     return partial, pairs
+
+
+def spi_totals_batch(objects_list, f: Callable) -> list:
+    """``[spi_balanced(obj, f).total for obj in objects_list]`` in one GPU launch
+    (``pc_pairs_batch``: one CTA per object array, the pairs evaluated in
+    float64 with the reference's own arithmetic, so counts are exact and sums
+    are float64).  Meant for many small problems (the paper's 100-1000
+    vectors per execution); arrays of more than 4096 objects fall back to
+    ``spi_balanced``.  Same argument checks and errors as ``spi_balanced``."""
+    arrays = [as_object_array(o) for o in objects_list]
+    code = _interaction_code(f) if any(len(a) >= 2 for a in arrays) else None
+    out = [None] * len(arrays)
+    batch = []
+    for idx, obj in enumerate(arrays):
+        if len(obj) < 2:
+            out[idx] = 0
+            continue
+        xyz = _device_coords(obj)
+        if xyz.dtype.kind == "f" and not np.isfinite(xyz).all():
+            out[idx] = spi_balanced(obj, f).total  # raises the reference's error for this array
+            continue
+        batch.append((idx, xyz.astype(np.float64) if xyz.dtype != np.float64 else xyz))
+    if batch:
+        results = _lib.pairs_batch([np.ascontiguousarray(x) for _, x in batch], code)
+        for (idx, xyz), r in zip(batch, results):
+            if r.error == _lib.PC_ERR_ARG:  # too many objects for one CTA: the full path
+                out[idx] = spi_balanced(arrays[idx], f).total
+            elif r.error:
+                raise InteractionDomainError("sphere coordinates must be finite")
+            else:
+                out[idx] = float(r.sum) if code == _lib.PC_COLLISION_INVSQ else int(r.count)
+    return out

@@ -595,3 +595,22 @@ def test_abi_argument_errors():
         lc.count_collisions_multi_gpu(np.zeros((4, 3), dtype=np.int64), 5, [1000])
     with pytest.raises(ValueError, match="integer"):
         _lib.pairs_batch([pts], _lib.PC_MANHATTAN1)
+
+
+def test_spi_totals_batch():
+    # many small SPI problems in one launch == spi_balanced per problem (C oracle)
+    rng = np.random.default_rng(12)
+    objs = [rng.random((k, 3)) * (k ** (1 / 3)) * 1.3 for k in (0, 1, 2, 7, 64, 500, 4096, 5000)]
+    objs.append(objs[4].astype(np.float32))
+    objs.append(rng.integers(0, 6, size=(300, 3)))
+    counts = se.spi_totals_batch(objs, se.collision_indicator)
+    sums = se.spi_totals_batch(objs, se.inverse_square)
+    for o, c, s in zip(objs, counts, sums):
+        if len(o) < 2:
+            assert c == 0 and s == 0
+            continue
+        want_c, want_s, _ = c_oracle.rows(o, 0, len(o), "balanced")
+        assert c == want_c and isinstance(c, int)
+        assert s == pytest.approx(want_s, rel=1e-12 if len(o) <= 4096 else REL_TOL)
+    with pytest.raises(TypeError):
+        se.spi_totals_batch(objs[3:5], lambda a, b: 1)
