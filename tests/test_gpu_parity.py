@@ -614,3 +614,26 @@ def test_spi_totals_batch():
         assert s == pytest.approx(want_s, rel=1e-12 if len(o) <= 4096 else REL_TOL)
     with pytest.raises(TypeError):
         se.spi_totals_batch(objs[3:5], lambda a, b: 1)
+
+
+def test_lattice_64bit_keys():
+    # a = 820: (2a+3)^3 = 4.4e9 cells > 2^32, so keys are 64-bit (17.7 GB grid); beads near the
+    # far corner have keys above 2^32
+    a = 820
+    assert _lib.load().pc_lattice_key_bytes(a) == 8
+    rng = np.random.default_rng(9)
+    beads = np.concatenate([rng.integers(a - 3, a + 1, size=(3000, 3)), rng.integers(-a, -a + 4, size=(3000, 3)),
+                            rng.integers(-a, a + 1, size=(3000, 3))])
+    side = 2 * a + 3
+    keys = np.ravel_multi_index(tuple((beads + a + 1).T), (side,) * 3)
+    assert keys.max() > 2**32
+    _, inv, occ = np.unique(keys, return_inverse=True, return_counts=True)
+    sp = pc.new_space(a)
+    rep = pc.count_collisions(beads, sp)
+    assert (rep.count, rep.cells_touched) == (int((occ * (occ - 1) // 2).sum()), len(occ))
+    pc.reset_sparse(sp)
+    rep = pc.count_contacts(beads, sp)
+    assert rep.count == c_oracle.int_pairs(beads)[1]
+    pc.reset_sparse(sp)
+    assert sp.is_zero()
+    del sp
