@@ -637,3 +637,20 @@ def test_lattice_64bit_keys():
     pc.reset_sparse(sp)
     assert sp.is_zero()
     del sp
+
+
+def test_non_contiguous_inputs():
+    # strided views, Fortran order and Sphere lists give the same results as contiguous copies
+    pts = gen.random_spheres(6001, 14.0, 5)
+    views = [pts[::2], np.asfortranarray(pts), pts.T.copy().T, [se.Sphere(*p) for p in pts[:500]]]
+    for v in views:
+        ref = np.ascontiguousarray(np.asarray(v if not isinstance(v, list) else [(s.x, s.y, s.z) for s in v], dtype=np.float64))
+        want = c_oracle.rows(ref, 0, len(ref), "balanced")
+        assert se.spi_balanced(v, se.collision_indicator).total == want[0]
+        assert se.spi_balanced(v, se.inverse_square).total == pytest.approx(want[1], rel=REL_TOL)
+    beads = gen.random_chain(5000, 4)[0]
+    sp = pc.new_space(int(np.abs(beads).max()))
+    for v in (beads[::3], np.asfortranarray(beads)):
+        rep = pc.count_collisions(v, sp)
+        pc.reset_sparse(sp)
+        assert rep.count == c_oracle.int_pairs(np.ascontiguousarray(v))[0]
