@@ -654,3 +654,28 @@ def test_non_contiguous_inputs():
         rep = pc.count_collisions(v, sp)
         pc.reset_sparse(sp)
         assert rep.count == c_oracle.int_pairs(np.ascontiguousarray(v))[0]
+
+
+def test_concurrent_callers():
+    # the library is thread-safe (per-device arena lock, thread-local errors): the
+    # reference's spi_parallel runs its workers on threads, and so may users
+    from concurrent.futures import ThreadPoolExecutor
+
+    inputs = [gen.random_spheres(3000 + 17 * k, 12.0, 40 + k) for k in range(8)]
+    chains = [gen.random_chain(2000, 60 + k)[0] for k in range(8)]
+    want = [c_oracle.rows(p, 0, len(p), "balanced")[0] for p in inputs]
+    want_l = [c_oracle.int_pairs(c)[0] for c in chains]
+
+    def job(k):
+        sp = pc.new_space(int(np.abs(chains[k]).max()))
+        out = []
+        for _ in range(5):
+            out.append(se.spi_balanced(inputs[k], se.collision_indicator).total)
+            out.append(pc.count_collisions(chains[k], sp).count)
+            pc.reset_sparse(sp)
+        return out
+
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        results = list(pool.map(job, range(8)))
+    for k, out in enumerate(results):
+        assert out[0::2] == [want[k]] * 5 and out[1::2] == [want_l[k]] * 5
