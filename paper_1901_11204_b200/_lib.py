@@ -103,6 +103,7 @@ _SIGS = {
 _lock = threading.Lock()
 _handle = None
 _device_checked = False
+_tls = threading.local()  # the CUDA current device is per host thread: set it in each calling thread
 
 
 def load(require_device: bool = True):
@@ -127,9 +128,10 @@ def load(require_device: bool = True):
                 raise PaircountUnavailable(
                     "no CUDA device visible to libpaircount (there is no CPU fallback): "
                     + _handle.pc_last_error().decode())
-            dev = int(os.environ.get("PAIRCOUNT_DEVICE", "0"))
-            check(_handle.pc_set_device(dev))
             _device_checked = True
+        if require_device and not getattr(_tls, "device_set", False):
+            check(_handle.pc_set_device(int(os.environ.get("PAIRCOUNT_DEVICE", "0"))))
+            _tls.device_set = True
         return _handle
 
 
