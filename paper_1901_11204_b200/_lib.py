@@ -130,7 +130,10 @@ def load(require_device: bool = True):
                     + _handle.pc_last_error().decode())
             _device_checked = True
         if require_device and not getattr(_tls, "device_set", False):
-            check(_handle.pc_set_device(int(os.environ.get("PAIRCOUNT_DEVICE", "0"))))
+            # PAIRCOUNT_DEVICE pins the device; without it the thread's current CUDA
+            # device (e.g. torch.cuda.set_device) is left alone
+            if "PAIRCOUNT_DEVICE" in os.environ:
+                check(_handle.pc_set_device(int(os.environ["PAIRCOUNT_DEVICE"])))
             _tls.device_set = True
         return _handle
 
