@@ -75,7 +75,9 @@ def spi_distributed(objects, f, schedule: str = "balanced", group=None,
     """Total of f over all pairs, rows sharded over the process group.
 
     ``compute(obj, f, lo, hi, schedule) -> (count_or_sum)`` evaluates one
-    slab; it defaults to the GPU kernels (``spi_engine.spi_rows``).  Returns
+    slab; it defaults to the GPU kernels (``spi_engine.spi_rows``), which run
+    on the calling thread's current CUDA device -- one process per GPU sets it
+    (``torch.cuda.set_device(local_rank)`` or ``PAIRCOUNT_DEVICE``).  Returns
     (total, per-rank partials, per-rank pair counts)."""
     import torch.distributed as dist
 
