@@ -335,7 +335,8 @@ def secondary(torch, lib, stream):
     api_ms = min(api_times[1:])  # first call pays the host pages' first touch
     out["cfg5_counting_array_n2^26"].update({
         "api_wall_ms": api_ms, "api_count": rep5.count,
-        "api_path": "count_collisions(int64 host beads, space) + reset_sparse: H2D of 1.61 GB + the device step"})
+        "api_path": "count_collisions(int64 host beads, space) + reset_sparse: host threads narrow the 1.61 GB "
+                    "of int64 beads to int32 in pinned chunks streamed to the device (0.8 GB H2D) + the device step"})
     del sp5, pts64
 
     # ---- config 4: 2^22 clustered points, count; the per-rank slabs of a 2/4/8-GPU split timed

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -1223,12 +1224,12 @@ int pc_lattice_reset_beads(const void* xyz, int32_t dtype, int32_t xyz_on_device
     std::lock_guard<std::mutex> lock(g_arena[dev & 63].mu);
     Arena* ar = nullptr;
     LatScratch sc;
-    int rc = lat_prepare(xyz, dtype, xyz_on_device, n, &ar, &sc, &s);
+    int rc = lat_prepare(xyz, dtype, xyz_on_device, n, half_extent, &ar, &sc, &s);
     if (rc) return rc;
     const long long side = 2 * half_extent + 3;
-    lat_keys_kernel<unsigned><<<sc.nslots, 256, 0, s>>>(sc.xyz, dtype, n, half_extent, side, nullptr, sc.bad);
+    lat_keys_kernel<unsigned><<<sc.nslots, 256, 0, s>>>(sc.xyz, sc.dtype, n, half_extent, side, nullptr, sc.bad);
     CK_LAUNCH("lat_keys_kernel");
-    lat_zero_beads_kernel<<<sc.nslots, 256, 0, s>>>(sc.xyz, dtype, n, half_extent, side, grid, sc.bad);
+    lat_zero_beads_kernel<<<sc.nslots, 256, 0, s>>>(sc.xyz, sc.dtype, n, half_extent, side, grid, sc.bad);
     CK_LAUNCH("lat_zero_beads_kernel");
     unsigned long long bad = 0;
     CK(cudaMemcpyAsync(&bad, sc.bad, 8, cudaMemcpyDeviceToHost, s));

@@ -525,22 +525,46 @@ def test_boundary_stress_random_offsets(trial):
 
 
 def test_large_host_int64_beads_narrowed_exactly():
-    # a large int64 host vector (dense regime, 9.6 MB): counts exact, and a bead
-    # beyond int32 or just outside the cube is still reported by its index
+    # large int64 host vectors go to the device narrowed to int32 through pinned
+    # chunks on host threads (lat_prepare): counts exact in the dense and sparse
+    # regimes and for Alg. 2, and a bead beyond int32 or just outside the cube is
+    # still reported by its index, whichever chunk it lands in
     rng = np.random.default_rng(8)
-    beads = rng.integers(-40, 41, size=(400_000, 3))
+    beads = rng.integers(-40, 41, size=(3_000_000, 3))
     sp = pc.new_space(40)
     rep = pc.count_collisions(beads, sp)
     keys = np.ravel_multi_index(tuple((beads + 41).T), (83, 83, 83))
-    occ = np.bincount(keys)
+    occ = np.bincount(keys, minlength=83**3)
     assert rep.count == int((occ * (occ - 1) // 2).sum()) and rep.cells_touched == np.count_nonzero(occ)
     pc.reset_sparse(sp)
-    for bad in (2**32 + 5, -(2**40), 41):
+    assert pc.count_contacts(beads, sp).count == _contacts_by_grid(occ.reshape(83, 83, 83), beads + 41)
+    pc.reset_sparse(sp)
+    for idx, bad in ((250_001, 2**32 + 5), (2_999_999, -(2**40)), (1_400_000, 41), (0, -41)):
         b2 = beads.copy()
-        b2[250_001, 1] = bad
-        with pytest.raises(lc.CoordinateRangeError, match="bead 250001"):
+        b2[idx, 1] = bad
+        with pytest.raises(lc.CoordinateRangeError, match=f"bead {idx} "):
             pc.count_collisions(b2, sp)
         assert sp.is_zero()
+    sparse = rng.integers(-500, 501, size=(600_000, 3))
+    sparse[::7] = sparse[0]
+    sp2 = pc.new_space(500)
+    keys = np.ravel_multi_index(tuple((sparse + 501).T), (1003,) * 3)
+    _, cnt = np.unique(keys, return_counts=True)
+    rep = pc.count_collisions(sparse, sp2)
+    assert (rep.count, rep.cells_touched) == (int((cnt * (cnt - 1) // 2).sum()), len(cnt))
+    pc.reset_sparse(sp2)
+    assert sp2.is_zero()
+
+
+def _contacts_by_grid(occ, shifted):
+    # sum over beads of the six face-neighbour occupancies (Alg. 2), halved
+    pad = np.pad(occ, 1)
+    x, y, z = (shifted + 1).T
+    tot = 0
+    for dx, dy, dz in ((1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)):
+        tot += int(pad[x + dx, y + dy, z + dz].sum())
+    assert tot % 2 == 0
+    return tot // 2
 
 
 @pytest.mark.parametrize("devs", [[0], [0, 0], [0, 0, 0, 0, 0]])
