@@ -263,7 +263,7 @@ def count_collisions_batch(vectors, space: LatticeSpace) -> list[CountReport]:
         return []
     # the library gathers the separate host vectors itself (threads, pinned
     # staging, int64 -> int32 narrowing): no host-side concatenation
-    ptrs = np.array([a.__array_interface__["data"][0] for a in arrays], dtype=np.uintp)
+    ptrs = np.array([_lib.host_address(a) for a in arrays], dtype=np.uintp)
     lengths = np.array([len(a) for a in arrays], dtype=np.int64)
     res = (_lib.LatticeResult * len(arrays))()
     lib = _lib.load()
