@@ -365,14 +365,20 @@ int stage_narrow_i64(const long long* src, long long n, long long a, int* dst, c
         CK(cudaHostAlloc(&sp.pinned, 2 * kStageThreads * kStageChunk, cudaHostAllocDefault));
         for (auto& e : sp.ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
+    for (auto& e : sp.ev) CK(cudaEventSynchronize(e));  // a previous call's copies out of the pool are done
     const long long total = 3 * n, per = (long long)(kStageChunk / 4);
     const long long nchunks = (total + per - 1) / per;
     const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
     const int nt = (int)std::min<long long>(std::min(hw, kStageThreads), nchunks);
     std::atomic<long long> next{0};
-    std::atomic<int> failed{0};
+    std::atomic<int> failed{0};  // first CUDA error of any worker (cudaError_t)
+    auto fail = [&](cudaError_t e) {
+        int none = 0;
+        failed.compare_exchange_strong(none, (int)e);
+    };
     auto work = [&](int t) {
-        if (cudaSetDevice(dev) != cudaSuccess) { failed = 1; return; }
+        cudaError_t e = cudaSetDevice(dev);
+        if (e != cudaSuccess) return fail(e);
         bool used[2] = {false, false};
         for (int k = 0; !failed; ++k) {
             const long long c = next.fetch_add(1);
@@ -380,18 +386,16 @@ int stage_narrow_i64(const long long* src, long long n, long long a, int* dst, c
             const int b = k & 1;
             int* buf = (int*)((char*)sp.pinned + (size_t)(2 * t + b) * kStageChunk);
             cudaEvent_t ev = sp.ev[2 * t + b];
-            if (used[b] && cudaEventSynchronize(ev) != cudaSuccess) { failed = 1; return; }
+            if (used[b] && (e = cudaEventSynchronize(ev)) != cudaSuccess) return fail(e);
             const long long lo = c * per, hi = std::min(total, lo + per);
             const long long* in = src + lo;
             for (long long q = 0; q < hi - lo; ++q) {
                 const long long x = in[q];
                 buf[q] = (x < -a || x > a) ? INT32_MAX : (int)x;
             }
-            if (cudaMemcpyAsync(dst + lo, buf, (size_t)(hi - lo) * 4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
-                cudaEventRecord(ev, s) != cudaSuccess) {
-                failed = 1;
-                return;
-            }
+            if ((e = cudaMemcpyAsync(dst + lo, buf, (size_t)(hi - lo) * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+                (e = cudaEventRecord(ev, s)) != cudaSuccess)
+                return fail(e);
             used[b] = true;
         }
     };
@@ -399,10 +403,7 @@ int stage_narrow_i64(const long long* src, long long n, long long a, int* dst, c
     for (int t = 0; t + 1 < nt; ++t) pool.emplace_back(work, t);
     work(nt - 1);
     for (auto& th : pool) th.join();
-    if (failed) {
-        CK(cudaGetLastError());
-        return arg_fail("staging host beads to the device failed");
-    }
+    if (failed) return cuda_fail("staging host beads to the device", (cudaError_t)failed.load());
     return PC_OK;
 }
 
