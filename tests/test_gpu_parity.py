@@ -703,3 +703,30 @@ def test_concurrent_callers():
         results = list(pool.map(job, range(8)))
     for k, out in enumerate(results):
         assert out[0::2] == [want[k]] * 5 and out[1::2] == [want_l[k]] * 5
+
+
+def test_concurrent_large_host_bead_vectors():
+    # several threads staging large int64 bead vectors at once (pinned chunk pool
+    # under the per-device arena lock): every count exact, every space clean after
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(21)
+    vecs = [rng.integers(-60, 61, size=(700_000 + 1000 * k, 3)) for k in range(4)]
+    want = []
+    for v in vecs:
+        _, cnt = np.unique(np.ravel_multi_index(tuple((v + 61).T), (123,) * 3), return_counts=True)
+        want.append((int((cnt * (cnt - 1) // 2).sum()), len(cnt)))
+
+    def job(k):
+        sp = pc.new_space(60)
+        out = []
+        for _ in range(3):
+            rep = pc.count_collisions(vecs[k], sp)
+            out.append((rep.count, rep.cells_touched))
+            pc.reset_sparse(sp)
+        return out, sp.is_zero()
+
+    with ThreadPoolExecutor(max_workers=4) as pool:
+        results = list(pool.map(job, range(4)))
+    for k, (out, clean) in enumerate(results):
+        assert out == [want[k]] * 3 and clean
