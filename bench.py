@@ -214,7 +214,8 @@ def secondary(torch, lib, stream):
     rows = {}
     for label, sched, tiling in (("naive_standard_per_row_tile", _lib.PC_STANDARD, _lib.PC_TILE_PER_ROW_TILE),
                                  ("balanced_per_row_tile", _lib.PC_BALANCED, _lib.PC_TILE_PER_ROW_TILE),
-                                 ("balanced_uniform_tiles", _lib.PC_BALANCED, _lib.PC_TILE_FLAT)):
+                                 ("balanced_uniform_tiles", _lib.PC_BALANCED, _lib.PC_TILE_FLAT),
+                                 ("balanced_uniform_tiles_tensor_cores", _lib.PC_BALANCED, _lib.PC_TILE_TC)):
         for _ in range(3):
             _lib.pairs_async(d2.data_ptr(), _lib.PC_F32, n2, _lib.PC_COLLISION, sched, np.array([0, n2]),
                              ws.data_ptr(), ws.numel(), res.data_ptr(), stream.cuda_stream, tiling)
@@ -231,6 +232,8 @@ def secondary(torch, lib, stream):
     rows["naive_over_balanced_time"] = rows["naive_standard_per_row_tile"]["kernel_ms"] / \
         rows["balanced_uniform_tiles"]["kernel_ms"]
     rows["paper_reference_ratio"] = "1.12x on P100 for N > 525,000 (PAPER.md:419)"
+    rows["tensor_cores_over_ffma_speedup"] = rows["balanced_uniform_tiles"]["kernel_ms"] / \
+        rows["balanced_uniform_tiles_tensor_cores"]["kernel_ms"]
     out["cfg2_naive_vs_balanced_n65536"] = rows
     del d2, ws
 
@@ -242,33 +245,42 @@ def secondary(torch, lib, stream):
     d3 = torch.from_numpy(obj3).cuda()
     ws3 = torch.empty(_lib.workspace_bytes(n3), dtype=torch.uint8, device="cuda")
     pairs3 = n3 * (n3 - 1) // 2
-    for _ in range(2):
-        _lib.pairs_async(d3.data_ptr(), _lib.PC_F32, n3, _lib.PC_COLLISION, _lib.PC_BALANCED, np.array([0, n3]),
-                         ws3.data_ptr(), ws3.numel(), res.data_ptr(), stream.cuda_stream, _lib.PC_TILE_FLAT)
-    torch.cuda.synchronize()
-    _lib.kernel_timing(True)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 5
-    e0.record(stream)
-    for _ in range(reps):
-        _lib.pairs_async(d3.data_ptr(), _lib.PC_F32, n3, _lib.PC_COLLISION, _lib.PC_BALANCED, np.array([0, n3]),
-                         ws3.data_ptr(), ws3.numel(), res.data_ptr(), stream.cuda_stream, _lib.PC_TILE_FLAT)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms_k, cnt_k = _lib.kernel_timing_read()
-    _lib.kernel_timing(False)
-    dev_ms = e0.elapsed_time(e1) / reps
+
+    def count_leg(tiling, reps=5):
+        for _ in range(2):
+            _lib.pairs_async(d3.data_ptr(), _lib.PC_F32, n3, _lib.PC_COLLISION, _lib.PC_BALANCED, np.array([0, n3]),
+                             ws3.data_ptr(), ws3.numel(), res.data_ptr(), stream.cuda_stream, tiling)
+        torch.cuda.synchronize()
+        _lib.kernel_timing(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            _lib.pairs_async(d3.data_ptr(), _lib.PC_F32, n3, _lib.PC_COLLISION, _lib.PC_BALANCED, np.array([0, n3]),
+                             ws3.data_ptr(), ws3.numel(), res.data_ptr(), stream.cuda_stream, tiling)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms, cnt = _lib.kernel_timing_read()
+        _lib.kernel_timing(False)
+        return ms / cnt, e0.elapsed_time(e1) / reps, int(res[0].item()), int(res[3].item())
+
+    k_ffma, dev_ffma, count_ffma, checks_ffma = count_leg(_lib.PC_TILE_FLAT)
+    k_tc, dev_tc, count_tc, checks_tc = count_leg(_lib.PC_TILE_AUTO)  # 2^20: the tensor-core kernel
     t0 = time.perf_counter()
     r3 = se.spi_balanced(obj3, se.collision_indicator)
     api_ms = (time.perf_counter() - t0) * 1e3
     out["cfg3_collision_count_n2^20"] = {
-        "count": int(res[0].item()), "api_count": int(r3.total),
-        "kernel_ms": ms_k / cnt_k, "device_ms_per_call": dev_ms,
-        "Gpair_per_s_kernel": pairs3 / (ms_k / cnt_k * 1e-3) / 1e9,
+        "count": count_tc, "api_count": int(r3.total), "ffma_count": count_ffma,
+        "kernel_ms": k_tc, "device_ms_per_call": dev_tc, "exact_checks": checks_tc,
+        "Gpair_per_s_kernel": pairs3 / (k_tc * 1e-3) / 1e9,
         "api_wall_ms": api_ms,
         "api_path": "spi_balanced(points, collision_indicator): numpy (n,3) f32 -> ctypes pc_pairs_host "
-                    "(H2D, prep, Gram-filter kernel, finalize, D2H) -> SpiResult",
-        "kernel": "pairs_kernel<128,12,192,GRAM,FLAT>"}
+                    "(H2D, prep, tensor-core Gram filter, exact pass, finalize, D2H) -> SpiResult",
+        "kernel": "pairs_tc_kernel (tcgen05.mma kind::tf32, 3xTF32 Gram filter, TMEM drained by 8 warps) + "
+                  "tc_exact_kernel",
+        "ffma_kernel": "pairs_kernel<128,12,192,GRAM,FLAT>", "ffma_kernel_ms": k_ffma,
+        "ffma_device_ms_per_call": dev_ffma, "ffma_exact_checks": checks_ffma,
+        "ffma_Gpair_per_s_kernel": pairs3 / (k_ffma * 1e-3) / 1e9}
+    ms_k, cnt_k = k_ffma, 1  # the naive comparison below is against the same FFMA inner code
     # the paper's comparison in its large-N regime (N > 525,000): the straightforward
     # scheme (standard schedule, one warp per row tile) on the same inner code
     _lib.kernel_timing(True)

@@ -63,6 +63,9 @@ extern "C" {
                               the schedule is standard                                         */
 #define PC_TILE_FLAT 2     /* balanced schedule lifted to uniform tiles: the (row tile, column)
                               space of equal-length windows split evenly over a persistent grid */
+#define PC_TILE_TC 3       /* the FLAT count on the tensor cores (tcgen05 Gram filter + exact
+                              re-check); counts only, balanced schedule, one whole-range call.
+                              PC_TILE_AUTO picks it for such calls with 2^14 <= n < 2^21      */
 
 typedef struct {
     int64_t count;         /* integer pair count (collisions / coincidences / contacts)           */

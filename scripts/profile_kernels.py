@@ -1,6 +1,6 @@
 """Run each hot kernel a few times on its benchmark size, for ncu captures.
 
-    python scripts/profile_kernels.py [direct|gram|gram_std|cfg2|cfg4|lattice|all] [--reps R]
+    python scripts/profile_kernels.py [direct|gram|tc|tc4|gram_std|cfg2|cfg4|lattice|all] [--reps R]
 
 Prints one timing line per case (CUDA events around the main kernel via
 pc_kernel_timing); the numbers under ncu are not bench values.
@@ -81,6 +81,16 @@ def main():
         pairs_case("direct_flat_2^20", 2**20, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, _lib.PC_TILE_FLAT, a.reps)
     if w in ("gram", "all"):
         pairs_case("gram_flat_2^20", 2**20, _lib.PC_COLLISION, _lib.PC_BALANCED, _lib.PC_TILE_FLAT, a.reps)
+    if w in ("tc", "all"):
+        pairs_case("tc_2^20", 2**20, _lib.PC_COLLISION, _lib.PC_BALANCED, _lib.PC_TILE_TC, a.reps)
+        pairs_case("tc_65536", 65536, _lib.PC_COLLISION, _lib.PC_BALANCED, _lib.PC_TILE_TC, a.reps, seed=0)
+    if w == "tc_small":
+        for n in (4096, 8192, 16384, 32768):
+            pairs_case(f"tc_{n}", n, _lib.PC_COLLISION, _lib.PC_BALANCED, _lib.PC_TILE_TC, a.reps, seed=0)
+            pairs_case(f"gram_flat_{n}", n, _lib.PC_COLLISION, _lib.PC_BALANCED, _lib.PC_TILE_FLAT, a.reps, seed=0)
+    if w in ("tc4", "all"):
+        pairs_case("tc_clustered_2^22", 2**22, _lib.PC_COLLISION, _lib.PC_BALANCED, _lib.PC_TILE_TC, a.reps,
+                   obj=gen.clustered_spheres(2**22).astype(np.float32))
     if w in ("gram_std", "all"):
         pairs_case("gram_naive_2^20", 2**20, _lib.PC_COLLISION, _lib.PC_STANDARD, _lib.PC_TILE_PER_ROW_TILE, a.reps)
     if w in ("cfg2", "all"):
