@@ -14,6 +14,9 @@
 //   pairs_kernel.cuh  the all-pairs kernel: warp-private row tiles, packed
 //                     FP32 Gram filter (count) / direct formula (sum), exact
 //                     re-check slow path, FLAT uniform tiles with dynamic claims
+//   pairs_tc.cuh      the count filter on the tensor cores: tcgen05.mma tf32
+//                     (3xTF32) into TMEM, warp-specialised loader / MMA /
+//                     drain warps, candidate queues + exact pass
 //   lattice.cuh       counting-array kernels (sparse regime) and the driver
 //   lattice_slab.cuh  dense regime: key partition + shared-memory slabs + TMA
 //                     bulk stores
