@@ -69,6 +69,30 @@ def check_spi(rng, stats):
                       f"[{b.start},{b.stop}): got {got} want {want}", flush=True)
 
 
+def check_tc(rng, stats):
+    # the tensor-core count filter forced at any size (PC_TILE_TC), every distribution,
+    # float and integer predicates
+    n = int(rng.choice([2, 9, 127, 129, 255, 257, 1000, 4097, 8191, 12345, 20000]))
+    pts, kind = random_points(rng, n)
+    (r,) = _lib.pairs_host(np.ascontiguousarray(pts), _lib.PC_COLLISION, _lib.PC_BALANCED, [0, n],
+                           tiling=_lib.PC_TILE_TC)
+    want = c_oracle.rows(pts, 0, n, "balanced")[0]
+    ok = r.count == want and r.error == 0
+    stats[("tc-count", ok)] += 1
+    if not ok:
+        print(f"MISMATCH tc-count n={n} {kind} {pts.dtype}: got {r.count} want {want}", flush=True)
+    span = int(rng.integers(1, 30))
+    beads = rng.integers(-span, span + 1, size=(n, 3))
+    if rng.random() < 0.3:
+        beads += np.int64(rng.integers(-2**40, 2**40))
+    col, con = c_oracle.int_pairs(beads)
+    for name, inter, want in (("tc-coincide", _lib.PC_COINCIDE, col), ("tc-manhattan1", _lib.PC_MANHATTAN1, con)):
+        (r,) = _lib.pairs_host(beads, inter, _lib.PC_BALANCED, [0, n], tiling=_lib.PC_TILE_TC)
+        stats[(name, r.count == want)] += 1
+        if r.count != want:
+            print(f"MISMATCH {name} n={n} span={span}: got {r.count} want {want}", flush=True)
+
+
 def check_int(rng, stats):
     n = int(rng.choice([1, 2, 5, 100, 1000, 4096, 5000, 20000]))
     span = int(rng.integers(1, 40))
@@ -122,6 +146,7 @@ def main():
         check_spi(rng, stats)
         check_int(rng, stats)
         check_lattice(rng, stats)
+        check_tc(rng, stats)
         rounds += 1
     fams = sorted({k for k, _ in stats})
     bad = 0
