@@ -4,6 +4,7 @@
 //   DIRECT: p = 1 + (x_i-x_j)^2 + (y_i-y_j)^2 + (z_i-z_j)^2   3 FADD2 + 3 FFMA2 per 2 pairs
 //   GRAM:   p = A_i + (B_j - 2 a_i.b_j), A_i = 1 + |a_i|^2     3 FFMA2 + 1 FADD2 per 2 pairs
 //   DIRECT-ASM: DIRECT with the library's inline-asm broadcast subtract (f2_rsub)
+//   DIRECT+EPI: DIRECT-ASM plus the library's per-chunk epilogue (fp64 row sums, flags)
 // and for both: 1/pa + 1/pc = (pa + pc) * rcp(pa * pc)       FMUL2 + FADD2 + 2 MUFU + FFMA2 per 4 pairs
 // Prints Tpair/s (the library's sum kernel: 4.41 at N = 2^20).  (The Gram form needs local origins to be accurate; this measures
 // only the instruction cost.)
@@ -50,6 +51,8 @@ __global__ void __launch_bounds__(128, 4) k(const float4* __restrict__ cols, flo
     float2 acc[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = make_float2(0.f, 0.f);
+    double dsum = 0.0;
+    unsigned flags = 0;
     for (int it = 0; it < reps; ++it) {
 #pragma unroll 2
         for (int k2 = 0; k2 < W; k2 += 4) {  // two column pairs per step
@@ -66,7 +69,7 @@ __global__ void __launch_bounds__(128, 4) k(const float4* __restrict__ cols, flo
                                                __ffma2_rn(f2(rx[r]), make_float2(A1.x, A1.y), make_float2(B1.z, B1.w))));
                     pa = __fadd2_rn(pa, f2(ra[r]));
                     pc = __fadd2_rn(pc, f2(ra[r]));
-                } else if (GRAM == 2) {
+                } else if (GRAM == 2 || GRAM == 3) {
                     float2 dx = f2_rsub(rx[r], make_float2(A0.x, A0.y));
                     float2 dy = f2_rsub(ry[r], make_float2(A0.z, A0.w));
                     float2 dz = f2_rsub(rz[r], make_float2(B0.x, B0.y));
@@ -89,7 +92,19 @@ __global__ void __launch_bounds__(128, 4) k(const float4* __restrict__ cols, flo
                 acc[r] = __ffma2_rn(sm, make_float2(rcp_approx(pr.x), rcp_approx(pr.y)), acc[r]);
             }
         }
+        if (GRAM == 3) {  // the library's per-chunk epilogue: fp64 row sums + conservative contact flags
+            unsigned fl = 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const float cs = acc[r].x + acc[r].y;
+                dsum += (double)cs;
+                fl |= (cs > 0.4999f ? 1u : 0u) << r;
+                acc[r] = make_float2(0.f, 0.f);
+            }
+            if (__any_sync(0xffffffffu, fl != 0)) flags |= fl;
+        }
     }
+    if (GRAM == 3) acc[0].x += (float)dsum + (float)flags;
     float t = 0.f;
 #pragma unroll
     for (int r = 0; r < R; ++r) t += acc[r].x + acc[r].y;
@@ -111,7 +126,7 @@ void run(const float4* d, float* o, int sms, long long* cyc) {
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     const double pairs = (double)grid * 128 * R * W * reps;
-    printf("%s: %.3f ms, %.3f Tpair/s\n", GRAM == 1 ? "gram      " : GRAM == 2 ? "direct-asm" : "direct    ", ms,
+    printf("%s: %.3f ms, %.3f Tpair/s\n", GRAM == 1 ? "gram      " : GRAM == 2 ? "direct-asm" : GRAM == 3 ? "direct+epi" : "direct    ", ms,
            pairs / (ms * 1e-3) / 1e12);
 }
 
@@ -131,6 +146,7 @@ int main() {
         run<0>(d, o, sms, cyc);
         run<1>(d, o, sms, cyc);
         run<2>(d, o, sms, cyc);
+        run<3>(d, o, sms, cyc);
     }
     return 0;
 }
