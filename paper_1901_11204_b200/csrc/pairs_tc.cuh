@@ -38,7 +38,7 @@ constexpr int kTcABytes = kTcM * 64, kTcBBytes = kTcN * 64;
 constexpr int kTcSmem = 2 * kTcABytes + kTcStages * kTcBBytes + 1024;  // > half the SM: one CTA per SM
 // PC_TILE_AUTO's range for it: below, the FFMA kernel's small-tile config wins; from
 // 2^21 up it stays on the FFMA kernel, whose exact path degrades more gracefully when
-// the data are clustered (2^22 clustered spheres: 1.57 s here vs 1.08 s, 350M vs 125M
+// the data are clustered (2^22 clustered spheres: 1.38 s here vs 1.08 s, 214M vs 125M
 // candidates through the wider band).
 constexpr long long kTcMinN = 1 << 14, kTcMaxN = 1 << 21;
 
