@@ -37,10 +37,11 @@ __global__ void __launch_bounds__(128, 4) k(const float4* __restrict__ cols, flo
     __syncthreads();
     float rx[R], ry[R], rz[R], ra[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-        rx[r] = 0.01f * (threadIdx.x + r);
-        ry[r] = 0.02f * r;
-        rz[r] = 0.03f * threadIdx.x;
+    for (int r = 0; r < R; ++r) {  // runtime row values (constants would fold into immediates)
+        const float4 rv = cols[(threadIdx.x * R + r) % W];
+        rx[r] = rv.x + 0.01f * r;
+        ry[r] = rv.y - 0.02f * r;
+        rz[r] = rv.z + 0.03f * threadIdx.x;
         ra[r] = 1.0f + rx[r] * rx[r] + ry[r] * ry[r] + rz[r] * rz[r];
         if (GRAM == 1) {
             rx[r] *= -2.f;
