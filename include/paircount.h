@@ -64,8 +64,9 @@ extern "C" {
 #define PC_TILE_FLAT 2     /* balanced schedule lifted to uniform tiles: the (row tile, column)
                               space of equal-length windows split evenly over a persistent grid */
 #define PC_TILE_TC 3       /* the FLAT count on the tensor cores (tcgen05 Gram filter + exact
-                              re-check); counts only, balanced schedule, one whole-range call.
-                              PC_TILE_AUTO picks it for such calls with 2^14 <= n < 2^21      */
+                              re-check); counts only, balanced schedule, any row ranges.
+                              PC_TILE_AUTO picks it when 2^14 <= n < 2^21 and the ranges
+                              cover at least n/8 rows                                          */
 
 typedef struct {
     int64_t count;         /* integer pair count (collisions / coincidences / contacts)           */

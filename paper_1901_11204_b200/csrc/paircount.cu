@@ -468,7 +468,7 @@ struct KernelCfg {
 #endif
 constexpr KernelCfg kBig{4, PC_BIG_R, 256};  // direct (sum) kernel: warp tile 32*R rows (256 by default)
 #ifndef PC_TC_AUTO
-#define PC_TC_AUTO 1  // whole-range balanced counts with kTcMinN <= n < kTcMaxN take the tensor-core kernel
+#define PC_TC_AUTO 1  // balanced counts with kTcMinN <= n < kTcMaxN (rows >= n/8) take the tensor-core kernel
 #endif
 #ifndef PC_GRAM_R
 #define PC_GRAM_R 12
@@ -500,7 +500,7 @@ WsLayout ws_layout(long long n) {
     l.slots = l.stats + 256;
     l.tc_a = align_up(l.slots + (size_t)max_slots(n) * sizeof(Slot), 1024);
     const TcGeom g = tc_geom(n < 0 ? 0 : n);  // tensor-core count kernel operands (64 B per staged point)
-    l.tc_b = align_up(l.tc_a + (size_t)g.n_tiles * kTcM * 64, 1024);
+    l.tc_b = align_up(l.tc_a + (size_t)g.n_rows * 64, 1024);
     l.tc_cand = align_up(l.tc_b + (size_t)g.n_ext * 64, 256);
     l.tc_cnt = align_up(l.tc_cand + (size_t)tc_cand_cap(n) * sizeof(uint2), 256);
     l.total = align_up(l.tc_cnt + 4 * 1024, 256);  // per-CTA queue lengths
@@ -592,16 +592,15 @@ int dispatch_cfg(PairsArgs args, bool flat, long long cap, int* nslots, cudaStre
     return launch_pairs<WARPS, R, W, DIRECT, false, COMP>(args, cap, nslots, s);
 }
 
-// The whole-range balanced count on the tensor cores (pairs_tc.cuh): operand staging,
-// the persistent kernel (one CTA per SM), the exact pass over its queued candidates,
-// the fixed-order slot sum.
-int run_pairs_tc(const PairsArgs& p, char* ws, const WsLayout& lay, long long n, long long cap,
-                 pc_pairs_result* dres, cudaStream_t s) {
+// Balanced counts on the tensor cores (pairs_tc.cuh): operands staged once per call,
+// then per row range the persistent kernel (one CTA per SM), the exact pass over its
+// queued candidates and the fixed-order slot sum.
+int run_pairs_tc(const PairsArgs& p, char* ws, const WsLayout& lay, long long n, long long cap, int nranges,
+                 const long long* bounds, pc_pairs_result* dres, cudaStream_t s) {
     const TcGeom g = tc_geom(n);
-    const long long npts = std::max(g.n_tiles * kTcM, g.n_ext);
+    const long long npts = std::max(g.n_rows, g.n_ext);
     const int pblocks = (int)std::min<long long>((npts + 255) / 256, (long long)num_sms() * 8);
-    prep_tc_kernel<<<pblocks, 256, 0, s>>>(p.xyz, p.dtype, n, p.st, g.n_tiles * kTcM, g.n_ext, ws + lay.tc_a,
-                                           ws + lay.tc_b);
+    prep_tc_kernel<<<pblocks, 256, 0, s>>>(p.xyz, p.dtype, n, p.st, g.n_rows, g.n_ext, ws + lay.tc_a, ws + lay.tc_b);
     CK_LAUNCH("prep_tc_kernel");
     static thread_local bool attr_set[64] = {false};
     int dev = 0;
@@ -623,33 +622,43 @@ int run_pairs_tc(const PairsArgs& p, char* ws, const WsLayout& lay, long long n,
     a.pred = p.pred;
     a.n = (int)n;
     a.thr = p.thr;
-    a.n_tiles = g.n_tiles;
     a.chunks = g.chunks;
-    a.items = g.n_tiles * g.chunks;
-    const int grid = (int)std::min<long long>(std::min(num_sms(), 1024), a.items);
     a.cand = (uint2*)(ws + lay.tc_cand);
     a.cand_counts = (unsigned*)(ws + lay.tc_cnt);
-    a.cand_per_cta = tc_cand_cap(n) / grid;
-    if (2 * grid > cap) return arg_fail("workspace too small for the CTA slots");
-    a.group = (int)std::max(1LL, std::min(16LL, a.items / ((long long)grid * 16)));
-    CK(cudaMemsetAsync(p.work_ctr, 0, sizeof(unsigned long long), s));
-    EvPair* ev = nullptr;
-    if (g_timing && g_ev_used < 4096) {
-        if (g_ev_used == g_ev_made) {
-            CK(cudaEventCreate(&g_ev[g_ev_made].a));
-            CK(cudaEventCreate(&g_ev[g_ev_made].b));
-            ++g_ev_made;
+    for (int k = 0; k < nranges; ++k) {
+        const long long lo = bounds[k], hi = bounds[k + 1];
+        int nslots = 0;
+        if (hi > lo) {
+            a.lo = (int)lo;
+            a.hi = (int)hi;
+            a.lo8 = (int)(lo & ~7LL);
+            a.n_tiles = (hi - a.lo8 + kTcM - 1) / kTcM;
+            a.items = a.n_tiles * g.chunks;
+            const int grid = (int)std::min<long long>(std::min(num_sms(), 1024), a.items);
+            a.cand_per_cta = tc_cand_cap(n) / grid;
+            a.group = (int)std::max(1LL, std::min(16LL, a.items / ((long long)grid * 16)));
+            if (2 * grid > cap) return arg_fail("workspace too small for the CTA slots");
+            CK(cudaMemsetAsync(p.work_ctr, 0, sizeof(unsigned long long), s));
+            EvPair* ev = nullptr;
+            if (g_timing && g_ev_used < 4096) {
+                if (g_ev_used == g_ev_made) {
+                    CK(cudaEventCreate(&g_ev[g_ev_made].a));
+                    CK(cudaEventCreate(&g_ev[g_ev_made].b));
+                    ++g_ev_made;
+                }
+                ev = &g_ev[g_ev_used++];
+                CK(cudaEventRecord(ev->a, s));
+            }
+            pairs_tc_kernel<<<grid, kTcWarps * 32, kTcSmem, s>>>(a);
+            CK_LAUNCH("pairs_tc_kernel");
+            tc_exact_kernel<<<grid, 256, 0, s>>>(a, p.slots + grid);
+            CK_LAUNCH("tc_exact_kernel");
+            if (ev) CK(cudaEventRecord(ev->b, s));
+            nslots = 2 * grid;
         }
-        ev = &g_ev[g_ev_used++];
-        CK(cudaEventRecord(ev->a, s));
+        finalize_kernel<<<1, 256, 0, s>>>(p.slots, nslots, p.st, row_pairs(n, lo, hi, PC_BALANCED), 0, dres + k);
+        CK_LAUNCH("finalize_kernel");
     }
-    pairs_tc_kernel<<<grid, kTcWarps * 32, kTcSmem, s>>>(a);
-    CK_LAUNCH("pairs_tc_kernel");
-    tc_exact_kernel<<<grid, 256, 0, s>>>(a, p.slots + grid);
-    CK_LAUNCH("tc_exact_kernel");
-    if (ev) CK(cudaEventRecord(ev->b, s));
-    finalize_kernel<<<1, 256, 0, s>>>(p.slots, 2 * grid, p.st, row_pairs(n, 0, n, PC_BALANCED), 0, dres);
-    CK_LAUNCH("finalize_kernel");
     return PC_OK;
 }
 
@@ -666,11 +675,13 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     if (nranges < 1 || !bounds) return arg_fail("need at least one row range");
     for (int k = 0; k < nranges; ++k)
         if (bounds[k] < 0 || bounds[k] > bounds[k + 1] || bounds[k + 1] > n) return arg_fail("bad row range bounds");
-    const bool whole = nranges == 1 && bounds[0] == 0 && bounds[1] == n;
-    const bool tc_ok = interaction != PC_COLLISION_INVSQ && schedule == PC_BALANCED && whole && n >= 2;
+    const bool tc_ok = interaction != PC_COLLISION_INVSQ && schedule == PC_BALANCED && n >= 2;
     if (tiling == PC_TILE_TC && !tc_ok)
-        return arg_fail("PC_TILE_TC needs a count interaction, the balanced schedule and the whole row range");
-    const bool use_tc = tc_ok && (tiling == PC_TILE_TC || (tiling == PC_TILE_AUTO && PC_TC_AUTO && n >= kTcMinN && n < kTcMaxN));
+        return arg_fail("PC_TILE_TC needs a count interaction and the balanced schedule");
+    long long rows = 0;  // AUTO: ranges of a few tiles stay on the FFMA kernel (the staging is per call)
+    for (int k = 0; k < nranges; ++k) rows += std::max(0LL, (long long)(bounds[k + 1] - bounds[k]));
+    const bool use_tc = tc_ok && (tiling == PC_TILE_TC || (tiling == PC_TILE_AUTO && PC_TC_AUTO && n >= kTcMinN &&
+                                                             n < kTcMaxN && rows * 8 >= n));
     if (tiling == PC_TILE_AUTO || tiling == PC_TILE_TC)
         tiling = schedule == PC_BALANCED ? PC_TILE_FLAT : PC_TILE_PER_ROW_TILE;
     if (tiling == PC_TILE_FLAT && schedule != PC_BALANCED)
@@ -711,7 +722,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     args.sched = schedule;
     args.n = (int)n;
     const long long cap = max_slots(n);
-    if (use_tc) return run_pairs_tc(args, ws, lay, n, cap, dres, s);
+    if (use_tc) return run_pairs_tc(args, ws, lay, n, cap, nranges, bounds, dres, s);
     for (int k = 0; k < nranges; ++k) {
         const long long lo = bounds[k], hi = bounds[k + 1];
         int nslots = 0;

@@ -51,19 +51,23 @@ __host__ __device__ inline long long tc_cand_cap(long long n) {
     return c < (1 << 16) ? (1 << 16) : c > (1 << 24) ? (1 << 24) : c;
 }
 
+// Operands are staged once per call in absolute point order; a row range [lo, hi) runs
+// tiles from lo8 = lo rounded down to the 8-point operand group, rows outside [lo, hi)
+// masked.  So the row operand covers up to n + 135 rows and the column operand up to
+// n + 135 + chunks * 256 points.
 struct TcGeom {
-    long long n_tiles, chunks, n_ext;  // row tiles, chunks per tile window, staged column points
+    long long chunks, n_rows, n_ext;  // chunks per tile window, staged row / column points
 };
 __host__ __device__ inline TcGeom tc_geom(long long n) {
     TcGeom g;
-    g.n_tiles = (n + kTcM - 1) / kTcM;
     g.chunks = (kTcM + n / 2 + kTcN - 1) / kTcN;  // s up to 127 + n/2
-    g.n_ext = g.n_tiles * kTcM + g.chunks * kTcN;
+    g.n_rows = ((n + 8 + kTcM - 1) / kTcM + 1) * kTcM;
+    g.n_ext = g.n_rows + g.chunks * kTcN;
     return g;
 }
 
 struct TcArgs {
-    const float4* aop;  // row operand, n_tiles*128 points (zeros past n)
+    const float4* aop;  // row operand, n_rows points (zeros past n)
     const float4* bop;  // column operand, n_ext points
     const float4* pts_even;  // pairs_kernel staging: w_i for the row thresholds
     const float4* pts_odd;
@@ -75,6 +79,7 @@ struct TcArgs {
     unsigned* cand_counts;  // queue length of each CTA
     long long cand_per_cta;
     int dtype, pred, n;
+    int lo, hi, lo8;  // the row range; tiles start at lo8 = lo & ~7
     float thr;
     long long n_tiles, chunks, items;
     int group;  // items per claim
@@ -234,7 +239,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) pairs_tc_kernel(const TcArgs
                     abuf ^= 1;
                     if (aloads[abuf] > 0) mbar_wait(a_empty + 8 * abuf, (unsigned)((aloads[abuf] - 1) & 1));
                     mbar_expect_tx(a_full + 8 * abuf, kTcABytes);
-                    bulk_g2s(sA + abuf * kTcABytes, (const char*)a.aop + tc_off(t * kTcM, 0), kTcABytes,
+                    bulk_g2s(sA + abuf * kTcABytes, (const char*)a.aop + tc_off(a.lo8 + t * kTcM, 0), kTcABytes,
                              a_full + 8 * abuf);
                     ++aloads[abuf];
                     cur_tile = t;
@@ -242,7 +247,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) pairs_tc_kernel(const TcArgs
                 }
                 s_item[sg] = (t << 24) | c | ((long long)abuf << 62) | flag;
                 mbar_expect_tx(b_full + 8 * sg, kTcBBytes);
-                bulk_g2s(sB + sg * kTcBBytes, (const char*)a.bop + tc_off(t * kTcM + c * kTcN, 0), kTcBBytes,
+                bulk_g2s(sB + sg * kTcBBytes, (const char*)a.bop + tc_off(a.lo8 + t * kTcM + c * kTcN, 0), kTcBBytes,
                          b_full + 8 * sg);
                 if (++c == C) {
                     c = 0;
@@ -311,10 +316,11 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) pairs_tc_kernel(const TcArgs
             if (item < 0) break;
             const long long t = item >> 24, c = item & ((1ll << 24) - 1);
             const int rl = quad * 32 + lane;
-            const long long i = t * kTcM + rl;
+            const long long i = a.lo8 + t * kTcM + rl;
+            const bool valid = i >= a.lo && i < a.hi;
             if (t != cur_tile) {
                 cur_tile = t;
-                if (i < n) {
+                if (valid) {
                     const float4 e = ((i & 1) ? a.pts_odd : a.pts_even)[2 * (i >> 1) + 1];
                     rc = force ? -INFINITY : -e.z - half_tb;  // e = (z_i, z_i1, w_i, w_i1)
                     lim = steps_for_dev(n, (int)i);
@@ -345,7 +351,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) pairs_tc_kernel(const TcArgs
             }
             // s of this lane's first column; rows own 1 <= s - rl <= lim
             const long long s0 = c * kTcN + half * 128;
-            const bool any_owned = i < n && s0 + 127 - rl >= 1 && s0 - rl <= lim;
+            const bool any_owned = valid && s0 + 127 - rl >= 1 && s0 - rl <= lim;
             const bool flag = any_owned && (force || max3f(bm[0], bm[1], fmaxf(bm[2], bm[3])) > rc);
             if (flag) {
                 // queue this row's owned candidates for the exact pass

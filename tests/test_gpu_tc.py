@@ -75,7 +75,7 @@ def test_tc_integer_predicates(seed):
 
 
 def test_tc_auto_dispatch_at_config2_size(golden_configs):
-    # PC_TILE_AUTO sends whole-range balanced counts with 2^14 <= n < 2^21 to the tensor
+    # PC_TILE_AUTO sends balanced counts with 2^14 <= n < 2^21 (ranges covering >= n/8 rows) to the tensor
     # cores: spi_balanced on config 2 keeps its golden count; a row-range call
     # (spi_parallel partials) stays on the FFMA kernel and agrees
     from tests.helpers import config_input
@@ -95,8 +95,32 @@ def test_tc_argument_errors():
         _tc(pts, _lib.PC_COLLISION_INVSQ)
     with pytest.raises(Exception, match="PC_TILE_TC"):
         _lib.pairs_host(pts, _lib.PC_COLLISION, _lib.PC_STANDARD, [0, 500], tiling=_lib.PC_TILE_TC)
-    with pytest.raises(Exception, match="PC_TILE_TC"):
-        _lib.pairs_host(pts, _lib.PC_COLLISION, _lib.PC_BALANCED, [0, 200, 500], tiling=_lib.PC_TILE_TC)
+
+
+@pytest.mark.parametrize("n", [1000, 4099])
+def test_tc_row_ranges_match_oracle_partials(n):
+    # row ranges (spi_parallel partials, spi_rows) on the tensor cores: tiles start at the
+    # range's 8-point group, rows outside the range masked; empty ranges give zero
+    pts = gen.random_spheres(n, (4.18879 * n) ** (1 / 3) / 1.26, 7).astype(np.float32)
+    bounds = [0, 13, 13, 500, 777, 778, n - 3, n]
+    res = _lib.pairs_host(pts, _lib.PC_COLLISION, _lib.PC_BALANCED, bounds, tiling=_lib.PC_TILE_TC)
+    for (lo, hi), r in zip(zip(bounds[:-1], bounds[1:]), res):
+        want, _, pairs = c_oracle.rows(pts, lo, hi, "balanced")
+        assert (r.count, r.pairs, r.error) == (want, pairs, 0), (lo, hi)
+    beads = gen.random_chain(n, 3)[0]
+    col, con = c_oracle.int_pairs(beads)
+    for inter, want in ((_lib.PC_COINCIDE, col), (_lib.PC_MANHATTAN1, con)):
+        res = _lib.pairs_host(beads, inter, _lib.PC_BALANCED, [0, 5, 333, n], tiling=_lib.PC_TILE_TC)
+        assert sum(r.count for r in res) == want
+
+
+def test_tc_auto_for_spi_parallel_partials():
+    # workers' ranges together cover n rows: PC_TILE_AUTO takes the tensor cores, and the
+    # partials equal the oracle's per-worker counts
+    pts = gen.random_spheres(40_000, 30.0, 11).astype(np.float32)
+    r = se.spi_parallel(pts, se.collision_indicator, workers=5, schedule="balanced")
+    for b, got in zip(se._partition(len(pts), 5), r.partials):
+        assert got == c_oracle.rows(pts, b.start, b.stop, "balanced")[0]
 
 
 def test_tc_exposed_through_the_drop_in_api():
