@@ -76,8 +76,8 @@ def test_tc_integer_predicates(seed):
 
 def test_tc_auto_dispatch_at_config2_size(golden_configs):
     # PC_TILE_AUTO sends balanced counts with 2^14 <= n < 2^21 (ranges covering >= n/8 rows) to the tensor
-    # cores: spi_balanced on config 2 keeps its golden count; a row-range call
-    # (spi_parallel partials) stays on the FFMA kernel and agrees
+    # cores: spi_balanced on config 2 keeps its golden count, and so do the summed
+    # spi_parallel partials and the FFMA kernel forced with PC_TILE_FLAT
     from tests.helpers import config_input
 
     pts = config_input(golden_configs, "cfg2")
