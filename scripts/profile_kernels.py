@@ -91,6 +91,11 @@ def main():
     if w in ("tc4", "all"):
         pairs_case("tc_clustered_2^22", 2**22, _lib.PC_COLLISION, _lib.PC_BALANCED, _lib.PC_TILE_TC, a.reps,
                    obj=gen.clustered_spheres(2**22).astype(np.float32))
+    if w == "tc4u":  # uniform 2^22 (config 4u) on both count kernels
+        obj = gen.random_spheres(2**22, 259.9657721761944, 2).astype(np.float32)
+        pairs_case("tc_uniform_2^22", 2**22, _lib.PC_COLLISION, _lib.PC_BALANCED, _lib.PC_TILE_TC, a.reps, obj=obj)
+        pairs_case("gram_flat_uniform_2^22", 2**22, _lib.PC_COLLISION, _lib.PC_BALANCED, _lib.PC_TILE_FLAT, a.reps,
+                   obj=obj)
     if w in ("gram_std", "all"):
         pairs_case("gram_naive_2^20", 2**20, _lib.PC_COLLISION, _lib.PC_STANDARD, _lib.PC_TILE_PER_ROW_TILE, a.reps)
     if w in ("cfg2", "all"):
