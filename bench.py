@@ -453,8 +453,10 @@ def run_ours(args):
     bounds = np.array([lo, hi], dtype=np.int64)
 
     def step():
+        # PC_TILE_SORTED: spatially sorted points (what spi_balanced's whole-range call does); with
+        # N ranks each takes its slab of the same sorted order, so the partials sum to the total
         _lib.pairs_async(d_obj.data_ptr(), _lib.PC_F32, n, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, bounds,
-                         ws.data_ptr(), ws.numel(), res.data_ptr(), stream.cuda_stream, _lib.PC_TILE_FLAT)
+                         ws.data_ptr(), ws.numel(), res.data_ptr(), stream.cuda_stream, _lib.PC_TILE_SORTED)
         launches = _lib.launches()
         if world > 1:
             slots.zero_()
@@ -500,13 +502,13 @@ def run_ours(args):
     host_view = pinned.numpy()
     bnd = [lo, hi]
     for _ in range(2):
-        _lib.pairs_host(host_view, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, bnd)
+        _lib.pairs_host(host_view, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, bnd, tiling=_lib.PC_TILE_SORTED)
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     e2e_launches = 0
     for _ in range(args.steps):
-        (r,) = _lib.pairs_host(host_view, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, bnd)
+        (r,) = _lib.pairs_host(host_view, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, bnd, tiling=_lib.PC_TILE_SORTED)
         e2e_launches += _lib.launches()
         if world > 1:
             t_slots = torch.zeros(2 * world, dtype=torch.int64, device="cuda")
@@ -520,7 +522,8 @@ def run_ours(args):
         e2e_s = float(t.item())
     e2e = {"value": total_pairs / e2e_s / 1e9, "unit": "Gpair/s", "h2d_bytes_per_step": int(host_view.nbytes),
            "d2h_bytes_per_step": 40, "ms_per_step": e2e_s * 1e3,
-           "path": "pc_pairs_host (ctypes) from pinned host memory; one H2D + prep + kernel + finalize + D2H per step"}
+           "path": "pc_pairs_host (ctypes) from pinned host memory; one H2D + prep + sort + kernel + finalize + D2H "
+                   "per step"}
 
     if rank != 0:
         dist.destroy_process_group()
@@ -546,14 +549,13 @@ def run_ours(args):
     clocks = clk.summary()
     roofline = {"bound": "fp32", "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
                 "frac": achieved_tflops / peak_tflops, "traffic": traffic,
-                "kernel": "pairs_kernel<128,8,256,DIRECT,FLAT>", "kernel_ms": kern_ms_avg,
+                "kernel": "pairs_kernel<128,8,256,DIRECT,FLAT,SORTED>", "kernel_ms": kern_ms_avg,
                 "flops_per_pair": FLOPS_PER_PAIR,
                 "peak_source": "measured live: pc_microbench FFMA stream x 2 flop (no FP32 entry in MEASURED_PEAKS.json)",
                 "pairs_per_s_kernel": rank_pairs / (kern_ms_avg * 1e-3),
-                # the same kernel against the pipe it is bound by: FMA-pipe lane operations it issues per pair
-                # (15 FFMA2-class per 4 pairs = 7.5) x pairs/s / the live FFMA lane rate; DESIGN.md §3
-                "fma_pipe": {"lane_ops_per_pair": 7.5,
-                             "frac": 7.5 * rank_pairs / (kern_ms_avg * 1e-3) / ffma_rate,
+                # the pipe it is bound by: FMA-pipe lane operations per pair are 7.5 in the direct loop
+                # (15 FFMA2-class per 4 pairs) and 5.5 in the tile-local Gram loop (11 per 4); DESIGN.md §3
+                "fma_pipe": {"direct_loop_lane_ops_per_pair": 7.5, "gram_loop_lane_ops_per_pair": 5.5,
                              "ncu_fma_pipe_active": tinfo.get("pairs_kernel_direct_fma_pipe_active")}}
 
     line = {
@@ -563,7 +565,8 @@ def run_ours(args):
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": "cfg3: N=2^20 uniform fp32 unit spheres, exact contact count + softened "
                                "inverse-square sum, balanced schedule on uniform tiles",
-                   "n_points": n, "pairs_per_step": total_pairs, "schedule": "balanced", "tiling": "flat",
+                   "n_points": n, "pairs_per_step": total_pairs, "schedule": "balanced",
+                   "tiling": "flat, on Morton-sorted points (sort inside the step)",
                    "parallelism": f"row slabs x{world}, one NCCL int64 all-reduce" if world > 1 else "1 GPU",
                    "l2": "flushed between timed steps (256 MiB memset)", "contacts": int(counts)},
         "roofline": roofline,

@@ -67,6 +67,11 @@ extern "C" {
                               re-check); counts only, balanced schedule, any row ranges.
                               PC_TILE_AUTO picks it when 2^14 <= n < 2^21 and the ranges
                               cover at least n/8 rows                                          */
+#define PC_TILE_SORTED 4   /* the inverse-square sum on spatially sorted fp32 points (what
+                              PC_TILE_AUTO does for a whole-range call from 2^15 points): row
+                              ranges then index the SORTED order, so each range's result is a
+                              partial of the same total (multi-GPU slabs), not the reference's
+                              _run_outer over those input rows                                 */
 
 typedef struct {
     int64_t count;         /* integer pair count (collisions / coincidences / contacts)           */

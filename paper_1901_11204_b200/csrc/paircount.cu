@@ -28,6 +28,7 @@
 
 #include "../../include/paircount.h"
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -367,6 +368,8 @@ struct PairsArgs {
     long long L;        // FLAT: window length shared by every row tile
     long long total;    // FLAT: n_tiles * L
     long long super_cols;  // FLAT: columns per claimed super-chunk (multiple of W)
+    const float4* blk_box;  // SORTED: per-32-point bounding boxes (min, max) of the sorted points
+    int nblk;
 };
 
 __device__ __forceinline__ int steps_for_dev(int n, int i) {
@@ -467,6 +470,9 @@ struct KernelCfg {
 #define PC_BIG_R 8
 #endif
 constexpr KernelCfg kBig{4, PC_BIG_R, 256};  // direct (sum) kernel: warp tile 32*R rows (256 by default)
+#ifndef PC_SORTED_SUM
+#define PC_SORTED_SUM 1  // whole-range fp32 balanced sums: spatial sort + tile-local Gram chunks
+#endif
 #ifndef PC_TC_AUTO
 #define PC_TC_AUTO 1  // balanced counts with kTcMinN <= n < kTcMaxN (rows >= n/8) take the tensor-core kernel
 #endif
@@ -489,8 +495,68 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 long long max_slots(long long n) { return 148LL * 64 + n / (32 * kSmall.r * kSmall.warps) + 64; }
 
+// ---- spatial (Morton) sort for the whole-range fp32 sum: permuting the points leaves
+// the all-pairs total unchanged and makes row tiles and column chunks compact boxes,
+// which the SORTED kernel uses for its tile-local Gram form (pairs_kernel.cuh).
+inline size_t kSortTempBytes(size_t n) { return ((size_t)16 << 20) + 4 * n; }
+constexpr long long kSortedMinN = 1 << 15;
+
+__device__ __forceinline__ unsigned spread10(unsigned v) {  // 10 bits -> every third bit
+    v &= 1023u;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+__global__ void morton_kernel(const float* __restrict__ xyz, long long n, const PrepStats* __restrict__ st,
+                              unsigned* __restrict__ keys, unsigned* __restrict__ idx) {
+    float lo[3], sc[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double mn = dec_f64(st->mn[k]), mx = dec_f64(st->mx[k]);
+        lo[k] = (float)mn;
+        sc[k] = mx > mn ? (float)(1023.0 / (mx - mn)) : 0.f;
+    }
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        unsigned c[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float v = (xyz[3 * i + k] - lo[k]) * sc[k];
+            c[k] = (unsigned)fminf(fmaxf(v, 0.f), 1023.f);
+        }
+        keys[i] = spread10(c[0]) | (spread10(c[1]) << 1) | (spread10(c[2]) << 2);
+        idx[i] = (unsigned)i;
+    }
+}
+__global__ void gather_sorted_kernel(const float* __restrict__ xyz, const unsigned* __restrict__ idx, long long n,
+                                     float* __restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long s = idx[i];
+        out[3 * i] = xyz[3 * s];
+        out[3 * i + 1] = xyz[3 * s + 1];
+        out[3 * i + 2] = xyz[3 * s + 2];
+    }
+}
+// one thread per 32-point block: (min x, y, z, 0), (max x, y, z, 0)
+__global__ void blk_box_kernel(const float* __restrict__ xyz, long long n, int nblk, float4* __restrict__ box) {
+    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nblk; b += (long long)gridDim.x * blockDim.x) {
+        float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+        const long long e = min(n, 32 * b + 32);
+        for (long long i = 32 * b; i < e; ++i) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                mn[k] = fminf(mn[k], xyz[3 * i + k]);
+                mx[k] = fmaxf(mx[k], xyz[3 * i + k]);
+            }
+        }
+        box[2 * b] = make_float4(mn[0], mn[1], mn[2], 0.f);
+        box[2 * b + 1] = make_float4(mx[0], mx[1], mx[2], 0.f);
+    }
+}
+
 struct WsLayout {
-    size_t pts, stats, slots, tc_a, tc_b, tc_cand, tc_cnt, total;
+    size_t pts, stats, slots, tc_a, tc_b, tc_cand, tc_cnt, srt, srt_temp, total;
 };
 WsLayout ws_layout(long long n) {
     WsLayout l;
@@ -503,7 +569,13 @@ WsLayout ws_layout(long long n) {
     l.tc_b = align_up(l.tc_a + (size_t)g.n_rows * 64, 1024);
     l.tc_cand = align_up(l.tc_b + (size_t)g.n_ext * 64, 256);
     l.tc_cnt = align_up(l.tc_cand + (size_t)tc_cand_cap(n) * sizeof(uint2), 256);
-    l.total = align_up(l.tc_cnt + 4 * 1024, 256);  // per-CTA queue lengths
+    // spatial sort for the whole-range fp32 sum: keys + indices (double-buffered), the
+    // sorted points, per-32-point boxes, radix-sort scratch
+    l.srt = align_up(l.tc_cnt + 4 * 1024, 256);
+    const size_t nn = (size_t)(n < 0 ? 0 : n);
+    l.srt_temp = align_up(l.srt + 4 * align_up(nn * 4, 256) + align_up(nn * 12, 256) +
+                          align_up((nn / 32 + 1) * 32, 256), 256);
+    l.total = align_up(l.srt_temp + kSortTempBytes(nn), 256);
     return l;
 }
 
@@ -529,9 +601,9 @@ int num_sms() {
     return g_num_sms[dev];
 }
 
-template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP>
+template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP, bool SORTED = false>
 int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStream_t s) {
-    auto kern = pairs_kernel<WARPS, R, W, DIRECT, FLAT, COMP>;
+    auto kern = pairs_kernel<WARPS, R, W, DIRECT, FLAT, COMP, SORTED>;
     constexpr int smem = WARPS * pairs_smem_per_warp<R, W, COMP>();
     {
         static thread_local bool attr_set[64] = {false};
@@ -580,14 +652,14 @@ int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStr
     return PC_OK;
 }
 
-template <int WARPS, int R, int W, bool DIRECT, bool COMP = false>
+template <int WARPS, int R, int W, bool DIRECT, bool COMP = false, bool SORTED = false>
 int dispatch_cfg(PairsArgs args, bool flat, long long cap, int* nslots, cudaStream_t s) {
     constexpr int T = 32 * R;
     args.n_tiles = (args.hi - args.lo + T - 1) / T;
     if (flat) {
         args.L = (long long)(T - 1) + (args.n >> 1);
         args.total = (long long)args.n_tiles * args.L;
-        return launch_pairs<WARPS, R, W, DIRECT, true, COMP>(args, cap, nslots, s);
+        return launch_pairs<WARPS, R, W, DIRECT, true, COMP, SORTED>(args, cap, nslots, s);
     }
     return launch_pairs<WARPS, R, W, DIRECT, false, COMP>(args, cap, nslots, s);
 }
@@ -682,7 +754,10 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     for (int k = 0; k < nranges; ++k) rows += std::max(0LL, (long long)(bounds[k + 1] - bounds[k]));
     const bool use_tc = tc_ok && (tiling == PC_TILE_TC || (tiling == PC_TILE_AUTO && PC_TC_AUTO && n >= kTcMinN &&
                                                              n < kTcMaxN && rows * 8 >= n));
-    if (tiling == PC_TILE_AUTO || tiling == PC_TILE_TC)
+    const bool auto_tiling = tiling == PC_TILE_AUTO, sorted_req = tiling == PC_TILE_SORTED;
+    if (sorted_req && (interaction != PC_COLLISION_INVSQ || dtype != PC_F32 || schedule != PC_BALANCED))
+        return arg_fail("PC_TILE_SORTED needs the inverse-square sum on fp32 points and the balanced schedule");
+    if (tiling == PC_TILE_AUTO || tiling == PC_TILE_TC || tiling == PC_TILE_SORTED)
         tiling = schedule == PC_BALANCED ? PC_TILE_FLAT : PC_TILE_PER_ROW_TILE;
     if (tiling == PC_TILE_FLAT && schedule != PC_BALANCED)
         return arg_fail("PC_TILE_FLAT needs the balanced schedule (equal windows per row tile)");
@@ -700,10 +775,41 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     // bbox init: minima to the largest ordered code, maxima to the smallest
     CK(cudaMemsetAsync(st, 0xff, offsetof(PrepStats, mx), s));
     CK(cudaMemsetAsync((char*)st + offsetof(PrepStats, mx), 0, sizeof(PrepStats) - offsetof(PrepStats, mx), s));
+    // whole-range fp32 sums over the balanced schedule run on spatially sorted points
+    // (PC_TILE_AUTO on the whole range, or PC_TILE_SORTED for row ranges of the sorted
+    // order; PC_TILE_FLAT keeps the input order, the plain kernel)
+    const bool whole_range = nranges == 1 && bounds[0] == 0 && bounds[1] == n;
+    const bool sorted = PC_SORTED_SUM && direct && !comp && schedule == PC_BALANCED && n >= kSortedMinN &&
+                        ((auto_tiling && whole_range) || sorted_req);
+    const float4* blk_box = nullptr;
+    const int nblk = (int)((n + 31) / 32);
     if (n > 0) {
         const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)num_sms() * 8);
         prep_bbox_kernel<<<blocks, 256, 0, s>>>(xyz, dtype, n, st);
         CK_LAUNCH("prep_bbox_kernel");
+        if (sorted) {
+            const size_t kb = align_up((size_t)n * 4, 256);
+            unsigned* k0 = (unsigned*)(ws + lay.srt);
+            unsigned* k1 = (unsigned*)(ws + lay.srt + kb);
+            unsigned* v0 = (unsigned*)(ws + lay.srt + 2 * kb);
+            unsigned* v1 = (unsigned*)(ws + lay.srt + 3 * kb);
+            float* xs = (float*)(ws + lay.srt + 4 * kb);
+            float4* box = (float4*)(ws + lay.srt + 4 * kb + align_up((size_t)n * 12, 256));
+            morton_kernel<<<blocks, 256, 0, s>>>((const float*)xyz, n, st, k0, v0);
+            CK_LAUNCH("morton_kernel");
+            cub::DoubleBuffer<unsigned> dk(k0, k1), dv(v0, v1);
+            size_t tb = 0;
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)n, 0, 30, s));
+            if (tb > kSortTempBytes((size_t)n)) return arg_fail("radix-sort scratch exceeds its reservation");
+            CK(cub::DeviceRadixSort::SortPairs(ws + lay.srt_temp, tb, dk, dv, (int)n, 0, 30, s));
+            g_launches += 4;  // the radix sort's passes
+            gather_sorted_kernel<<<blocks, 256, 0, s>>>((const float*)xyz, dv.Current(), n, xs);
+            CK_LAUNCH("gather_sorted_kernel");
+            blk_box_kernel<<<(nblk + 255) / 256, 256, 0, s>>>(xs, n, nblk, box);
+            CK_LAUNCH("blk_box_kernel");
+            xyz = xs;  // from here on the call works on the sorted points
+            blk_box = box;
+        }
         if (comp) prep_stage_kernel<true, true><<<blocks, 256, 0, s>>>(xyz, dtype, n, st, pts_even, pts_odd);
         else if (direct) prep_stage_kernel<true, false><<<blocks, 256, 0, s>>>(xyz, dtype, n, st, pts_even, pts_odd);
         else prep_stage_kernel<false, false><<<blocks, 256, 0, s>>>(xyz, dtype, n, st, pts_even, pts_odd);
@@ -714,6 +820,8 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     args.pts_odd = pts_odd;
     args.xyz = xyz;
     args.st = st;
+    args.blk_box = blk_box;
+    args.nblk = nblk;
     args.slots = slots;
     args.work_ctr = &st->work_ctr;
     args.dtype = dtype;
@@ -737,6 +845,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
                               : dispatch_cfg<kSmall.warps, kSmall.r, kSmall.w, false>(args, flat, cap, &nslots, s);
             else
                 rc = comp     ? dispatch_cfg<kBigComp.warps, kBigComp.r, kBigComp.w, true, true>(args, flat, cap, &nslots, s)
+                     : sorted ? dispatch_cfg<kBig.warps, kBig.r, kBig.w, true, false, true>(args, flat, cap, &nslots, s)
                      : direct ? dispatch_cfg<kBig.warps, kBig.r, kBig.w, true>(args, flat, cap, &nslots, s)
                               : dispatch_cfg<kBigGram.warps, kBigGram.r, kBigGram.w, false>(args, flat, cap, &nslots, s);
             if (rc) return rc;

@@ -29,6 +29,16 @@
 // static split left a ~30% occupancy tail in ncu).  PER_ROW_TILE: warp g
 // walks tile g.
 
+__device__ __forceinline__ float warp_min_f(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_max_f(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
 __device__ __forceinline__ float2 f2_fma(float a, float2 b, float2 c) {  // a*b + c, a broadcast
     return __ffma2_rn(make_float2(a, a), b, c);
 }
@@ -110,7 +120,14 @@ constexpr int pairs_smem_per_warp() {
     return (2 * W + 32 * R) / 2 * (COMP ? 3 : 2) * (int)sizeof(float4);
 }
 
-template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP = false>
+// SORTED (sum kernel, whole-range calls on spatially sorted fp32 points): a chunk whose
+// columns are far from the tile's rows (per-32-point bounding boxes) is
+// evaluated in Gram form against tile-local origins, p = A_i + (B_j - 2 a_i.b_j), with
+// a_i = q_i - o, b_j = q_j - o, A_i = 1 + |a_i|^2, B_j = |b_j|^2: 4 packed ops per two
+// pairs instead of 6.  Taken only where the bound on the form's rounding error,
+// 5u (|a|max + |b|max)^2, is below 2e-6 (1 + dmin^2) -- every such term within 2e-6
+// relative, 5x inside the 1e-5 tolerance -- and dmin > 2, so the chunk holds no contact.
+template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP = false, bool SORTED = false>
 __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsArgs a) {
     constexpr int T = 32 * R;
     constexpr int PS = COMP ? 3 : 2;  // float4 per column pair
@@ -234,6 +251,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     };
 
     float rx[R], ry[R], rz[R], rc[R];
+    float tmin[3] = {0.f, 0.f, 0.f}, tmax[3] = {0.f, 0.f, 0.f};  // SORTED: the tile's bounding box
     float rxl[R], ryl[R], rzl[R];  // COMP: low parts of the row coordinates
     int cur_tile = -1;
     unsigned valid_rows = 0;
@@ -332,6 +350,22 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 rc[r] = ok ? (force ? -INFINITY : -v.w - half_tb) : INFINITY;
                 valid_rows |= (ok ? 1u : 0u) << r;
             }
+            if (SORTED) {
+                float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if ((valid_rows >> r) & 1u) {
+                        mn[0] = fminf(mn[0], rx[r]); mx[0] = fmaxf(mx[0], rx[r]);
+                        mn[1] = fminf(mn[1], ry[r]); mx[1] = fmaxf(mx[1], ry[r]);
+                        mn[2] = fminf(mn[2], rz[r]); mx[2] = fmaxf(mx[2], rz[r]);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    tmin[k] = warp_min_f(mn[k]);
+                    tmax[k] = warp_max_f(mx[k]);
+                }
+            }
             __syncwarp();  // the row buffer may be restaged below
         }
 
@@ -406,7 +440,88 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             float2 acc[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] = make_float2(0.f, 0.f);
-            if (COMP && dense) {
+            bool gram = false, no_contact = false;
+            float o[3] = {0.f, 0.f, 0.f};
+            if (SORTED && dense) {
+                // the chunk's bounding box from the per-32-point boxes it covers; columns are
+                // j0 .. j0+W-1 mod n: one run of blocks, or two when the window wraps
+                const int jw = j0 >= n ? j0 - n : j0;
+                const int jend = jw + W - 1;  // last column, before wrapping
+                const int nb1 = (min(jend, n - 1) >> 5) - (jw >> 5) + 1;
+                const int nb2 = jend >= n ? ((jend - n) >> 5) + 1 : 0;
+                float cmn[3] = {INFINITY, INFINITY, INFINITY}, cmx[3] = {-INFINITY, -INFINITY, -INFINITY};
+                if (lane < nb1 + nb2) {
+                    const int b = lane < nb1 ? (jw >> 5) + lane : lane - nb1;
+                    const float4 lo4 = a.blk_box[2 * b], hi4 = a.blk_box[2 * b + 1];
+                    cmn[0] = lo4.x; cmn[1] = lo4.y; cmn[2] = lo4.z;
+                    cmx[0] = hi4.x; cmx[1] = hi4.y; cmx[2] = hi4.z;
+                }
+                float gap2 = 0.f, rt2 = 0.f, bm2 = 0.f;
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const float cl = warp_min_f(cmn[k]), ch = warp_max_f(cmx[k]);
+                    o[k] = 0.5f * (tmin[k] + tmax[k]);
+                    const float g = fmaxf(0.f, fmaxf(cl - tmax[k], tmin[k] - ch));
+                    gap2 += g * g;
+                    const float ht = 0.5f * (tmax[k] - tmin[k]);
+                    rt2 += ht * ht;
+                    const float bb = fmaxf(fabsf(cl - o[k]), fabsf(ch - o[k]));
+                    bm2 += bb * bb;
+                }
+                // 5u (|a| + |b|)^2 <= 2e-6 (1 + dmin^2), u = 2^-24: five roundings of terms of at
+                // most (|a| + |b|)^2 against p >= 1 + dmin^2
+                const float ab = sqrtf(rt2) + sqrtf(bm2);
+                gram = gap2 > 4.5f && 2.98023223876953125e-07f * ab * ab <= 2e-6f * (1.f + gap2);
+                // boxes more than 1.5 apart: no contact, so no rescan however large the chunk's
+                // sums (on sorted points the chunks next to a tile have many near terms)
+                no_contact = gap2 > 2.25f;
+            }
+            if (SORTED && gram) {
+                // columns to tile-local form in place: (bx, by, bz, B = |b|^2) per point
+                float4* spw = const_cast<float4*>(sp);
+#pragma unroll
+                for (int q = 0; q < W / 64; ++q) {
+                    const int e = q * 32 + lane;  // pair entry: points 2e, 2e+1 of the chunk
+                    const float4 A = spw[2 * e], B = spw[2 * e + 1];
+                    const float bx0 = A.x - o[0], bx1 = A.y - o[0], by0 = A.z - o[1], by1 = A.w - o[1];
+                    const float bz0 = B.x - o[2], bz1 = B.y - o[2];
+                    spw[2 * e] = make_float4(bx0, bx1, by0, by1);
+                    spw[2 * e + 1] = make_float4(bz0, bz1, fmaf(bz0, bz0, fmaf(by0, by0, bx0 * bx0)),
+                                                 fmaf(bz1, bz1, fmaf(by1, by1, bx1 * bx1)));
+                }
+                __syncwarp();
+                // rows in Gram form in the row registers themselves (restored from the row
+                // buffer after the chunk): -2 a_i and A_i = 1 + |a_i|^2
+                float ga[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const float ax = rx[r] - o[0], ay = ry[r] - o[1], az = rz[r] - o[2];
+                    rx[r] = -2.f * ax;
+                    ry[r] = -2.f * ay;
+                    rz[r] = -2.f * az;
+                    ga[r] = 1.f + fmaf(az, az, fmaf(ay, ay, ax * ax));
+                }
+                float* gx = rx;
+                float* gy = ry;
+                float* gz = rz;
+#pragma unroll kDirectUnroll
+                for (int k = 0; k < W; k += 4) {
+                    const float4 A0 = sp[k], B0 = sp[k + 1], A1 = sp[k + 2], B1 = sp[k + 3];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        float2 t0 = f2_fma(gx[r], make_float2(A0.x, A0.y), make_float2(B0.z, B0.w));
+                        t0 = f2_fma(gy[r], make_float2(A0.z, A0.w), t0);
+                        t0 = f2_fma(gz[r], make_float2(B0.x, B0.y), t0);
+                        float2 t1 = f2_fma(gx[r], make_float2(A1.x, A1.y), make_float2(B1.z, B1.w));
+                        t1 = f2_fma(gy[r], make_float2(A1.z, A1.w), t1);
+                        t1 = f2_fma(gz[r], make_float2(B1.x, B1.y), t1);
+                        const float2 p0 = __fadd2_rn(t0, make_float2(ga[r], ga[r]));
+                        const float2 p1 = __fadd2_rn(t1, make_float2(ga[r], ga[r]));
+                        const float2 pr = __fmul2_rn(p0, p1), sm = __fadd2_rn(p0, p1);
+                        acc[r] = __ffma2_rn(sm, make_float2(rcp_approx(pr.x), rcp_approx(pr.y)), acc[r]);
+                    }
+                }
+            } else if (COMP && dense) {
                 // ---- compensated direct formula: dr = (hi_i - hi_j) + (lo_i - lo_j) keeps the
                 // separation to ~2u relative however far the points sit from the centre
                 const float2 one = make_float2(1.0f, 1.0f);
@@ -476,6 +591,18 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 const float cs = acc[r].x + acc[r].y;
                 sum += (double)cs;
                 fl |= (cs > sum_flag ? 1u : 0u) << r;  // conservative: a contact's term alone exceeds it
+            }
+            if (SORTED && no_contact) fl = 0;  // also covers the Gram chunks, whose columns were rewritten
+            if (SORTED && gram && staged_tile == tile) {
+                // back to the raw rows for the tile's next chunks (a new tile reloads them anyway)
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const float4 v = col_hi<COMP>(rowbuf, r * 32 + lane);
+                    const bool ok = (valid_rows >> r) & 1u;
+                    rx[r] = ok ? v.x : 0.f;
+                    ry[r] = ok ? v.y : 0.f;
+                    rz[r] = ok ? v.z : 0.f;
+                }
             }
         }
 

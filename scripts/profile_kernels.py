@@ -1,6 +1,6 @@
 """Run each hot kernel a few times on its benchmark size, for ncu captures.
 
-    python scripts/profile_kernels.py [direct|gram|tc|tc4|gram_std|cfg2|cfg4|lattice|all] [--reps R]
+    python scripts/profile_kernels.py [direct|sorted|gram|tc|tc4|gram_std|cfg2|cfg4|lattice|all] [--reps R]
 
 Prints one timing line per case (CUDA events around the main kernel via
 pc_kernel_timing); the numbers under ncu are not bench values.
@@ -79,6 +79,8 @@ def main():
     w = a.what
     if w in ("direct", "all"):
         pairs_case("direct_flat_2^20", 2**20, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, _lib.PC_TILE_FLAT, a.reps)
+    if w in ("sorted", "all"):  # the headline's path: Morton-sorted points, tile-local Gram chunks
+        pairs_case("direct_sorted_2^20", 2**20, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, _lib.PC_TILE_SORTED, a.reps)
     if w in ("gram", "all"):
         pairs_case("gram_flat_2^20", 2**20, _lib.PC_COLLISION, _lib.PC_BALANCED, _lib.PC_TILE_FLAT, a.reps)
     if w in ("tc", "all"):
