@@ -69,6 +69,19 @@ def check_spi(rng, stats):
                       f"[{b.start},{b.stop}): got {got} want {want}", flush=True)
 
 
+def check_sorted(rng, stats):
+    # the headline's path: whole-range fp32 sums on Morton-sorted points (n >= 2^15)
+    n = int(rng.integers(32768, 70000))
+    pts, kind = random_points(rng, n)
+    pts = pts.astype(np.float32)
+    (r,) = _lib.pairs_host(pts, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, n])
+    want_c, want_s, _ = c_oracle.rows(pts, 0, n, "balanced")
+    ok = r.count == want_c and math.isclose(r.sum, want_s, rel_tol=1e-6)
+    stats[("sorted-sum", ok)] += 1
+    if not ok:
+        print(f"MISMATCH sorted-sum n={n} {kind}: got {r.count} {r.sum!r} want {want_c} {want_s!r}", flush=True)
+
+
 def check_tc(rng, stats):
     # the tensor-core count filter forced at any size (PC_TILE_TC), every distribution,
     # float and integer predicates
@@ -137,6 +150,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--minutes", type=float, default=15.0)
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--sorted", action="store_true", help="also whole-range fp32 sums on the sorted path (slower)")
     args = p.parse_args()
     rng = np.random.default_rng(args.seed)
     stats: Counter = Counter()
@@ -147,6 +161,8 @@ def main():
         check_int(rng, stats)
         check_lattice(rng, stats)
         check_tc(rng, stats)
+        if args.sorted:
+            check_sorted(rng, stats)
         rounds += 1
     fams = sorted({k for k, _ in stats})
     bad = 0
