@@ -29,6 +29,11 @@
 // static split left a ~30% occupancy tail in ncu).  PER_ROW_TILE: warp g
 // walks tile g.
 
+__device__ __forceinline__ float min3f(float a, float b, float c) {
+    float d;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
 __device__ __forceinline__ float warp_min_f(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -441,6 +446,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] = make_float2(0.f, 0.f);
             bool gram = false, no_contact = false;
+            unsigned near_fl = 0;  // SORTED near chunks: rows with some p < thr2
             float o[3] = {0.f, 0.f, 0.f};
             if (SORTED && dense) {
                 // the chunk's bounding box from the per-32-point boxes it covers; columns are
@@ -543,6 +549,34 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                         acc[r] = __ffma2_rn(sm, make_float2(rcp_approx(pr.x), rcp_approx(pr.y)), acc[r]);
                     }
                 }
+            } else if (SORTED && dense && !no_contact) {
+                // ---- a chunk next to the tile on sorted points: many moderately near terms, so
+                // the chunk-sum test would flag nearly every row; track each row's smallest p
+                // instead (two FMNMX3 per four pairs) and flag the rows with a candidate
+                const float2 one = make_float2(1.0f, 1.0f);
+                float pm[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) pm[r] = INFINITY;
+#pragma unroll 1
+                for (int k = 0; k < W; k += 4) {
+                    const float4 A0 = sp[k], B0 = sp[k + 1], A1 = sp[k + 2], B1 = sp[k + 3];
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        float2 dx = f2_rsub(rx[r], make_float2(A0.x, A0.y));
+                        float2 dy = f2_rsub(ry[r], make_float2(A0.z, A0.w));
+                        float2 dz = f2_rsub(rz[r], make_float2(B0.x, B0.y));
+                        const float2 p0 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __ffma2_rn(dx, dx, one)));
+                        dx = f2_rsub(rx[r], make_float2(A1.x, A1.y));
+                        dy = f2_rsub(ry[r], make_float2(A1.z, A1.w));
+                        dz = f2_rsub(rz[r], make_float2(B1.x, B1.y));
+                        const float2 p1 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __ffma2_rn(dx, dx, one)));
+                        pm[r] = fminf(min3f(pm[r], p0.x, p0.y), fminf(p1.x, p1.y));
+                        const float2 pr = __fmul2_rn(p0, p1), sm = __fadd2_rn(p0, p1);
+                        acc[r] = __ffma2_rn(sm, make_float2(rcp_approx(pr.x), rcp_approx(pr.y)), acc[r]);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) near_fl |= (pm[r] < thr2 ? 1u : 0u) << r;
             } else if (dense) {
                 // ---- direct formula, packed: p = 1 + |dr|^2 for two columns per FADD2/FFMA2;
                 // two column pairs share one FMUL2/FADD2/FFMA2 for 1/pa + 1/pc = (pa+pc)/(pa*pc)
@@ -593,6 +627,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 fl |= (cs > sum_flag ? 1u : 0u) << r;  // conservative: a contact's term alone exceeds it
             }
             if (SORTED && no_contact) fl = 0;  // also covers the Gram chunks, whose columns were rewritten
+            if (SORTED && dense && !no_contact) fl = near_fl;  // exact candidates, not chunk sums
             if (SORTED && gram && staged_tile == tile) {
                 // back to the raw rows for the tile's next chunks (a new tile reloads them anyway)
 #pragma unroll
