@@ -132,6 +132,8 @@ constexpr int pairs_smem_per_warp() {
 // pairs instead of 6.  Taken only where the bound on the form's rounding error,
 // 5u (|a|max + |b|max)^2, is below 2e-6 (1 + dmin^2) -- every such term within 2e-6
 // relative, 5x inside the 1e-5 tolerance -- and dmin > 2, so the chunk holds no contact.
+// The boxes also decide the contact test: more than 1.5 apart, none; closer, each row's
+// smallest p flags its candidates (the chunk-sum test would flag every row there).
 template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP = false, bool SORTED = false>
 __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsArgs a) {
     constexpr int T = 32 * R;
