@@ -13,7 +13,9 @@
 //                     all-pairs host driver, per-device arena, the C ABI
 //   pairs_kernel.cuh  the all-pairs kernel: warp-private row tiles, packed
 //                     FP32 Gram filter (count) / direct formula (sum), exact
-//                     re-check slow path, FLAT uniform tiles with dynamic claims
+//                     re-check slow path, FLAT uniform tiles with dynamic claims;
+//                     SORTED: the sum on Morton-sorted points (sort kernels in
+//                     this file) with tile-local Gram chunks
 //   pairs_tc.cuh      the count filter on the tensor cores: tcgen05.mma tf32
 //                     (3xTF32) into TMEM, warp-specialised loader / MMA /
 //                     drain warps, candidate queues + exact pass
