@@ -74,3 +74,32 @@ def test_sorted_argument_errors():
                         tiling=_lib.PC_TILE_SORTED)
     with pytest.raises(Exception, match="PC_TILE_SORTED"):
         _lib.pairs_host(pts, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, 40_000], tiling=_lib.PC_TILE_SORTED)
+
+
+def test_sorted_path_non_finite_and_degenerate_inputs():
+    # a NaN or inf anywhere: the C ABI reports a domain error on the sorted path too; the
+    # drop-in raises what the reference raises for NaN (AccumulationError naming the first
+    # pair for the float sum, InteractionDomainError for collision_indicator) and refuses
+    # an isolated inf (whose terms the reference would add as zeros) with
+    # InteractionDomainError.  Points on a line (a flat bounding box: zero Morton scale on
+    # two axes) stay exact.
+    n = 40_000
+    pts = gen.random_spheres(n, 30.0, 2).astype(np.float32)
+    for bad in (np.nan, np.inf):
+        p = pts.copy()
+        p[31_337, 1] = bad
+        (r,) = _lib.pairs_host(p, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, n])
+        assert r.error == _lib.PC_ERR_DOMAIN
+        if np.isnan(bad):
+            with pytest.raises(se.AccumulationError, match="31337"):
+                se.spi_balanced(p, se.inverse_square)
+        else:
+            with pytest.raises(se.InteractionDomainError):
+                se.spi_balanced(p, se.inverse_square)
+        with pytest.raises(se.InteractionDomainError):
+            se.spi_balanced(p, se.collision_indicator)
+    line = np.zeros((n, 3), np.float32)
+    line[:, 0] = np.arange(n, dtype=np.float32) * 0.75
+    want_c, want_s, _ = c_oracle.rows(line, 0, n, "balanced")
+    (r,) = _lib.pairs_host(line, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, n])
+    assert r.count == want_c and abs(r.sum - want_s) <= 1e-6 * want_s
