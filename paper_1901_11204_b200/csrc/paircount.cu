@@ -804,7 +804,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
             CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int)n, 0, 30, s));
             if (tb > kSortTempBytes((size_t)n)) return arg_fail("radix-sort scratch exceeds its reservation");
             CK(cub::DeviceRadixSort::SortPairs(ws + lay.srt_temp, tb, dk, dv, (int)n, 0, 30, s));
-            g_launches += 4;  // the radix sort's passes
+            // (the radix sort's kernels are CUB's, not counted in g_launches)
             gather_sorted_kernel<<<blocks, 256, 0, s>>>((const float*)xyz, dv.Current(), n, xs);
             CK_LAUNCH("gather_sorted_kernel");
             blk_box_kernel<<<(nblk + 255) / 256, 256, 0, s>>>(xs, n, nblk, box);
