@@ -351,6 +351,35 @@ def secondary(torch, lib, stream):
                     "of int64 beads to int32 in pinned chunks streamed to the device (0.8 GB H2D) + the device step"})
     del sp5, pts64
 
+    # ---- the headline workload split 2/4/8 ways the way the multi-GPU step splits it (slabs of
+    # the sorted order, PC_TILE_SORTED): each slab timed alone on this GPU, giving the balance
+    # of the split and a projected per-GPU step (the exchange is one 16-byte all-reduce)
+    from paper_1901_11204_b200.distributed import row_slabs
+
+    d3s = torch.from_numpy(workload_input()).cuda()
+    ws3s = torch.empty(_lib.workspace_bytes(n3), dtype=torch.uint8, device="cuda")
+    res3s = torch.zeros(8, dtype=torch.int64, device="cuda")
+
+    def run_sorted_slab(lo, hi):
+        _lib.kernel_timing(True)
+        _lib.pairs_async(d3s.data_ptr(), _lib.PC_F32, n3, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED,
+                         np.array([lo, hi]), ws3s.data_ptr(), ws3s.numel(), res3s.data_ptr(), stream.cuda_stream,
+                         _lib.PC_TILE_SORTED)
+        ms_k, _ = _lib.kernel_timing_read()
+        _lib.kernel_timing(False)
+        return ms_k, int(res3s[0].item())
+
+    run_sorted_slab(0, n3)
+    full3_ms, full3_count = run_sorted_slab(0, n3)
+    split3 = {"kernel_ms_1gpu": full3_ms}
+    for g in (2, 4, 8):
+        times, counts = zip(*(run_sorted_slab(lo, hi) for lo, hi in row_slabs(n3, g, "balanced")))
+        split3[f"split{g}"] = {"slab_ms_max": max(times), "slab_ms_min": min(times),
+                               "projected_speedup": full3_ms / max(times),
+                               "partials_sum_equals_total": sum(counts) == full3_count}
+    out["cfg3_headline_sorted_slabs"] = split3
+    del d3s, ws3s
+
     # ---- config 4: 2^22 clustered points, count; the per-rank slabs of a 2/4/8-GPU split timed
     # one after another on this GPU (ranks never wait on each other: the only exchange is the final
     # all-reduce), giving the load balance of the split and a projected multi-GPU step.
