@@ -471,7 +471,10 @@ struct KernelCfg {
 #ifndef PC_BIG_R
 #define PC_BIG_R 8
 #endif
-constexpr KernelCfg kBig{4, PC_BIG_R, 256};  // direct (sum) kernel: warp tile 32*R rows (256 by default)
+#ifndef PC_BIG_W
+#define PC_BIG_W 256
+#endif
+constexpr KernelCfg kBig{4, PC_BIG_R, PC_BIG_W};  // direct (sum) kernel: warp tile 32*R rows (256 by default)
 #ifndef PC_SORTED_SUM
 #define PC_SORTED_SUM 1  // whole-range fp32 balanced sums: spatial sort + tile-local Gram chunks
 #endif
