@@ -34,7 +34,11 @@ extern "C" {
 #define PC_OK 0
 #define PC_ERR_CUDA (-1)
 #define PC_ERR_ARG 1       /* bad argument (ValueError / TypeError)                       */
-#define PC_ERR_DOMAIN 2    /* non-finite coordinate -> InteractionDomainError (spi_engine.py:32-33,70-71) */
+#define PC_ERR_DOMAIN 2    /* counts: a non-finite coordinate -> InteractionDomainError (spi_engine.py:32-33,
+                              70-71); sums: a NaN term (inf - inf or a NaN coordinate in an owned pair)
+                              -> AccumulationError (spi_engine.py:93-95).  A sum with non-finite
+                              coordinates but no NaN term is evaluated in float64 exactly as the
+                              reference does (1/(1+inf) = 0) and returns PC_OK.                   */
 #define PC_ERR_RANGE 3     /* bead outside [-a,a]^3 -> CoordinateRangeError (lattice_counter.py:31-32,98-105);
                               detail = index of the first offending bead                   */
 #define PC_ERR_OVERFLOW 4  /* occupancy >= 2^32-1 -> OccupancyOverflowError (lattice_counter.py:132-135) */
@@ -81,6 +85,26 @@ typedef struct {
     int32_t error;         /* PC_OK or PC_ERR_DOMAIN                                               */
     int32_t reserved;
 } pc_pairs_result;
+
+/* What the kernels of one pc_pairs* call did (pc_pairs_last_profile /
+ * pc_pairs_profile_read): chunks per inner loop (a chunk = pairs_per_chunk
+ * pair cells, T rows x W columns, some masked on edge chunks), rows the slow
+ * path re-tested, exact re-checks, work claims.  Evidence for bench.py's
+ * executed-instruction roofline; integers, identical on every run. */
+typedef struct {
+    int64_t chunks_gram;     /* sum on sorted points, tile-local Gram form            */
+    int64_t chunks_main;     /* unmasked main loop (direct sum / Gram count filter)    */
+    int64_t chunks_near;     /* sorted sum, direct formula + per-row contact minimum   */
+    int64_t chunks_far;      /* sorted sum, direct formula, no contact test needed     */
+    int64_t chunks_edge;     /* masked per-pair chunks                                 */
+    int64_t rows_rescanned;  /* flagged (row, chunk) re-tests by the slow path         */
+    int64_t exact_checks;    /* pairs re-evaluated by the exact predicate              */
+    int64_t claims;          /* FLAT work claims (float64 partial slots)               */
+    int64_t pairs;           /* pairs owned by the call's rows                         */
+    int64_t pairs_per_chunk; /* T x W of the kernel (0: tensor-core or no kernel)      */
+    int32_t kernel;          /* 1 Gram count, 2 direct sum, 3 sorted sum, 4 compensated sum, 5 tensor-core count */
+    int32_t f64_taken;       /* 1: the float64 kernel evaluated the sum (non-finite / huge / wide input) */
+} pc_pairs_profile;
 
 typedef struct {
     int64_t count;         /* CountReport.count (collisions) or contacts                          */
@@ -134,6 +158,25 @@ int pc_pairs_async(const void* xyz, int32_t dtype, int64_t n, int32_t interactio
 int pc_pairs_host(const void* xyz_host, int32_t dtype, int64_t n, int32_t interaction,
                   int32_t schedule, int32_t tiling, int32_t nranges, const int64_t* bounds,
                   pc_pairs_result* results);
+
+/* One part of a row range for multi-GPU work: the kernel's row tiles of
+ * [lo, hi) dealt round-robin over nparts calls (tiles part, part + nparts,
+ * ...), so every part holds the same mix of near and far work however the
+ * points are ordered (with PC_TILE_SORTED, spatially sorted).  The nparts
+ * results add up to the [lo, hi) result (counts exactly).  A part is not a
+ * reference worker's partial: spi_parallel partials use contiguous ranges. */
+int pc_pairs_part_async(const void* xyz, int32_t dtype, int64_t n, int32_t interaction, int32_t schedule,
+                        int32_t tiling, int64_t lo, int64_t hi, int32_t part, int32_t nparts, void* workspace,
+                        size_t workspace_bytes, pc_pairs_result* result_device, void* stream);
+int pc_pairs_part_host(const void* xyz_host, int32_t dtype, int64_t n, int32_t interaction, int32_t schedule,
+                       int32_t tiling, int64_t lo, int64_t hi, int32_t part, int32_t nparts,
+                       pc_pairs_result* result);
+
+/* the profile of the last pc_pairs_host / pc_pairs_part_host call on this thread */
+int pc_pairs_last_profile(pc_pairs_profile* out);
+/* the profile of the last pc_pairs / pc_pairs_async / pc_pairs_part_async call on
+ * this workspace (n as passed to it); synchronises `stream` */
+int pc_pairs_profile_read(const void* workspace, int64_t n, pc_pairs_profile* out, void* stream);
 
 /* Single-process multi-GPU all-pairs (SURVEY.md §8(b) pc_multi_pairs): device
  * d computes the rows [bounds[d], bounds[d+1]) of the host input (bounds[0] = 0,

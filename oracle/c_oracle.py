@@ -19,6 +19,7 @@ def _lib():
     lib.orc_rows_f64.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int64,
                                  ctypes.c_int64, _i64p, _f64p, _i64p]
     lib.orc_int_pairs.argtypes = [ctypes.c_void_p, ctypes.c_int64, _i64p, _i64p]
+    lib.orc_total_f64.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _i64p, _f64p]
     return lib
 
 
@@ -40,3 +41,16 @@ def int_pairs(beads):
     col, con = ctypes.c_int64(), ctypes.c_int64()
     _lib().orc_int_pairs(arr.ctypes.data, len(arr), ctypes.byref(col), ctypes.byref(con))
     return col.value, con.value
+
+
+def total(obj, lo: int = 0, hi: int | None = None, lib=None):
+    """(contact count, inverse-square sum) over every pair i < j with i in
+    [lo, hi) (standard-schedule rows; [0, n) is the whole triangle).  ``lib``
+    may be another build of oracle.c (the golden script's -march=native one)."""
+    arr = np.ascontiguousarray(np.asarray(obj, dtype=np.float64).reshape(-1, 3))
+    hi = len(arr) if hi is None else hi
+    c, s = ctypes.c_int64(), ctypes.c_double()
+    L = lib or _lib()
+    if L.orc_total_f64(arr.ctypes.data, len(arr), lo, hi, ctypes.byref(c), ctypes.byref(s)):
+        raise ValueError("bad row range")
+    return c.value, s.value

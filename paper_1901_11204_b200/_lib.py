@@ -40,6 +40,7 @@ EXPORTED = (
     "pc_last_error", "pc_version", "pc_device_count", "pc_set_device", "pc_device_alloc",
     "pc_device_free", "pc_memcpy_h2d", "pc_memcpy_d2h", "pc_stream_sync",
     "pc_pairs_workspace_bytes", "pc_pairs", "pc_pairs_async", "pc_pairs_host", "pc_pairs_multi", "pc_pairs_batch",
+    "pc_pairs_part_async", "pc_pairs_part_host", "pc_pairs_last_profile", "pc_pairs_profile_read",
     "pc_last_launch_count", "pc_kernel_timing", "pc_kernel_timing_read", "pc_lattice_grid_cells", "pc_lattice_key_bytes",
     "pc_lattice_collisions", "pc_lattice_contacts", "pc_lattice_reset_keys", "pc_lattice_clear",
     "pc_lattice_collisions_batch", "pc_lattice_collisions_vectors", "pc_lattice_collisions_multi",
@@ -58,6 +59,17 @@ class PaircountError(RuntimeError):
 class PairsResult(ctypes.Structure):
     _fields_ = [("count", ctypes.c_int64), ("sum", ctypes.c_double), ("pairs", ctypes.c_int64),
                 ("exact_checks", ctypes.c_int64), ("error", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class PairsProfile(ctypes.Structure):
+    """pc_pairs_profile: what the kernels of one call did (include/paircount.h)."""
+    _fields_ = [("chunks_gram", ctypes.c_int64), ("chunks_main", ctypes.c_int64), ("chunks_near", ctypes.c_int64),
+                ("chunks_far", ctypes.c_int64), ("chunks_edge", ctypes.c_int64), ("rows_rescanned", ctypes.c_int64),
+                ("exact_checks", ctypes.c_int64), ("claims", ctypes.c_int64), ("pairs", ctypes.c_int64),
+                ("pairs_per_chunk", ctypes.c_int64), ("kernel", ctypes.c_int32), ("f64_taken", ctypes.c_int32)]
+
+    def as_dict(self) -> dict:
+        return {name: int(getattr(self, name)) for name, _ in self._fields_}
 
 
 class LatticeResult(ctypes.Structure):
@@ -82,6 +94,11 @@ _SIGS = {
     "pc_pairs_async": ([_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _sz, _vp, _vp], ctypes.c_int),
     "pc_pairs_host": ([_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
     "pc_pairs_multi": ([_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "pc_pairs_part_async": ([_vp, _i32, _i64, _i32, _i32, _i32, _i64, _i64, _i32, _i32, _vp, _sz, _vp, _vp],
+                            ctypes.c_int),
+    "pc_pairs_part_host": ([_vp, _i32, _i64, _i32, _i32, _i32, _i64, _i64, _i32, _i32, _vp], ctypes.c_int),
+    "pc_pairs_last_profile": ([_vp], ctypes.c_int),
+    "pc_pairs_profile_read": ([_vp, _i64, _vp, _vp], ctypes.c_int),
     "pc_pairs_batch": ([_vp, _vp, _i32, _i32, _i32, _vp, _vp], ctypes.c_int),
     "pc_last_launch_count": ([], _i32),
     "pc_kernel_timing": ([_i32], ctypes.c_int),
@@ -117,7 +134,9 @@ def load(require_device: bool = True):
                     "(there is no CPU fallback)")
             lib = ctypes.CDLL(str(LIB_PATH))
             for name, (args, res) in _SIGS.items():
-                fn = getattr(lib, name)
+                fn = getattr(lib, name, None)
+                if fn is None:  # an older build under PAIRCOUNT_LIB (A/B timing); test_abi checks the shipped one
+                    continue
                 fn.argtypes = args
                 fn.restype = res
             _handle = lib
@@ -149,6 +168,14 @@ def check(rc: int) -> None:
         raise ValueError(last_error())
 
 
+def device_count() -> int:
+    """CUDA devices visible to libpaircount (0 when none)."""
+    cnt = ctypes.c_int32(0)
+    if load(require_device=False).pc_device_count(ctypes.byref(cnt)) != PC_OK:
+        return 0
+    return int(cnt.value)
+
+
 def launches() -> int:
     """Kernel launches issued by the last pairs/lattice call on this thread."""
     return int(load(require_device=False).pc_last_launch_count())
@@ -168,6 +195,39 @@ def pairs_host(xyz: np.ndarray, interaction: int, schedule: int, bounds, tiling:
                            b.ctypes.data, ctypes.addressof(res))
     check(rc)
     return list(res)
+
+
+def pairs_part_host(xyz: np.ndarray, interaction: int, schedule: int, lo: int, hi: int, part: int, nparts: int,
+                    tiling: int = PC_TILE_AUTO):
+    """pc_pairs_part_host: row tiles part, part + nparts, ... of [lo, hi); returns one PairsResult."""
+    lib = load()
+    arr = np.ascontiguousarray(xyz)
+    res = PairsResult()
+    check(lib.pc_pairs_part_host(arr.ctypes.data, DTYPE_CODES[arr.dtype], len(arr), interaction, schedule, tiling,
+                                 lo, hi, part, nparts, ctypes.byref(res)))
+    return res
+
+
+def pairs_part_async(xyz_ptr: int, dtype_code: int, n: int, interaction: int, schedule: int, lo: int, hi: int,
+                     part: int, nparts: int, workspace_ptr: int, workspace_bytes: int, results_dev_ptr: int,
+                     stream_ptr: int, tiling: int = PC_TILE_AUTO) -> None:
+    """Device-pointer entry of pc_pairs_part_async: enqueue, no synchronisation."""
+    check(load().pc_pairs_part_async(xyz_ptr, dtype_code, n, interaction, schedule, tiling, lo, hi, part, nparts,
+                                     workspace_ptr, workspace_bytes, results_dev_ptr, stream_ptr))
+
+
+def last_profile() -> PairsProfile:
+    """Profile of the last pc_pairs_host / pc_pairs_part_host call on this thread."""
+    prof = PairsProfile()
+    check(load().pc_pairs_last_profile(ctypes.byref(prof)))
+    return prof
+
+
+def profile_read(workspace_ptr: int, n: int, stream_ptr: int) -> PairsProfile:
+    """Profile of the last device-pointer call on this workspace (synchronises the stream)."""
+    prof = PairsProfile()
+    check(load().pc_pairs_profile_read(workspace_ptr, n, ctypes.byref(prof), stream_ptr))
+    return prof
 
 
 def pairs_multi(xyz: np.ndarray, interaction: int, schedule: int, devices, bounds, tiling: int = PC_TILE_AUTO):

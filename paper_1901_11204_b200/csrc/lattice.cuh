@@ -468,8 +468,10 @@ int lattice_run(const void* xyz_in, int dtype, int on_device, long long n, long 
     // dense regime on a clean grid: shared-memory slab histogram (lattice_slab.cuh)
     // crossover: n scattered atomics at ~21 G/s vs streaming 4 B/cell + ~40 B/bead at HBM rate -> n > cells/67
     // (contacts too: the slab histogram populates the grid, then one stencil pass)
-    const bool slab = clean && sizeof(KT) == 4 && (unsigned long long)n * 64 > cells && n < (1LL << 32) - 1;
-    const int nbuckets = (int)((cells + (1ull << kBucketShift) - 1) >> kBucketShift);
+    // the slab path's bucket tables cover kMaxBuckets << kBucketShift = 2^31 cells
+    const bool slab = clean && sizeof(KT) == 4 && (unsigned long long)n * 64 > cells && n < (1LL << 32) - 1 &&
+                      cells <= ((unsigned long long)kMaxBuckets << kBucketShift);
+    const int nbuckets = slab ? (int)((cells + (1ull << kBucketShift) - 1) >> kBucketShift) : 0;
     const size_t kbytes = align_up((size_t)n * 4 + 64, 256);  // +16 keys: aligned staging windows may overrun
     const size_t abytes = align_up((kMaxBuckets + 1) * 4, 256), cbytes4 = align_up((kMaxCoarse + 1) * 4, 256);
     const size_t extra = slab ? 2 * kbytes + 3 * abytes + 3 * cbytes4 + align_up((size_t)nbuckets * sizeof(LatSlot), 256)

@@ -30,7 +30,7 @@ constexpr int kBucketShift = 17;  // 128K cells per bucket
 constexpr int kSlabShift = 13;    // 8K cells per shared-memory slab (2 x 32 KB buffers)
 constexpr int kSlabCells = 1 << kSlabShift;
 constexpr int kSubSlabs = 1 << (kBucketShift - kSlabShift);  // 16
-constexpr int kMaxBuckets = 16384;                             // grids below 2^32 cells
+constexpr int kMaxBuckets = 16384;                             // grids of up to 2^31 cells
 constexpr int kKeyCap = 16384;    // keys of one bucket staged on chip (2x the uniform mean)
 #ifndef PC_SLAB_BUFS
 #define PC_SLAB_BUFS 3

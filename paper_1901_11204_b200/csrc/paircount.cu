@@ -269,6 +269,17 @@ __device__ __forceinline__ double bbox_span(const PrepStats& st, int dtype) {
 // this span that passes 1e-7 and the sum takes pairs_f64_kernel instead.
 constexpr double kCompMaxSpan = 67108864.0;  // 2^26
 
+// Inverse-square sums the float64 kernel (pairs_f64_kernel) evaluates instead of the fp32
+// kernels, decided on the device from the prep statistics (no host synchronisation):
+//   * a non-finite coordinate: every term is then the reference's own float64 value --
+//     1/(1+inf) = 0 for a pair with an isolated inf, NaN where inf - inf or a NaN enters
+//     (spi_engine.py:84-99: the host layer turns a NaN sum into AccumulationError);
+//   * |coordinate| >= 1e18, where fp32 squares overflow;
+//   * a compensated (non-f32) call whose span defeats the hi + lo staging.
+__device__ __forceinline__ bool f64_takes(const PrepStats& st, int dtype, bool comp) {
+    return st.nonfinite || !(dec_f64_or0(st.maxabs) < 1e18) || (comp && bbox_span(st, dtype) > kCompMaxSpan);
+}
+
 // Staged value of point i: centred fp32 q and w = -|q|^2/2 (Gram), or the
 // raw fp32 coordinates (direct formula).
 template <bool DIRECT>
@@ -349,12 +360,42 @@ __global__ void prep_stage_kernel(const void* __restrict__ xyz, int dtype, long 
 // ------------------------------------------------------------------------
 // the all-pairs kernel
 // ------------------------------------------------------------------------
+// One record per CTA.  path[] counts the chunks each inner loop evaluated (kPath*), the
+// evidence behind the bench's executed-instruction roofline; rescans counts the rows the
+// slow path re-tested.  All integer: the order CTAs finish in cannot change them.
+constexpr int kPathGram = 0;   // sum on sorted points: tile-local Gram form
+constexpr int kPathMain = 1;   // unmasked main loop: direct formula (sum) / Gram filter (count)
+constexpr int kPathNear = 2;   // sum on sorted points: direct formula + per-row minimum (contact test)
+constexpr int kPathFar = 3;    // sum on sorted points: direct formula, boxes too far apart for a contact
+constexpr int kPathEdge = 4;   // masked per-pair chunk (leading / trailing / ragged)
+constexpr int kNumPaths = 5;
 struct Slot {
     unsigned long long count;
     unsigned long long checks;
     double sum;
-    unsigned long long pad;
+    unsigned path[kNumPaths];
+    unsigned rescans;
+    unsigned pad[4];
 };
+static_assert(sizeof(Slot) == 64, "Slot is one 64-byte record");
+
+// FLAT work claims (guided self-scheduling): claim c of stage k covers columns
+// [b0[k] + (c - c0[k]) * s[k], + s[k]) of the flat (row tile, window column) space.  Stage k
+// hands out P claims (P = the grid's warps) of half the remaining work split P ways, the last
+// stage single chunks, so the tail is one chunk and a claim's index is a fixed function of
+// its columns: the float64 sum of claim c goes to claim_sums[c] and the finalize adds those
+// in index order -- bit-reproducible sums whichever warp ran which claim.
+#ifndef PC_GUIDED
+#define PC_GUIDED 1
+#endif
+#ifndef PC_CLAIM_MAX
+#define PC_CLAIM_MAX 16
+#endif
+constexpr int kMaxStages = 48;
+#ifndef PC_CLAIMS_CAP
+#define PC_CLAIMS_CAP (1 << 20)
+#endif
+constexpr long long kClaimsCap = PC_CLAIMS_CAP;
 
 struct PairsArgs {
     const float4* pts_even;  // pair arrays, see prep_stage_kernel
@@ -369,9 +410,13 @@ struct PairsArgs {
     int n_tiles;        // row tiles in [lo, hi)
     long long L;        // FLAT: window length shared by every row tile
     long long total;    // FLAT: n_tiles * L
-    long long super_cols;  // FLAT: columns per claimed super-chunk (multiple of W)
     const float4* blk_box;  // SORTED: per-32-point bounding boxes (min, max) of the sorted points
     int nblk;
+    int tstride, toff;   // row tiles of this call: toff, toff + tstride, ... (pc_pairs_part_async)
+    int tile_rows;       // T of the launched kernel (the float64 kernel follows the same tiles)
+    double* claim_sums;  // FLAT direct: one float64 partial per claim
+    int nstage;          // FLAT: claim stages (see kMaxStages)
+    long long st_c0[kMaxStages + 1], st_b0[kMaxStages], st_s[kMaxStages];
 };
 
 __device__ __forceinline__ int steps_for_dev(int n, int i) {
@@ -383,21 +428,36 @@ __device__ __forceinline__ int steps_for_dev(int n, int i) {
 #include "pairs_kernel.cuh"
 #include "pairs_tc.cuh"
 
-// Fixed-order sum of the CTA slots into one result record.
-__global__ void finalize_kernel(const Slot* __restrict__ slots, int nslots, const PrepStats* __restrict__ st,
-                                long long pairs, int direct, pc_pairs_result* __restrict__ out) {
-    __shared__ unsigned long long sc[256], sk[256];
+// Fixed-order sum of the CTA slots and the claim partials into one result record (one
+// block of 256 threads, a fixed partition and tree: the float64 sum is bit-reproducible),
+// and the call's path counters added into the workspace's profile record.
+__global__ void finalize_kernel(const Slot* __restrict__ slots, int nslots, const double* __restrict__ claims,
+                                int nclaims, int claims_hold_sums, const PrepStats* __restrict__ st, int dtype,
+                                long long pairs, int direct,
+                                pc_pairs_result* __restrict__ out, pc_pairs_profile* __restrict__ prof,
+                                int kernel_id, long long pairs_per_chunk) {
+    __shared__ unsigned long long sc[256], sk[256], sp[kNumPaths + 1][256];
     __shared__ double ss[256];
-    unsigned long long c = 0, k = 0;
+    unsigned long long c = 0, k = 0, pth[kNumPaths + 1] = {0, 0, 0, 0, 0, 0};
     double s = 0.0;
-    for (int q = threadIdx.x; q < nslots; q += blockDim.x) { c += slots[q].count; k += slots[q].checks; s += slots[q].sum; }
+    for (int q = threadIdx.x; q < nslots; q += blockDim.x) {
+        c += slots[q].count;
+        k += slots[q].checks;
+        s += slots[q].sum;
+        for (int u = 0; u < kNumPaths; ++u) pth[u] += slots[q].path[u];
+        pth[kNumPaths] += slots[q].rescans;
+    }
+    if (claims_hold_sums)
+        for (int q = threadIdx.x; q < nclaims; q += blockDim.x) s += claims[q];
     sc[threadIdx.x] = c; sk[threadIdx.x] = k; ss[threadIdx.x] = s;
+    for (int u = 0; u <= kNumPaths; ++u) sp[u][threadIdx.x] = pth[u];
     __syncthreads();
     for (int h = blockDim.x / 2; h > 0; h >>= 1) {
         if (threadIdx.x < h) {
             sc[threadIdx.x] += sc[threadIdx.x + h];
             sk[threadIdx.x] += sk[threadIdx.x + h];
             ss[threadIdx.x] += ss[threadIdx.x + h];
+            for (int u = 0; u <= kNumPaths; ++u) sp[u][threadIdx.x] += sp[u][threadIdx.x + h];
         }
         __syncthreads();
     }
@@ -407,28 +467,45 @@ __global__ void finalize_kernel(const Slot* __restrict__ slots, int nslots, cons
         r.sum = ss[0];
         r.pairs = pairs;
         r.exact_checks = (long long)sk[0];
-        r.error = st->nonfinite ? PC_ERR_DOMAIN : PC_OK;
-        if (direct && r.error == PC_OK && !(dec_f64_or0(st->maxabs) < 1e18)) r.error = PC_ERR_ARG;
+        // counts: a non-finite coordinate is InteractionDomainError (collision_indicator,
+        // spi_engine.py:70-71); sums: the float64 kernel evaluated the reference's terms and a
+        // NaN among them is AccumulationError (spi_engine.py:93-95)
+        r.error = direct ? (isnan(ss[0]) ? PC_ERR_DOMAIN : PC_OK) : (st->nonfinite ? PC_ERR_DOMAIN : PC_OK);
         r.reserved = 0;
         *out = r;
+        prof->chunks_gram += (long long)sp[kPathGram][0];
+        prof->chunks_main += (long long)sp[kPathMain][0];
+        prof->chunks_near += (long long)sp[kPathNear][0];
+        prof->chunks_far += (long long)sp[kPathFar][0];
+        prof->chunks_edge += (long long)sp[kPathEdge][0];
+        prof->rows_rescanned += (long long)sp[kNumPaths][0];
+        prof->exact_checks += (long long)sk[0];
+        prof->claims += nclaims;
+        prof->pairs += pairs;
+        prof->pairs_per_chunk = pairs_per_chunk;
+        prof->kernel = kernel_id;
+        if (direct && f64_takes(*st, dtype, direct == 2)) prof->f64_taken = 1;
     }
 }
 
-// Sum + count for float64/integer input whose span defeats the compensated fp32
-// staging (bbox_span > kCompMaxSpan): every owned pair in float64, the count with
-// the reference's own arithmetic (spi_engine.py:68-73) and the term 1/(1+d2) in
-// float64.  Always launched after the compensated kernel; exactly one of the two
-// does the work (each checks the span), the other writes zero slots.
-__global__ void __launch_bounds__(256) pairs_f64_kernel(const PairsArgs a, Slot* __restrict__ slots) {
+// Sum + count in float64 for the calls f64_takes() routes here (non-finite
+// coordinates, |c| >= 1e18, or a non-f32 span the compensated staging cannot hold):
+// every owned pair with the reference's own arithmetic -- the count as
+// collision_indicator (spi_engine.py:68-73), the term 1/(1+d2) as the softened
+// inverse square.  Always launched after the fp32 kernel of a sum call; exactly one
+// of the two does the work (both read the prep statistics), the other writes zero
+// slots.  Rows follow the fp32 kernel's tiles (tile_rows, tstride, toff).
+__global__ void __launch_bounds__(256) pairs_f64_kernel(const PairsArgs a, int comp, Slot* __restrict__ slots) {
     __shared__ unsigned long long s_c[8];
     __shared__ double s_s[8];
-    const bool wide = bbox_span(*a.st, a.dtype) > kCompMaxSpan;
+    const bool wide = f64_takes(*a.st, a.dtype, comp != 0);
     unsigned long long cnt = 0;
     double sum = 0.0;
     if (wide) {
         const bool bal = a.sched == PC_BALANCED;
         for (long long i = a.lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.hi;
              i += (long long)gridDim.x * blockDim.x) {
+            if (a.tstride > 1 && ((i - a.lo) / a.tile_rows) % a.tstride != a.toff) continue;
             const long long m = bal ? steps_for_dev(a.n, (int)i) : (long long)a.n - 1 - i;
             const double xi = coord_f64(a.xyz, a.dtype, i, 0), yi = coord_f64(a.xyz, a.dtype, i, 1),
                          zi = coord_f64(a.xyz, a.dtype, i, 2);
@@ -452,7 +529,7 @@ __global__ void __launch_bounds__(256) pairs_f64_kernel(const PairsArgs a, Slot*
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        Slot sl{0ull, 0ull, 0.0, 0ull};
+        Slot sl{};
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
             sl.count += s_c[w];
             sl.sum += s_s[w];
@@ -561,15 +638,17 @@ __global__ void blk_box_kernel(const float* __restrict__ xyz, long long n, int n
 }
 
 struct WsLayout {
-    size_t pts, stats, slots, tc_a, tc_b, tc_cand, tc_cnt, srt, srt_temp, total;
+    size_t pts, stats, prof, slots, claims, tc_a, tc_b, tc_cand, tc_cnt, srt, srt_temp, total;
 };
 WsLayout ws_layout(long long n) {
     WsLayout l;
     const size_t pair_bytes = align_up((size_t)(n / 2 + 1) * 3 * sizeof(float4), 256);  // up to 3 float4 per pair
     l.pts = 0;  // even pairs, then odd pairs
     l.stats = 2 * pair_bytes;
-    l.slots = l.stats + 256;
-    l.tc_a = align_up(l.slots + (size_t)max_slots(n) * sizeof(Slot), 1024);
+    l.prof = l.stats + 256;  // pc_pairs_profile of the last call
+    l.slots = l.prof + 256;
+    l.claims = align_up(l.slots + (size_t)max_slots(n) * sizeof(Slot), 256);
+    l.tc_a = align_up(l.claims + (size_t)kClaimsCap * sizeof(double), 1024);
     const TcGeom g = tc_geom(n < 0 ? 0 : n);  // tensor-core count kernel operands (64 B per staged point)
     l.tc_b = align_up(l.tc_a + (size_t)g.n_rows * 64, 1024);
     l.tc_cand = align_up(l.tc_b + (size_t)g.n_ext * 64, 256);
@@ -607,7 +686,7 @@ int num_sms() {
 }
 
 template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP, bool SORTED = false>
-int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStream_t s) {
+int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, int* nclaims_out, cudaStream_t s) {
     auto kern = pairs_kernel<WARPS, R, W, DIRECT, FLAT, COMP, SORTED>;
     constexpr int smem = WARPS * pairs_smem_per_warp<R, W, COMP>();
     {
@@ -620,6 +699,7 @@ int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStr
         }
     }
     int grid;
+    *nclaims_out = 0;
     if (FLAT) {
         static thread_local int occ_cache[64] = {0};
         int dev = 0;
@@ -632,9 +712,35 @@ int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStr
         const long long want = (long long)num_sms() * occ_cache[dev & 63];
         const long long chunks = (args.total + W - 1) / W;
         grid = (int)std::max(1LL, std::min(want, (chunks + WARPS - 1) / WARPS));
-        // ~8 super-chunks per warp, each 1..16 chunks
-        const long long per = chunks / ((long long)grid * WARPS * 8);
-        args.super_cols = (long long)W * std::max(1LL, std::min(16LL, per));
+        // claim stages: uniform claims of S chunks for the bulk (S <= PC_CLAIM_MAX, larger only to keep
+        // the claim count within kClaimsCap), then a guided tail -- P claims of (remaining / 2P) chunks,
+        // halving down to single chunks -- so the last claim to finish is one chunk
+        const long long P = (long long)grid * WARPS;
+        long long S = std::max(1LL, std::min((long long)PC_CLAIM_MAX, chunks / (8 * P)));
+        S = std::max(S, (chunks + (kClaimsCap / 2) - 1) / (kClaimsCap / 2));
+        long long rem = chunks, c0 = 0, b0 = 0;
+        int ns = 0;
+        auto add_stage = [&](long long sz, long long k) {
+            args.st_c0[ns] = c0;
+            args.st_b0[ns] = b0;
+            args.st_s[ns] = sz * W;
+            c0 += k;
+            b0 += k * sz * W;
+            rem -= k * sz;
+            ++ns;
+        };
+        const long long bulk = PC_GUIDED ? (chunks - std::min(chunks, 2 * P * S)) / S : chunks / S;
+        if (bulk > 0) add_stage(S, bulk);
+        while (rem > 0) {
+            if (ns == kMaxStages) return arg_fail("too many claim stages");
+            const long long sz = std::max(1LL, std::min(S, rem / (2 * P)));
+            add_stage(sz, sz == 1 ? rem : std::min(P, rem / sz));
+        }
+        args.st_c0[ns] = c0;
+        args.nstage = ns;
+        if (c0 > kClaimsCap) return arg_fail("workspace too small for the claim partials");
+        *nclaims_out = (int)c0;
+        if (DIRECT) CK(cudaMemsetAsync(args.claim_sums, 0, (size_t)c0 * sizeof(double), s));
     } else {
         grid = (args.n_tiles + WARPS - 1) / WARPS;
     }
@@ -657,23 +763,54 @@ int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, cudaStr
     return PC_OK;
 }
 
+// Row tiles of one call: the tiles toff, toff + tstride, ... of [lo, hi) (all of them when
+// tstride = 1) -- pc_pairs_part_async deals a range's tiles round-robin over nparts calls.
+struct TileSel {
+    int tstride, toff;
+};
+inline int tiles_of(long long lo, long long hi, int T, TileSel ts) {
+    const long long all = (hi - lo + T - 1) / T;
+    return all > ts.toff ? (int)((all - ts.toff + ts.tstride - 1) / ts.tstride) : 0;
+}
+// pairs owned by the selected tiles' rows
+long long tile_sel_pairs(long long n, long long lo, long long hi, int T, TileSel ts, int sched) {
+    if (ts.tstride == 1) return row_pairs(n, lo, hi, sched);
+    long long p = 0;
+    for (long long t = ts.toff; lo + t * T < hi; t += ts.tstride)
+        p += row_pairs(n, lo + t * T, std::min(hi, lo + (t + 1) * T), sched);
+    return p;
+}
+// kernel ids recorded in pc_pairs_profile.kernel
+constexpr int kKernGram = 1, kKernDirect = 2, kKernSorted = 3, kKernComp = 4, kKernTc = 5;
+
 template <int WARPS, int R, int W, bool DIRECT, bool COMP = false, bool SORTED = false>
-int dispatch_cfg(PairsArgs args, bool flat, long long cap, int* nslots, cudaStream_t s) {
+int dispatch_cfg(PairsArgs args, bool flat, TileSel ts, long long cap, int* nslots, int* nclaims, int* tile_rows,
+                 long long* pairs_per_chunk, cudaStream_t s) {
     constexpr int T = 32 * R;
-    args.n_tiles = (args.hi - args.lo + T - 1) / T;
+    args.tstride = ts.tstride;
+    args.toff = ts.toff;
+    args.tile_rows = T;
+    args.n_tiles = tiles_of(args.lo, args.hi, T, ts);
+    *tile_rows = T;
+    *pairs_per_chunk = (long long)T * W;
+    *nclaims = 0;
+    if (args.n_tiles == 0) {  // a tile part with no tiles (more parts than tiles)
+        *nslots = 0;
+        return PC_OK;
+    }
     if (flat) {
         args.L = (long long)(T - 1) + (args.n >> 1);
         args.total = (long long)args.n_tiles * args.L;
-        return launch_pairs<WARPS, R, W, DIRECT, true, COMP, SORTED>(args, cap, nslots, s);
+        return launch_pairs<WARPS, R, W, DIRECT, true, COMP, SORTED>(args, cap, nslots, nclaims, s);
     }
-    return launch_pairs<WARPS, R, W, DIRECT, false, COMP>(args, cap, nslots, s);
+    return launch_pairs<WARPS, R, W, DIRECT, false, COMP>(args, cap, nslots, nclaims, s);
 }
 
 // Balanced counts on the tensor cores (pairs_tc.cuh): operands staged once per call,
 // then per row range the persistent kernel (one CTA per SM), the exact pass over its
 // queued candidates and the fixed-order slot sum.
 int run_pairs_tc(const PairsArgs& p, char* ws, const WsLayout& lay, long long n, long long cap, int nranges,
-                 const long long* bounds, pc_pairs_result* dres, cudaStream_t s) {
+                 const long long* bounds, pc_pairs_result* dres, pc_pairs_profile* prof, cudaStream_t s) {
     const TcGeom g = tc_geom(n);
     const long long npts = std::max(g.n_rows, g.n_ext);
     const int pblocks = (int)std::min<long long>((npts + 255) / 256, (long long)num_sms() * 8);
@@ -733,7 +870,8 @@ int run_pairs_tc(const PairsArgs& p, char* ws, const WsLayout& lay, long long n,
             if (ev) CK(cudaEventRecord(ev->b, s));
             nslots = 2 * grid;
         }
-        finalize_kernel<<<1, 256, 0, s>>>(p.slots, nslots, p.st, row_pairs(n, lo, hi, PC_BALANCED), 0, dres + k);
+        finalize_kernel<<<1, 256, 0, s>>>(p.slots, nslots, nullptr, 0, 0, p.st, p.dtype, row_pairs(n, lo, hi, PC_BALANCED),
+                                          0, dres + k, prof, kKernTc, (long long)kTcM * kTcN);
         CK_LAUNCH("finalize_kernel");
     }
     return PC_OK;
@@ -741,8 +879,9 @@ int run_pairs_tc(const PairsArgs& p, char* ws, const WsLayout& lay, long long n,
 
 int run_pairs(const void* xyz, int dtype, long long n, int interaction, int schedule, int tiling,
               int nranges, const long long* bounds, void* workspace, size_t wsb,
-              pc_pairs_result* dres, cudaStream_t s) {
+              pc_pairs_result* dres, cudaStream_t s, TileSel ts = TileSel{1, 0}) {
     g_launches = 0;
+    if (ts.tstride < 1 || ts.toff < 0 || ts.toff >= ts.tstride) return arg_fail("bad tile part (0 <= part < nparts)");
     if (dtype < PC_F32 || dtype > PC_I64) return arg_fail("unknown dtype");
     if (schedule != PC_STANDARD && schedule != PC_BALANCED) return arg_fail("unknown schedule");
     if (interaction < PC_COLLISION || interaction > PC_MANHATTAN1) return arg_fail("unknown interaction");
@@ -757,8 +896,10 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
         return arg_fail("PC_TILE_TC needs a count interaction and the balanced schedule");
     long long rows = 0;  // AUTO: ranges of a few tiles stay on the FFMA kernel (the staging is per call)
     for (int k = 0; k < nranges; ++k) rows += std::max(0LL, (long long)(bounds[k + 1] - bounds[k]));
-    const bool use_tc = tc_ok && (tiling == PC_TILE_TC || (tiling == PC_TILE_AUTO && PC_TC_AUTO && n >= kTcMinN &&
-                                                             n < kTcMaxN && rows * 8 >= n));
+    if (tiling == PC_TILE_TC && ts.tstride != 1) return arg_fail("PC_TILE_TC does not take tile parts");
+    const bool use_tc = tc_ok && ts.tstride == 1 &&
+                        (tiling == PC_TILE_TC || (tiling == PC_TILE_AUTO && PC_TC_AUTO && n >= kTcMinN &&
+                                                  n < kTcMaxN && rows * 8 >= n));
     const bool auto_tiling = tiling == PC_TILE_AUTO, sorted_req = tiling == PC_TILE_SORTED;
     if (sorted_req && (interaction != PC_COLLISION_INVSQ || dtype != PC_F32 || schedule != PC_BALANCED))
         return arg_fail("PC_TILE_SORTED needs the inverse-square sum on fp32 points and the balanced schedule");
@@ -773,13 +914,16 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     float4* pts_even = (float4*)(ws + lay.pts);
     float4* pts_odd = (float4*)(ws + lay.pts + lay.stats / 2);
     PrepStats* st = (PrepStats*)(ws + lay.stats);
+    pc_pairs_profile* prof = (pc_pairs_profile*)(ws + lay.prof);
     Slot* slots = (Slot*)(ws + lay.slots);
+    double* claims = (double*)(ws + lay.claims);
     const bool direct = interaction == PC_COLLISION_INVSQ;
     const bool comp = direct && dtype != PC_F32;  // f32 coordinates are exact as staged
 
     // bbox init: minima to the largest ordered code, maxima to the smallest
     CK(cudaMemsetAsync(st, 0xff, offsetof(PrepStats, mx), s));
     CK(cudaMemsetAsync((char*)st + offsetof(PrepStats, mx), 0, sizeof(PrepStats) - offsetof(PrepStats, mx), s));
+    CK(cudaMemsetAsync(prof, 0, sizeof(pc_pairs_profile), s));
     // whole-range fp32 sums over the balanced schedule run on spatially sorted points
     // (PC_TILE_AUTO on the whole range, or PC_TILE_SORTED for row ranges of the sorted
     // order; PC_TILE_FLAT keeps the input order, the plain kernel)
@@ -828,6 +972,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     args.blk_box = blk_box;
     args.nblk = nblk;
     args.slots = slots;
+    args.claim_sums = claims;
     args.work_ctr = &st->work_ctr;
     args.dtype = dtype;
     args.pred = interaction == PC_COINCIDE ? kPredCoincide : interaction == PC_MANHATTAN1 ? kPredManhattan1 : kPredSphere;
@@ -835,34 +980,45 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     args.sched = schedule;
     args.n = (int)n;
     const long long cap = max_slots(n);
-    if (use_tc) return run_pairs_tc(args, ws, lay, n, cap, nranges, bounds, dres, s);
+    if (use_tc) return run_pairs_tc(args, ws, lay, n, cap, nranges, bounds, dres, prof, s);
+    const int kern_id = !direct ? kKernGram : comp ? kKernComp : sorted ? kKernSorted : kKernDirect;
     for (int k = 0; k < nranges; ++k) {
         const long long lo = bounds[k], hi = bounds[k + 1];
-        int nslots = 0;
+        int nslots = 0, nclaims = 0, trows = 1;
+        long long ppc = 0;
         if (hi > lo && n >= 2) {
             args.lo = (int)lo;
             args.hi = (int)hi;
             const bool flat = tiling == PC_TILE_FLAT;
             int rc;
+#define PC_DISPATCH(CFG, ...) dispatch_cfg<CFG.warps, CFG.r, CFG.w, __VA_ARGS__>(args, flat, ts, cap, &nslots, &nclaims, \
+                                                                                &trows, &ppc, s)
             if (n < kSmallN)
-                rc = comp     ? dispatch_cfg<kSmall.warps, kSmall.r, kSmall.w, true, true>(args, flat, cap, &nslots, s)
-                     : direct ? dispatch_cfg<kSmall.warps, kSmall.r, kSmall.w, true>(args, flat, cap, &nslots, s)
-                              : dispatch_cfg<kSmall.warps, kSmall.r, kSmall.w, false>(args, flat, cap, &nslots, s);
+                rc = comp     ? PC_DISPATCH(kSmall, true, true)
+                     : direct ? PC_DISPATCH(kSmall, true)
+                              : PC_DISPATCH(kSmall, false);
             else
-                rc = comp     ? dispatch_cfg<kBigComp.warps, kBigComp.r, kBigComp.w, true, true>(args, flat, cap, &nslots, s)
-                     : sorted ? dispatch_cfg<kBig.warps, kBig.r, kBig.w, true, false, true>(args, flat, cap, &nslots, s)
-                     : direct ? dispatch_cfg<kBig.warps, kBig.r, kBig.w, true>(args, flat, cap, &nslots, s)
-                              : dispatch_cfg<kBigGram.warps, kBigGram.r, kBigGram.w, false>(args, flat, cap, &nslots, s);
+                rc = comp     ? PC_DISPATCH(kBigComp, true, true)
+                     : sorted ? PC_DISPATCH(kBig, true, false, true)
+                     : direct ? PC_DISPATCH(kBig, true)
+                              : PC_DISPATCH(kBigGram, false);
+#undef PC_DISPATCH
             if (rc) return rc;
-            if (comp) {  // the wide-span float64 path (does nothing unless the span needs it)
+            if (direct) {  // the float64 path (does nothing unless f64_takes: non-finite, huge, wide span)
+                args.tstride = ts.tstride;
+                args.toff = ts.toff;
+                args.tile_rows = trows;
                 const int g2 = (int)std::min<long long>((hi - lo + 255) / 256, (long long)num_sms() * 4);
                 if (nslots + g2 > cap) return arg_fail("workspace too small for the CTA slots");
-                pairs_f64_kernel<<<g2, 256, 0, s>>>(args, slots + nslots);
+                pairs_f64_kernel<<<g2, 256, 0, s>>>(args, comp ? 1 : 0, slots + nslots);
                 CK_LAUNCH("pairs_f64_kernel");
                 nslots += g2;
             }
         }
-        finalize_kernel<<<1, 256, 0, s>>>(slots, nslots, st, row_pairs(n, lo, hi, schedule), direct ? 1 : 0, dres + k);
+        const long long pr = hi > lo && n >= 2 ? tile_sel_pairs(n, lo, hi, trows, ts, schedule) : 0;
+        finalize_kernel<<<1, 256, 0, s>>>(slots, nslots, claims, nclaims, direct ? 1 : 0, st, dtype, pr,
+                                          direct ? (comp ? 2 : 1) : 0,
+                                          dres + k, prof, kern_id, ppc);
         CK_LAUNCH("finalize_kernel");
     }
     return PC_OK;
@@ -1014,8 +1170,12 @@ int pc_pairs(const void* xyz, int32_t dtype, int64_t n, int32_t interaction, int
     return rc;
 }
 
-int pc_pairs_host(const void* xyz_host, int32_t dtype, int64_t n, int32_t interaction, int32_t schedule,
-                  int32_t tiling, int32_t nranges, const int64_t* bounds, pc_pairs_result* results) {
+}  // extern "C"
+namespace {
+thread_local pc_pairs_profile g_last_prof;
+
+int pairs_host_run(const void* xyz_host, int32_t dtype, int64_t n, int32_t interaction, int32_t schedule,
+                   int32_t tiling, int32_t nranges, const int64_t* bounds, pc_pairs_result* results, TileSel ts) {
     if (dtype < PC_F32 || dtype > PC_I64) return arg_fail("unknown dtype");
     if (n < 0) return arg_fail("negative n");
     if (nranges < 1) return arg_fail("need at least one row range");
@@ -1033,13 +1193,49 @@ int pc_pairs_host(const void* xyz_host, int32_t dtype, int64_t n, int32_t intera
     if (n > 0) CK(cudaMemcpyAsync(base, xyz_host, (size_t)n * 3 * dtype_bytes(dtype), cudaMemcpyHostToDevice, s));
     pc_pairs_result* dres = (pc_pairs_result*)(base + in_bytes + ws_bytes);
     rc = run_pairs(base, dtype, n, interaction, schedule, tiling, nranges, (const long long*)bounds,
-                   base + in_bytes, ws_bytes, dres, s);
+                   base + in_bytes, ws_bytes, dres, s, ts);
     const int launches = g_launches;
-    if (rc == PC_OK)
+    if (rc == PC_OK) {
         CK(cudaMemcpyAsync(results, dres, sizeof(pc_pairs_result) * nranges, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&g_last_prof, base + in_bytes + ws_layout(n).prof, sizeof g_last_prof,
+                           cudaMemcpyDeviceToHost, s));
+    }
     CK(cudaStreamSynchronize(s));
     g_launches = launches;
     return rc;
+}
+}  // namespace
+extern "C" {
+
+int pc_pairs_host(const void* xyz_host, int32_t dtype, int64_t n, int32_t interaction, int32_t schedule,
+                  int32_t tiling, int32_t nranges, const int64_t* bounds, pc_pairs_result* results) {
+    return pairs_host_run(xyz_host, dtype, n, interaction, schedule, tiling, nranges, bounds, results, TileSel{1, 0});
+}
+
+int pc_pairs_part_host(const void* xyz_host, int32_t dtype, int64_t n, int32_t interaction, int32_t schedule,
+                       int32_t tiling, int64_t lo, int64_t hi, int32_t part, int32_t nparts, pc_pairs_result* result) {
+    const int64_t b[2] = {lo, hi};
+    return pairs_host_run(xyz_host, dtype, n, interaction, schedule, tiling, 1, b, result, TileSel{nparts, part});
+}
+
+int pc_pairs_part_async(const void* xyz, int32_t dtype, int64_t n, int32_t interaction, int32_t schedule,
+                        int32_t tiling, int64_t lo, int64_t hi, int32_t part, int32_t nparts, void* workspace,
+                        size_t workspace_bytes, pc_pairs_result* result_device, void* stream) {
+    const long long b[2] = {lo, hi};
+    return run_pairs(xyz, dtype, n, interaction, schedule, tiling, 1, b, workspace, workspace_bytes, result_device,
+                     (cudaStream_t)stream, TileSel{nparts, part});
+}
+
+int pc_pairs_last_profile(pc_pairs_profile* out) {
+    *out = g_last_prof;
+    return PC_OK;
+}
+
+int pc_pairs_profile_read(const void* workspace, int64_t n, pc_pairs_profile* out, void* stream) {
+    CK(cudaMemcpyAsync(out, (const char*)workspace + ws_layout(n < 0 ? 0 : n).prof, sizeof *out,
+                       cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    return PC_OK;
 }
 
 int pc_pairs_multi(const void* xyz_host, int32_t dtype, int64_t n, int32_t interaction, int32_t schedule,
@@ -1125,7 +1321,11 @@ int pc_lattice_collisions_multi(const void* xyz_host, int32_t dtype, int64_t n, 
             if (!ml.stream) CK(cudaStreamCreateWithFlags(&ml.stream, cudaStreamNonBlocking));
             cudaStream_t s = ml.stream;
             const size_t in_b = align_up((size_t)n * 3 * dtype_bytes(dtype), 256);
-            const size_t cmp_b = align_up((size_t)n * 12 + 16, 256), key_b = align_up((size_t)n * 4 + 64, 256);
+            // slab grids of >= 2^32 cells (a >= 812 on one device, a >= 1024 on two) take 8-byte keys
+            const unsigned long long cells = (unsigned long long)(xhi - xlo + 2) * side * side;
+            const bool wide_keys = cells >= (1ull << 32);
+            const size_t cmp_b = align_up((size_t)n * 12 + 16, 256),
+                         key_b = align_up((size_t)n * (wide_keys ? 8 : 4) + 64, 256);
             const size_t need = in_b + cmp_b + key_b + 256;
             if (ml.cap < need) {
                 if (ml.buf) CK(cudaFree(ml.buf));
@@ -1134,7 +1334,6 @@ int pc_lattice_collisions_multi(const void* xyz_host, int32_t dtype, int64_t n, 
                 CK(cudaMalloc(&ml.buf, need + need / 8));
                 ml.cap = need + need / 8;
             }
-            const unsigned long long cells = (unsigned long long)(xhi - xlo + 2) * side * side;
             if (ml.grid_cells < cells) {
                 if (ml.grid) CK(cudaFree(ml.grid));
                 ml.grid = nullptr;
@@ -1145,7 +1344,7 @@ int pc_lattice_collisions_multi(const void* xyz_host, int32_t dtype, int64_t n, 
             }
             char* base = (char*)ml.buf;
             int* cmp = (int*)(base + in_b);
-            unsigned* keys = (unsigned*)(base + in_b + cmp_b);
+            void* keys = base + in_b + cmp_b;
             unsigned long long* ctr = (unsigned long long*)(base + in_b + cmp_b + key_b);  // [0] kept, [1] bad
             if (n > 0) CK(cudaMemcpyAsync(base, xyz_host, (size_t)n * 3 * dtype_bytes(dtype), cudaMemcpyHostToDevice, s));
             CK(cudaMemsetAsync(ctr, 0, 8, s));
@@ -1165,8 +1364,10 @@ int pc_lattice_collisions_multi(const void* xyz_host, int32_t dtype, int64_t n, 
                 return PC_OK;
             }
             pc_lattice_result sub;
-            const int rc = lattice_run<unsigned>(cmp, PC_I32, 1, (long long)hc[0], a, ml.grid, keys, 1, 0, &sub, s,
-                                                 cells);
+            const int rc = wide_keys ? lattice_run<unsigned long long>(cmp, PC_I32, 1, (long long)hc[0], a, ml.grid,
+                                                                       keys, 1, 0, &sub, s, cells)
+                                     : lattice_run<unsigned>(cmp, PC_I32, 1, (long long)hc[0], a, ml.grid, keys, 1, 0,
+                                                             &sub, s, cells);
             CK(cudaMemsetAsync(ml.grid, 0, cells * 4, s));  // keep the slab grid clean for the next call
             CK(cudaStreamSynchronize(s));
             if (rc == PC_ERR_OVERFLOW) {

@@ -110,10 +110,10 @@ __device__ __forceinline__ void fence_proxy_async_shared() {
 #define PC_MINB 4
 #endif
 #ifndef PC_GRAM_UNROLL
-#define PC_GRAM_UNROLL 8
+#define PC_GRAM_UNROLL 12
 #endif
 #ifndef PC_DIRECT_UNROLL
-#define PC_DIRECT_UNROLL 2
+#define PC_DIRECT_UNROLL 1
 #endif
 constexpr int kDirectUnroll = PC_DIRECT_UNROLL;
 constexpr int kGramUnroll = PC_GRAM_UNROLL;
@@ -142,16 +142,22 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     static_assert(W % 64 == 0 && T % 64 == 0, "buffers must hold whole pairs for every lane");
     extern __shared__ __align__(16) float4 s_dyn[];
     __shared__ unsigned long long s_red[WARPS][2];
+    // per-warp bookkeeping kept out of the register file (the loops run at 126-128 registers):
+    // chunks per inner loop (kPath*) + rescanned rows, and the claim ids of the current / next chunk
+    __shared__ unsigned s_path[WARPS][kNumPaths + 1];
+    __shared__ long long s_claim[WARPS][2];
     __shared__ __align__(8) unsigned long long s_bar[WARPS][2];  // per-warp TMA completion, one per column buffer
     __shared__ double s_sum[WARPS];
 
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const long long gw = (long long)blockIdx.x * WARPS + wid;
-    if (COMP && bbox_span(*a.st, a.dtype) > kCompMaxSpan) {  // pairs_f64_kernel takes this call
-        if (threadIdx.x == 0) a.slots[blockIdx.x] = Slot{0ull, 0ull, 0.0, 0ull};
+#ifndef PC_NO_F64EXIT
+    if (DIRECT && f64_takes(*a.st, a.dtype, COMP)) {  // pairs_f64_kernel takes this call
+        if (threadIdx.x == 0) a.slots[blockIdx.x] = Slot{};
         return;
     }
+#endif
     const int n = a.n;
     const bool bal = a.sched == PC_BALANCED;
 
@@ -169,33 +175,45 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     // this warp's walk: `left` columns starting at (tile, off); L = window length
     int tile, off, L;
     long long left = 0;
-    // FLAT: warps claim super-chunks of a.super_cols columns from a global counter, so
+    // FLAT: warps claim work from one global counter in guided stages (kMaxStages), so
     // SM-to-SM speed differences and slow-path rescans cannot leave a tail.
-    const long long SUPER = a.super_cols;
     auto claim = [&](int& t, int& o, long long& lft) {
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(a.work_ctr, (unsigned long long)SUPER);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if ((long long)base >= a.total) {
+        unsigned long long c = 0;
+        if (lane == 0) c = atomicAdd(a.work_ctr, 1ull);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        int k = 0;
+        while (k < a.nstage && (long long)c >= a.st_c0[k + 1]) ++k;
+        if (k == a.nstage) {
             lft = 0;
             return;
         }
-        const long long e = (long long)base + SUPER < a.total ? (long long)base + SUPER : a.total;
-        t = (int)((long long)base / L);
-        o = (int)((long long)base - (long long)t * L);
-        lft = e - (long long)base;
+        const long long base = a.st_b0[k] + ((long long)c - a.st_c0[k]) * a.st_s[k];
+        const long long e = base + a.st_s[k] < a.total ? base + a.st_s[k] : a.total;
+        if (base >= e) {
+            lft = 0;
+            return;
+        }
+        if (lane == 0) s_claim[wid][1] = (long long)c;  // the next chunk's claim
+        t = (int)(base / L);
+        o = (int)(base - (long long)t * L);
+        lft = e - base;
     };
+    // first row of tile t of this call (tiles toff, toff + tstride, ... of [lo, hi))
+    auto row0 = [&](int t) -> int { return a.lo + (t * a.tstride + a.toff) * T; };
+    if (lane < kNumPaths + 1) s_path[wid][lane] = 0u;
+    __syncwarp();
     if (FLAT) {
         L = (int)a.L;
         tile = 0;
         off = 0;
         claim(tile, off, left);
+        if (lane == 0) s_claim[wid][0] = s_claim[wid][1];
     } else {
         tile = (int)gw;
         off = 0;
         L = 0;
         if (gw < a.n_tiles) {
-            const int i0 = a.lo + tile * T;
+            const int i0 = row0(tile);
             L = bal ? T - 1 + (n >> 1) : n - 1 - i0;
         }
         left = L;
@@ -218,7 +236,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     // a far column (0, 0, 0, fw): its Gram value is -inf, never a candidate
     const float fw = DIRECT ? 0.f : -INFINITY;
     auto stage_cols = [&](int buf, int t, int o, int wc) {
-        const int j0 = a.lo + t * T + o + 1;  // column k sits at j0 + k (mod n when balanced)
+        const int j0 = row0(t) + o + 1;  // column k sits at j0 + k (mod n when balanced)
         float4* sp = sp0 + buf * (W / 2 * PS);
 #pragma unroll
         for (int q = 0; q < W / 64; ++q) {
@@ -245,7 +263,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
         }
     };
     auto stage_rows = [&](int t) {  // rows i0 .. i0+T-1 (only those < n are read)
-        const int i0 = a.lo + t * T;
+        const int i0 = row0(t);
 #pragma unroll
         for (int q = 0; q < T / 64; ++q) {
             const int rl = 2 * (q * 32 + lane);  // rows rl, rl+1
@@ -264,6 +282,11 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     unsigned valid_rows = 0;
     unsigned long long cnt = 0, checks = 0;
     double sum = 0.0;
+    auto count_path = [&](int k, unsigned v) {
+#ifndef PC_NO_PATHS
+        if (lane == 0) s_path[wid][k] += v;
+#endif
+    };
 
     // Staging of chunk (t, o, wcn) into column buffer b, with the tile's rows when asked.  A full
     // chunk whose window does not wrap is ONE contiguous run of pair entries, and a whole row tile
@@ -284,7 +307,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     unsigned pend = 0;  // bit b: TMA in flight into buffer b; bit 2: a cp.async group in flight
     unsigned phase = 0; // bit b: parity of buffer b's next mbarrier phase
     auto stage = [&](int b, int t, int o, int wcn, bool rows) {
-        const int i0n = a.lo + t * T;
+        const int i0n = row0(t);
         int jw = i0n + o + 1;
         if (bal) jw = wrap(jw);
         const bool cols_tma = kTma && wcn == W && jw + W - 1 < n;
@@ -336,7 +359,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             cp_async_wait<0>();
         }
         __syncwarp();
-        const int i0 = a.lo + tile * T;
+        const int i0 = row0(tile);
         if (tile != cur_tile) {
             cur_tile = tile;
             valid_rows = 0;
@@ -410,6 +433,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             float m[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) m[r] = -INFINITY;
+            count_path(off + 1 >= T ? kPathMain : kPathEdge, 1u);
             if (off + 1 >= T) {
                 // ---- Gram filter, packed: 3 FFMA2 + 1 FMNMX3 per two pairs.  Unowned
                 // cells past a row's window only cost a rescan if they are contacts.
@@ -628,6 +652,10 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 sum += (double)cs;
                 fl |= (cs > sum_flag ? 1u : 0u) << r;  // conservative: a contact's term alone exceeds it
             }
+            count_path((SORTED && gram) ? kPathGram
+                       : !dense ? kPathEdge
+                       : (SORTED && !no_contact) ? kPathNear
+                       : SORTED ? kPathFar : kPathMain, 1u);
             if (SORTED && no_contact) fl = 0;  // also covers the Gram chunks, whose columns were rewritten
             if (SORTED && dense && !no_contact) fl = near_fl;  // exact candidates, not chunk sums
             if (SORTED && gram && staged_tile == tile) {
@@ -691,6 +719,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 const int r = __ffs(rows_any) - 1;
                 rows_any &= rows_any - 1;
                 const unsigned owners = __ballot_sync(0xffffffffu, (fl >> r) & 1u);
+                count_path(kNumPaths, __popc(owners));
                 float vx = 0.f, vy = 0.f, vz = 0.f, vc = 0.f;
 #pragma unroll
                 for (int rr = 0; rr < R; ++rr)
@@ -703,7 +732,22 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 rescan(vx, vy, vz, vc, r, owners);
             }
         }
-        __syncwarp();  // the buffer just read is restaged next iteration
+        __syncwarp();  // the buffer just read is restaged next iteration (and s_claim is visible)
+        if (FLAT) {
+            // end of a claim (a new one was taken for the next chunk, or the work ran out): its
+            // float64 partial goes to its own slot, a fixed association (DESIGN.md §3 "Slots").
+            // Decided from shared memory so no flag stays live across the inner loops.
+            const long long c0 = s_claim[wid][0], c1 = s_claim[wid][1];
+            if (c0 != c1 || nleft == 0) {
+                if (DIRECT) {
+                    const double cs = warp_sum(sum);
+                    if (lane == 0) a.claim_sums[c0] = cs;
+                    sum = 0.0;
+                }
+                __syncwarp();
+                if (lane == 0) s_claim[wid][0] = c1;
+            }
+        }
         tile = ntile;
         off = noff;
         left = nleft;
@@ -722,11 +766,13 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        Slot s{0ull, 0ull, 0.0, 0ull};
+        Slot s{};
         for (int q = 0; q < WARPS; ++q) {
             s.count += s_red[q][0];
             s.checks += s_red[q][1];
             s.sum += s_sum[q];
+            for (int k = 0; k < kNumPaths; ++k) s.path[k] += s_path[q][k];
+            s.rescans += s_path[q][kNumPaths];
         }
         a.slots[blockIdx.x] = s;
     }

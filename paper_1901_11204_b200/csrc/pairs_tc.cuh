@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) pairs_tc_kernel(const TcArgs
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) {
-        Slot sl{0ull, 0ull, 0.0, 0ull};
+        Slot sl{};
         for (int w = 0; w < kTcWarps; ++w) {
             sl.count += s_red[w][0];
             sl.checks += s_red[w][1];
@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(256) tc_exact_kernel(const TcArgs a, Slot* __r
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        Slot sl{0ull, 0ull, 0.0, 0ull};
+        Slot sl{};
         for (int w = 0; w < 8; ++w) {
             sl.count += s_c[w];
             sl.checks += s_k[w];

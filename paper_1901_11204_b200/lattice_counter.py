@@ -339,7 +339,7 @@ def count_collisions_multi_gpu(beads, half_extent: int, devices=None) -> CountRe
         raise ValueError(f"half_extent must be >= 0, got {half_extent}")
     lib = _lib.load()
     if devices is None:
-        devices = list(range(int(lib.pc_device_count())))
+        devices = list(range(_lib.device_count()))
     devs = np.ascontiguousarray(np.asarray(list(devices), dtype=np.int32))
     if len(devs) == 0:
         raise ValueError("need at least one device")

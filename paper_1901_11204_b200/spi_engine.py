@@ -140,48 +140,95 @@ def _device_coords(obj: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(obj)
 
 
-def _first_nonfinite_pair(obj: np.ndarray, f, schedule: str, lo: int, hi: int):
-    """Error path only: the first (row, partner) in the reference's
-    evaluation order whose contribution is non-finite."""
-    n = len(obj)
-    bad = ~np.isfinite(obj).all(axis=1)
-    for i in range(lo, hi):
-        if schedule == "standard":
-            js = np.arange(i + 1, n)
-        else:
-            steps = n // 2 if (n % 2 or i < n // 2) else n // 2 - 1
-            js = (i + np.arange(1, steps + 1)) % n
-        if len(js) == 0 or not (bad[i] or bad[js].any()):
-            continue
-        vals = np.asarray(f(obj[i], obj[js]), dtype=np.float64)
-        miss = np.nonzero(~np.isfinite(vals))[0]
-        if len(miss):
-            return i, int(js[miss[0]])
+def _window_len(n: int, rows: np.ndarray, schedule: str) -> np.ndarray:
+    """Partners each row owns (pair_schedule.py:49-59)."""
+    if schedule == "standard":
+        return n - 1 - rows
+    if n % 2:
+        return np.full(len(rows), (n - 1) // 2, dtype=np.int64)
+    return np.where(rows < n // 2, n // 2, n // 2 - 1)
+
+
+def _first_bad_pair(xyz: np.ndarray, schedule: str, ranges, nan_only: bool):
+    """Error path only (no interaction is evaluated): the first (row, partner)
+    in the reference's evaluation order -- ranges in order, rows in order,
+    partners in window order (spi_engine.py:102-120) -- that involves a
+    non-finite point (``nan_only=False``: collision_indicator raises for
+    such a batch, spi_engine.py:70-71) or whose softened inverse-square term
+    is NaN (``nan_only=True``: a NaN coordinate, or the same infinity on the
+    same axis of both points; 1/(1+inf) = 0 is finite, spi_engine.py:93-95).
+    Returns (range index, i, j) or None."""
+    n = len(xyz)
+    finite = np.isfinite(xyz)
+    bad = np.nonzero(~finite.all(axis=1))[0]
+    if len(bad) == 0:
+        return None
+    nanrow = np.isnan(xyz).any(axis=1)
+    bxyz = xyz[bad]
+    for k, (lo, hi) in enumerate(ranges):
+        for r0 in range(lo, hi, 4096):
+            rows = np.arange(r0, min(hi, r0 + 4096), dtype=np.int64)
+            wl = _window_len(n, rows, schedule)
+            best = np.full(len(rows), np.iinfo(np.int64).max, dtype=np.int64)
+            # a row whose own point is NaN (or any non-finite, for the count) fails at its first partner
+            own_bad = nanrow[rows] if nan_only else ~finite[rows].all(axis=1)
+            best[own_bad & (wl >= 1)] = 1
+            for b0 in range(0, len(bad), 256):
+                bs = bad[b0:b0 + 256]
+                off = bs[None, :] - rows[:, None]
+                if schedule == "balanced":
+                    off %= n
+                owned = (off >= 1) & (off <= wl[:, None])
+                if nan_only:
+                    pts = xyz[rows]
+                    same_inf = (np.isinf(pts)[:, None, :] & (pts[:, None, :] == bxyz[None, b0:b0 + 256, :])).any(-1)
+                    owned &= nanrow[bs][None, :] | same_inf
+                best = np.minimum(best, np.where(owned, off, np.iinfo(np.int64).max).min(axis=1))
+            hit = np.nonzero(best < np.iinfo(np.int64).max)[0]
+            if len(hit):
+                i = int(rows[hit[0]])
+                j = i + int(best[hit[0]])
+                return k, i, (j % n if schedule == "balanced" else j)
     return None
 
 
 def _prepare(obj: np.ndarray, f, ranges: list[tuple[int, int]], schedule: str):
-    """(interaction code, device-ready coordinates) after the reference's
-    domain checks for the rows in ``ranges`` (spi_engine.py:84-99)."""
-    code = _interaction_code(f)
-    xyz = _device_coords(obj)
-    if xyz.dtype.kind == "f" and not np.isfinite(xyz).all():
-        if code == _lib.PC_COLLISION:
-            raise InteractionDomainError("sphere coordinates must be finite")
-        for lo, hi in ranges:
-            hit = _first_nonfinite_pair(obj, f, schedule, lo, hi)
-            if hit:
-                raise AccumulationError(f"non-finite contribution for pair ({hit[0]}, {hit[1]})")
-        raise InteractionDomainError("coordinates must be finite for the GPU inverse-square sum")
-    return code, xyz
+    """(interaction code, device-ready coordinates).  Non-finite coordinates
+    are found by the device (prep statistics), not by a host scan: see
+    _resolve_domain for how they map onto the reference's errors."""
+    del ranges, schedule
+    return _interaction_code(f), _device_coords(obj)
+
+
+def _resolve_domain(xyz: np.ndarray, code: int, schedule: str, ranges, results, rerun):
+    """Reference semantics for a call whose device result flags PC_ERR_DOMAIN.
+
+    * collision_indicator: InteractionDomainError if some owned pair of the
+      ranges touches a non-finite point (the reference's batch check,
+      spi_engine.py:70-71); otherwise those points are in no evaluated pair
+      and the call is rerun with them zeroed.
+    * inverse_square: the device evaluated every term in float64 (isolated
+      infinities give 0, as in the reference); a NaN sum means a NaN term, and
+      the reference raises AccumulationError naming the first such pair
+      (spi_engine.py:93-95)."""
+    if not any(r.error == _lib.PC_ERR_DOMAIN for r in results):
+        return results
+    if code == _lib.PC_COLLISION_INVSQ:
+        hit = _first_bad_pair(xyz, schedule, ranges, nan_only=True)
+        if hit is None:
+            raise AccumulationError("non-finite contribution (pair not located)")
+        raise AccumulationError(f"non-finite contribution for pair ({hit[1]}, {hit[2]})")
+    if xyz.dtype.kind != "f" or _first_bad_pair(xyz, schedule, ranges, nan_only=False) is not None:
+        raise InteractionDomainError("sphere coordinates must be finite")
+    clean = xyz.copy()
+    clean[~np.isfinite(clean).all(axis=1)] = 0
+    return rerun(clean)
 
 
 def _partial_of(r, code: int, n: int, lo: int, hi: int, schedule: str):
     """Typed partial of one kernel result record (int count or float sum)."""
     if r.error == _lib.PC_ERR_DOMAIN:
         raise InteractionDomainError("sphere coordinates must be finite")
-    if r.error == _lib.PC_ERR_ARG:
-        raise ValueError("coordinates too large for the fp32 inverse-square kernel (|c| >= 1e18)")
     pairs = row_pairs(n, lo, hi, schedule)
     if int(r.pairs) != pairs:
         raise RuntimeError(f"kernel pair count {r.pairs} != closed form {pairs}")
@@ -197,7 +244,12 @@ def _run_ranges(obj: np.ndarray, f, ranges: list[tuple[int, int]], schedule: str
         return [(0, 0) for _ in ranges]
     code, xyz = _prepare(obj, f, ranges, schedule)
     bounds = [ranges[0][0]] + [hi for _, hi in ranges]
-    results = _lib.pairs_host(xyz, code, _lib.SCHEDULE_CODES[schedule], bounds)
+    sched = _lib.SCHEDULE_CODES[schedule]
+
+    def run(x):
+        return _lib.pairs_host(x, code, sched, bounds)
+
+    results = _resolve_domain(xyz, code, schedule, ranges, run(xyz), run)
     return [_partial_of(r, code, n, lo, hi, schedule) for (lo, hi), r in zip(ranges, results)]
 
 

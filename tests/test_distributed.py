@@ -90,9 +90,54 @@ def test_slabs_cover_and_balance():
 
 
 def test_pack_roundtrip():
-    s = D.pack_partial(12345, 0.1 + 0.2, 1, 3)
-    counts, sums = D.unpack_partials(s, 3)
+    s = D.pack_partial(12345, 0.1 + 0.2, 1, 3, is_float=True, pairs=77)
+    counts, sums, flags, pairs = D.unpack_partials(s, 3)
     assert counts == [0, 12345, 0] and sums[1] == 0.1 + 0.2 and sums[0] == 0.0
+    assert flags == [0, 1, 0] and pairs == [0, 77, 0]
+
+
+def _ref_compute(obj, f, lo, hi, schedule):
+    """The reference's _run_outer typing (spi_engine.py:109-120): an empty block is int 0."""
+    from oracle import c_oracle
+
+    if lo == hi:
+        return 0
+    c, s, _ = c_oracle.rows(obj, lo, hi, schedule)
+    return c if f == "count" else s
+
+
+def _empty_rank_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        objs = np.array([[0.0, 0.0, 0.0], [0.5, 0.0, 0.0]], dtype=np.float64)
+        q.put((rank, D.spi_distributed(objs, "sum", "balanced", compute=_ref_compute)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_empty_rank_float_sum_same_on_every_rank():
+    """world 3, n = 2: one rank owns no rows and returns int 0 (as the
+    reference's empty worker does); every rank still returns the float total
+    (the partial type now travels with the partial)."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_empty_rank_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = 1.0 / (1.0 + 0.25)
+    for rank in range(world):
+        total, partials, pairs = results[rank]
+        assert total == want and isinstance(total, float)
+        assert sum(pairs) == 1
+        assert 0 in partials and any(isinstance(p, float) for p in partials)
 
 
 def _gpu_worker(rank, world, port, q):

@@ -487,8 +487,12 @@ def test_filter_bypass_for_huge_spans():
     ints = np.array([[2**62, 0, 0], [2**62, 0, 0], [-2**62, 1, 0], [-2**62, 0, 0], [5, 5, 5]], dtype=np.int64)
     assert pc.oracle_collisions(ints) == c_oracle.int_pairs(ints)[0] == 1
     assert pc.oracle_contacts(ints) == c_oracle.int_pairs(ints)[1]
-    with pytest.raises(ValueError):
-        se.spi_balanced(np.array([[0.0, 0, 0], [1e19, 0, 0]]), se.inverse_square)
+    # |c| >= 1e18 overflows fp32 squares: the float64 kernel evaluates the reference's terms
+    huge = np.array([[0.0, 0, 0], [1e19, 0, 0], [1e19 + 2**12, 0.5, 0], [-3e25, 1, 2]])
+    _, s_want, _ = c_oracle.rows(huge, 0, len(huge), "balanced")
+    assert se.spi_balanced(huge, se.inverse_square).total == pytest.approx(s_want, rel=1e-12)
+    assert se.spi_balanced(huge.astype(np.float32), se.inverse_square).total == pytest.approx(
+        c_oracle.rows(huge.astype(np.float32), 0, len(huge), "balanced")[1], rel=1e-12)
 
 
 def test_row_range_api_edges():

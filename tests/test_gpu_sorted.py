@@ -77,27 +77,34 @@ def test_sorted_argument_errors():
 
 
 def test_sorted_path_non_finite_and_degenerate_inputs():
-    # a NaN or inf anywhere: the C ABI reports a domain error on the sorted path too; the
-    # drop-in raises what the reference raises for NaN (AccumulationError naming the first
-    # pair for the float sum, InteractionDomainError for collision_indicator) and refuses
-    # an isolated inf (whose terms the reference would add as zeros) with
-    # InteractionDomainError.  Points on a line (a flat bounding box: zero Morton scale on
-    # two axes) stay exact.
+    # Non-finite coordinates, reference semantics (spi_engine.py:84-99): the sum's terms are
+    # evaluated in float64 by the device (pairs_f64_kernel), so an isolated inf adds
+    # 1/(1+inf) = 0 terms and the total matches the oracle; a NaN term (a NaN coordinate, or
+    # the same inf on one axis of both points) is AccumulationError naming the first pair in
+    # the reference's order; collision_indicator raises InteractionDomainError.  Points on a
+    # line (a flat bounding box: zero Morton scale on two axes) stay exact.
     n = 40_000
     pts = gen.random_spheres(n, 30.0, 2).astype(np.float32)
-    for bad in (np.nan, np.inf):
+    for bad in (np.inf, -np.inf):
         p = pts.copy()
         p[31_337, 1] = bad
+        want_c, want_s, _ = c_oracle.rows(p, 0, n, "balanced")
         (r,) = _lib.pairs_host(p, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, n])
-        assert r.error == _lib.PC_ERR_DOMAIN
-        if np.isnan(bad):
-            with pytest.raises(se.AccumulationError, match="31337"):
-                se.spi_balanced(p, se.inverse_square)
-        else:
-            with pytest.raises(se.InteractionDomainError):
-                se.spi_balanced(p, se.inverse_square)
+        assert r.error == 0 and r.count == want_c and abs(r.sum - want_s) <= 1e-12 * want_s
+        assert se.spi_balanced(p, se.inverse_square).total == r.sum
+        assert _lib.last_profile().f64_taken == 1
         with pytest.raises(se.InteractionDomainError):
             se.spi_balanced(p, se.collision_indicator)
+    p = pts.copy()
+    p[31_337, 1] = np.nan
+    (r,) = _lib.pairs_host(p, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, n])
+    assert r.error == _lib.PC_ERR_DOMAIN
+    with pytest.raises(se.AccumulationError, match=r"\(11337, 31337\)"):
+        se.spi_balanced(p, se.inverse_square)
+    p = pts.copy()
+    p[100, 2] = p[7000, 2] = np.inf  # inf - inf on the same axis: NaN term
+    with pytest.raises(se.AccumulationError, match=r"\(100, 7000\)"):
+        se.spi_balanced(p, se.inverse_square)
     line = np.zeros((n, 3), np.float32)
     line[:, 0] = np.arange(n, dtype=np.float32) * 0.75
     want_c, want_s, _ = c_oracle.rows(line, 0, n, "balanced")

@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 import paper_1901_11204_b200 as pc
+from paper_1901_11204_b200 import _lib
 from paper_1901_11204_b200 import lattice_counter as lc
 from paper_1901_11204_b200 import spi_engine as se
 
@@ -65,13 +66,68 @@ def test_unsupported_interaction_raises_type_error():
         se.spi_balanced(np.zeros((4, 3)), lambda a, b: 1)
 
 
-def test_nonfinite_rejected_before_launch():
+def _brute_first_bad(xyz, schedule, ranges, nan_only):
+    """The reference's evaluation order, pair by pair (spi_engine.py:102-120)."""
+    n = len(xyz)
+    for k, (lo, hi) in enumerate(ranges):
+        for i in range(lo, hi):
+            if schedule == "standard":
+                js = range(i + 1, n)
+            else:
+                steps = n // 2 if (n % 2 or i < n // 2) else n // 2 - 1
+                js = [(i + s) % n for s in range(1, steps + 1)]
+            for j in js:
+                a, b = xyz[i].astype(np.float64), xyz[j].astype(np.float64)
+                if nan_only:
+                    with np.errstate(all="ignore"):
+                        bad = not np.isfinite(1.0 / (1.0 + ((a - b) ** 2).sum()))
+                else:
+                    bad = not (np.isfinite(a).all() and np.isfinite(b).all())
+                if bad:
+                    return k, i, j
+    return None
+
+
+def test_first_bad_pair_matches_reference_order():
+    """Error-path locator (no interaction evaluated on the host) against a
+    pair-by-pair walk: NaN terms (NaN coordinate, same infinity on one axis)
+    for the inverse-square sum, any non-finite point for the count."""
+    rng = np.random.default_rng(5)
+    specials = [np.nan, np.inf, -np.inf]
+    for trial in range(300):
+        n = int(rng.integers(2, 40))
+        xyz = rng.normal(size=(n, 3))
+        for _ in range(int(rng.integers(1, 4))):
+            xyz[rng.integers(0, n), rng.integers(0, 3)] = specials[int(rng.integers(0, 3))]
+        sched = ("standard", "balanced")[trial % 2]
+        w = int(rng.integers(1, 5))
+        ranges = [(b.start, b.stop) for b in se._partition(n, w)]
+        for nan_only in (True, False):
+            assert se._first_bad_pair(xyz, sched, ranges, nan_only) == \
+                _brute_first_bad(xyz, sched, ranges, nan_only), (trial, nan_only)
+
+
+def test_resolve_domain_maps_reference_errors():
+    """PC_ERR_DOMAIN from the device -> the reference's exception (host logic
+    only: the device results are stand-ins)."""
+    class R:
+        def __init__(self, error):
+            self.error, self.count, self.sum, self.pairs = error, 0, 0.0, 0
+
     pts = np.zeros((4, 3))
     pts[2, 1] = np.nan
-    with pytest.raises(se.InteractionDomainError):
-        se.spi_balanced(pts, se.collision_indicator)
     with pytest.raises(se.AccumulationError, match=r"\(0, 2\)"):
-        se.spi_standard(pts, se.inverse_square)
+        se._resolve_domain(pts, _lib.PC_COLLISION_INVSQ, "standard", [(0, 4)], [R(_lib.PC_ERR_DOMAIN)], None)
+    with pytest.raises(se.InteractionDomainError):
+        se._resolve_domain(pts, _lib.PC_COLLISION, "balanced", [(0, 4)], [R(_lib.PC_ERR_DOMAIN)], None)
+    # rows [3, 4) of the standard schedule own no pair: the bad point is never evaluated, so the
+    # call is rerun with it zeroed instead of raising (the reference returns 0 there)
+    seen = []
+    out = se._resolve_domain(pts, _lib.PC_COLLISION, "standard", [(3, 4)], [R(_lib.PC_ERR_DOMAIN)],
+                             lambda x: seen.append(x.copy()) or [R(0)])
+    assert out[0].error == 0 and np.isfinite(seen[0]).all()
+    ok = [R(0)]
+    assert se._resolve_domain(pts, _lib.PC_COLLISION, "standard", [(0, 4)], ok, None) is ok
 
 
 def test_symmetry_audit_runs_on_host():
