@@ -8,14 +8,19 @@ at N=2^20, 1/2/4/8 B200, vs the CPU reference).
 Workload (config 3): N = 2^20 uniform fp32 unit-diameter
 spheres (generators.random_spheres(2^20, (4*pi*N/3)^(1/3), 1)), one step =
 one pass over all C(N,2) pairs computing the exact contact count and the
-softened inverse-square sum, balanced schedule on uniform tiles.  With N>1
-ranks each GPU owns an equal-work slab of outer rows and the partials meet in
-one NCCL int64 all-reduce (strong scaling: total work fixed).
+softened inverse-square sum (Morton sort + the sorted kernel, as spi_balanced
+runs it).  With N>1 ranks, rank r runs row tiles r, r+N, ... of the sorted
+order and the partials meet in one NCCL int64 all-reduce (strong scaling:
+total work fixed).  Every run also reports north_star's scaling config
+(2^22 clustered spheres, count + sum) under the same split
+(``cfg4_clustered_n2^22``).
 
 Rank 0 prints ONE JSON line.  `value` is device-resident throughput (inputs
 already in HBM; CUDA events on the launching stream; max over ranks); `e2e`
-is the same metric through the C-ABI host entry (pc_pairs_host) with the
-pinned host array copied in and the result copied out every step.
+is the same metric through the public API -- spi_balanced (N=1) or
+distributed.spi_distributed (N>1) on a pageable numpy array, host copies in
+the timed region; `roofline.frac` is the executed FMA-pipe work (path counters
+x per-loop SASS cost) against the measured FFMA peak.
 """
 
 from __future__ import annotations
@@ -126,6 +131,9 @@ class ClockSampler:
 
 # ------------------------------------------------------------ reference --
 def run_reference(args):
+    """The reference's own CPU implementation on this box's host cores: the
+    unmodified package from baseline/_ref (``_run_outer`` per sampled row,
+    fork pool over every core), or the oracle port when it is not installed."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
@@ -135,22 +143,24 @@ def run_reference(args):
     n = len(obj)
     cores = os.cpu_count() or 1
     per_step = cores * max(1, args.ref_rows_per_core)
-    times, pairs = [], []
+    times, pairs, kind = [], [], cb.kind()
     for step in range(args.warmup + args.steps):
         rows = cb.sample_rows(n, per_step, 1, offset=step * 7919)
-        p, wall, used = cb.time_sample(obj, rows, "balanced", processes=cores)
+        p, wall, used, kind = cb.time_sample(obj, rows, "balanced", processes=cores)
         if step >= args.warmup:
             times.append(wall)
             pairs.append(p)
     rate = sum(pairs) / sum(times) / 1e9
+    impl = ("unmodified reference paircount (baseline/_ref) _run_outer" if kind == "reference"
+            else "oracle numpy port of the reference's _run_outer")
     line = {
-        "impl": "reference", "metric": f"G pair-tests/s at N=2^20 (contact count + inverse-square sum)",
+        "impl": "reference", "metric": "G pair-tests/s at N=2^20 (contact count + inverse-square sum)",
         "value": rate, "unit": "Gpair/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg3: 2^20 uniform spheres, balanced schedule, reference per-row numpy (oracle port)",
+        "config": {"workload": f"cfg3: 2^20 uniform spheres, balanced schedule, {impl} per sampled row",
                    "n_points": n, "sample": f"{per_step} balanced rows per step x 2 interaction passes"},
-        "cpu_baseline": {"value": rate, "unit": "Gpair/s", "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": rate, "unit": "Gpair/s", "cores": cores, "kind": kind,
                          "sample": f"{per_step} rows/step of {n} ({sum(pairs)} pair-tests timed)",
                          "cpu": cb.cpu_model(), "numpy": np.__version__},
         "e2e": {"value": rate, "unit": "Gpair/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -169,11 +179,52 @@ def cpu_baseline_leg(obj, rows_per_core):
 
     cores = os.cpu_count() or 1
     rows = cb.sample_rows(len(obj), cores * rows_per_core, 1)
-    pairs, wall, used = cb.time_sample(obj, rows, "balanced", processes=cores)
-    return {"value": pairs / wall / 1e9, "unit": "Gpair/s", "cores": used, "kind": "port",
-            "sample": f"{len(rows)} balanced rows of N=2^20 (reference per-row numpy, collision_indicator + "
-                      f"inverse-square passes, fork pool), {pairs} pair-tests in {wall:.1f} s",
+    pairs, wall, used, kind = cb.time_sample(obj, rows, "balanced", processes=cores)
+    who = ("the unmodified reference (baseline/_ref) _run_outer" if kind == "reference"
+           else "the oracle port of the reference's _run_outer")
+    return {"value": pairs / wall / 1e9, "unit": "Gpair/s", "cores": used, "kind": kind,
+            "sample": f"{len(rows)} balanced rows of N=2^20 ({who}: collision_indicator + inverse-square "
+                      f"passes, fork pool over all cores), {pairs} pair-tests in {wall:.1f} s",
             "cpu": cb.cpu_model(), "numpy": np.__version__}
+
+
+def sass_model():
+    """Per-pair FMA-pipe cycles of each inner loop, from the shipped kernels' SASS
+    (scripts/sass_model.py; tests/test_sass_model.py keeps it in sync)."""
+    f = ROOT / "profiles" / "sass_model.json"
+    return json.loads(f.read_text())["kernels"] if f.exists() else {}
+
+
+EDGE_FMA_CYCLES = 8.0  # masked scalar loop: 3 FADD + 3 FFMA + FADD + mask arithmetic per pair (not pinned)
+
+
+def executed_roofline(prof, kern_s, clock_mhz, sms, kernel="sorted_sum"):
+    """FMA-pipe busy fraction predicted from what the kernel executed (path
+    counters x per-pair SASS cost) over the kernel's own duration."""
+    m = sass_model().get(kernel, {})
+    cyc = {"gram": m.get("gram", {}).get("fma_cycles_per_pair"),
+           "near": m.get("near", {}).get("fma_cycles_per_pair"),
+           "far": m.get("direct", {}).get("fma_cycles_per_pair"),
+           "main": m.get("direct", {}).get("fma_cycles_per_pair")}
+    if any(v is None for v in cyc.values()) or not prof.pairs_per_chunk:
+        return None
+    ppc = prof.pairs_per_chunk
+    lane_cycles = ppc * (prof.chunks_gram * cyc["gram"] + prof.chunks_near * cyc["near"] +
+                         prof.chunks_far * cyc["far"] + prof.chunks_main * cyc["main"] +
+                         prof.chunks_edge * EDGE_FMA_CYCLES)
+    # (the slow path's rescans -- rows_rescanned x W columns -- are < 0.1 % of the pairs and left out)
+    smsp_cycles = lane_cycles / 32.0
+    avail = kern_s * clock_mhz * 1e6 * sms * 4
+    chunks = prof.chunks_gram + prof.chunks_near + prof.chunks_far + prof.chunks_main + prof.chunks_edge
+    # a packed FFMA2/FADD2/FMUL2 is 2 lane-ops in 2 pipe cycles, a scalar FMA-pipe op 1 in 1: per lane,
+    # pipe cycles per pair = FMA-pipe lane-ops per pair
+    return {"frac": smsp_cycles / avail, "fma_lane_ops_per_pair": lane_cycles / max(1, prof.pairs),
+            "fma_cycles_per_pair_by_loop": cyc, "clock_mhz": clock_mhz,
+            "path_mix": {"gram": prof.chunks_gram / chunks, "near": prof.chunks_near / chunks,
+                         "far_direct": prof.chunks_far / chunks, "main_direct": prof.chunks_main / chunks,
+                         "edge": prof.chunks_edge / chunks},
+            "chunks": chunks, "pairs_per_chunk": ppc, "rows_rescanned": prof.rows_rescanned,
+            "exact_checks": prof.exact_checks, "claims": prof.claims}
 
 
 def secondary(torch, lib, stream):
@@ -351,64 +402,63 @@ def secondary(torch, lib, stream):
                     "of int64 beads to int32 in pinned chunks streamed to the device (0.8 GB H2D) + the device step"})
     del sp5, pts64
 
-    # ---- the headline workload split 2/4/8 ways the way the multi-GPU step splits it (slabs of
-    # the sorted order, PC_TILE_SORTED): each slab timed alone on this GPU, giving the balance
-    # of the split and a projected per-GPU step (the exchange is one 16-byte all-reduce)
+    # ---- the headline workload split 2/4/8 ways the way the multi-GPU step splits it: row tiles of
+    # the sorted order dealt round-robin (pc_pairs_part_async; what bench N>1 and spi_distributed run),
+    # beside contiguous slabs of the sorted order (round 1's split).  Each share timed alone on this
+    # GPU: the balance of the split and a projected per-GPU step (the exchange is one all-reduce).
     from paper_1901_11204_b200.distributed import row_slabs
+
+    def split_legs(d, n_, ws_, res_, interaction, tiling, worlds=(2, 4, 8)):
+        def timed(fn):
+            _lib.kernel_timing(True)
+            fn()
+            ms_k, _ = _lib.kernel_timing_read()
+            _lib.kernel_timing(False)
+            torch.cuda.synchronize()
+            return ms_k, int(res_[0].item()), int(res_[2].item())
+
+        def whole():
+            _lib.pairs_async(d.data_ptr(), _lib.PC_F32, n_, interaction, _lib.PC_BALANCED, np.array([0, n_]),
+                             ws_.data_ptr(), ws_.numel(), res_.data_ptr(), stream.cuda_stream, tiling)
+
+        timed(whole)
+        full_ms, full_count, _ = timed(whole)
+        out_ = {"kernel_ms_1gpu": full_ms, "count": full_count}
+        for g in worlds:
+            parts = [timed(lambda k=k: _lib.pairs_part_async(
+                d.data_ptr(), _lib.PC_F32, n_, interaction, _lib.PC_BALANCED, 0, n_, k, g, ws_.data_ptr(),
+                ws_.numel(), res_.data_ptr(), stream.cuda_stream, tiling)) for k in range(g)]
+            slabs = [timed(lambda lo=lo, hi=hi: _lib.pairs_async(
+                d.data_ptr(), _lib.PC_F32, n_, interaction, _lib.PC_BALANCED, np.array([lo, hi]), ws_.data_ptr(),
+                ws_.numel(), res_.data_ptr(), stream.cuda_stream, tiling)) for lo, hi in row_slabs(n_, g, "balanced")]
+            out_[f"split{g}"] = {
+                "tile_parts": {"ms_max": max(t for t, _, _ in parts), "ms_min": min(t for t, _, _ in parts),
+                               "projected_speedup": full_ms / max(t for t, _, _ in parts),
+                               "counts_add_up": sum(c for _, c, _ in parts) == full_count},
+                "contiguous_slabs": {"ms_max": max(t for t, _, _ in slabs), "ms_min": min(t for t, _, _ in slabs),
+                                     "projected_speedup": full_ms / max(t for t, _, _ in slabs),
+                                     "counts_add_up": sum(c for _, c, _ in slabs) == full_count}}
+        return out_
 
     d3s = torch.from_numpy(workload_input()).cuda()
     ws3s = torch.empty(_lib.workspace_bytes(n3), dtype=torch.uint8, device="cuda")
     res3s = torch.zeros(8, dtype=torch.int64, device="cuda")
-
-    def run_sorted_slab(lo, hi):
-        _lib.kernel_timing(True)
-        _lib.pairs_async(d3s.data_ptr(), _lib.PC_F32, n3, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED,
-                         np.array([lo, hi]), ws3s.data_ptr(), ws3s.numel(), res3s.data_ptr(), stream.cuda_stream,
-                         _lib.PC_TILE_SORTED)
-        ms_k, _ = _lib.kernel_timing_read()
-        _lib.kernel_timing(False)
-        return ms_k, int(res3s[0].item())
-
-    run_sorted_slab(0, n3)
-    full3_ms, full3_count = run_sorted_slab(0, n3)
-    split3 = {"kernel_ms_1gpu": full3_ms}
-    for g in (2, 4, 8):
-        times, counts = zip(*(run_sorted_slab(lo, hi) for lo, hi in row_slabs(n3, g, "balanced")))
-        split3[f"split{g}"] = {"slab_ms_max": max(times), "slab_ms_min": min(times),
-                               "projected_speedup": full3_ms / max(times),
-                               "partials_sum_equals_total": sum(counts) == full3_count}
-    out["cfg3_headline_sorted_slabs"] = split3
+    out["cfg3_headline_split"] = split_legs(d3s, n3, ws3s, res3s, _lib.PC_COLLISION_INVSQ, _lib.PC_TILE_SORTED)
     del d3s, ws3s
 
-    # ---- config 4: 2^22 clustered points, count; the per-rank slabs of a 2/4/8-GPU split timed
-    # one after another on this GPU (ranks never wait on each other: the only exchange is the final
-    # all-reduce), giving the load balance of the split and a projected multi-GPU step.
-    from paper_1901_11204_b200.distributed import row_slabs
-
+    # ---- config 4: 2^22 clustered points; the count (FFMA2 Gram filter) and the count + sum (sorted
+    # pass) on one GPU and split 2/4/8 ways, each share timed alone (ranks never wait on each other)
     n4 = 2**22
     obj4 = gen.clustered_spheres(n4).astype(np.float32)
     d4 = torch.from_numpy(obj4).cuda()
     ws4 = torch.empty(_lib.workspace_bytes(n4), dtype=torch.uint8, device="cuda")
     res4 = torch.zeros(8, dtype=torch.int64, device="cuda")
-
-    def run_slab(lo, hi):
-        _lib.kernel_timing(True)
-        _lib.pairs_async(d4.data_ptr(), _lib.PC_F32, n4, _lib.PC_COLLISION, _lib.PC_BALANCED, np.array([lo, hi]),
-                         ws4.data_ptr(), ws4.numel(), res4.data_ptr(), stream.cuda_stream, _lib.PC_TILE_FLAT)
-        ms_k, _ = _lib.kernel_timing_read()
-        _lib.kernel_timing(False)
-        return ms_k, int(res4[0].item())
-
-    run_slab(0, n4)  # warm-up
-    full_ms, full_count = run_slab(0, n4)
     pairs4 = n4 * (n4 - 1) // 2
-    cfg4 = {"kernel_ms_1gpu": full_ms, "Gpair_per_s_1gpu": pairs4 / (full_ms * 1e-3) / 1e9, "count": full_count}
-    for g in (2, 4, 8):
-        times, counts = zip(*(run_slab(lo, hi) for lo, hi in row_slabs(n4, g, "balanced")))
-        cfg4[f"split{g}"] = {"slab_ms_max": max(times), "slab_ms_min": min(times),
-                             "projected_step_ms": max(times), "projected_speedup": full_ms / max(times),
-                             "partials_sum_equals_total": sum(counts) == full_count}
-    out["cfg4_clustered_n2^22_count"] = cfg4
+    c4 = split_legs(d4, n4, ws4, res4, _lib.PC_COLLISION, _lib.PC_TILE_FLAT)
+    c4["Gpair_per_s_1gpu"] = pairs4 / (c4["kernel_ms_1gpu"] * 1e-3) / 1e9
+    s4 = split_legs(d4, n4, ws4, res4, _lib.PC_COLLISION_INVSQ, _lib.PC_TILE_SORTED)
+    s4["Gpair_per_s_1gpu"] = pairs4 / (s4["kernel_ms_1gpu"] * 1e-3) / 1e9
+    out["cfg4_clustered_n2^22"] = {"count_ffma_gram": c4, "count_plus_sum_sorted": s4}
     del d4, ws4
 
     # ---- many small vectors: the paper's setting (1000 chain vectors per execution)
@@ -449,13 +499,13 @@ def secondary(torch, lib, stream):
 
 # ------------------------------------------------------------------ ours --
 def run_ours(args):
-    import ctypes
-
     import torch
     import torch.distributed as dist
 
     from paper_1901_11204_b200 import _lib
-    from paper_1901_11204_b200.distributed import row_slabs
+    from paper_1901_11204_b200 import distributed as D
+    from paper_1901_11204_b200 import spi_engine as se
+    from paper_1901_11204_b200.pair_schedule import row_pairs
 
     rank, world, local = dist_env()
     if args.shared_gpu:
@@ -469,28 +519,29 @@ def run_ours(args):
             dist.init_process_group("gloo")
     lib = _lib.load()
     stream = torch.cuda.current_stream()
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
 
     obj = workload_input()
     n = len(obj)
-    lo, hi = row_slabs(n, world, "balanced")[rank]
     total_pairs = n * (n - 1) // 2
     d_obj = torch.from_numpy(obj).cuda()
     ws = torch.empty(_lib.workspace_bytes(n), dtype=torch.uint8, device="cuda")
     res = torch.zeros(8, dtype=torch.int64, device="cuda")  # pc_pairs_result (40 B)
-    slots = torch.zeros(2 * world, dtype=torch.int64, device="cuda")
+    slots = torch.zeros(4 * world, dtype=torch.int64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    bounds = np.array([lo, hi], dtype=np.int64)
 
     def step():
-        # PC_TILE_SORTED: spatially sorted points (what spi_balanced's whole-range call does); with
-        # N ranks each takes its slab of the same sorted order, so the partials sum to the total
-        _lib.pairs_async(d_obj.data_ptr(), _lib.PC_F32, n, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, bounds,
-                         ws.data_ptr(), ws.numel(), res.data_ptr(), stream.cuda_stream, _lib.PC_TILE_SORTED)
+        # the whole-range sum on Morton-sorted points (what spi_balanced runs); with N ranks rank r
+        # runs row tiles r, r+N, ... of the same sorted order (pc_pairs_part_async, D.choose_split)
+        _lib.pairs_part_async(d_obj.data_ptr(), _lib.PC_F32, n, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, 0, n,
+                              rank, world, ws.data_ptr(), ws.numel(), res.data_ptr(), stream.cuda_stream,
+                              _lib.PC_TILE_SORTED)
         launches = _lib.launches()
         if world > 1:
             slots.zero_()
-            slots[2 * rank: 2 * rank + 2].copy_(res[0:2])
-            dist.all_reduce(slots)  # the one NCCL int64 all-reduce of partials
+            slots[4 * rank: 4 * rank + 2].copy_(res[0:2])  # count, float64 sum bits
+            slots[4 * rank + 3].copy_(res[2])                # pairs
+            dist.all_reduce(slots)  # the one NCCL int64 all-reduce of the partials
         return launches
 
     for _ in range(args.warmup):
@@ -515,77 +566,98 @@ def run_ours(args):
     torch.cuda.synchronize()
     kern_ms, kern_launches = _lib.kernel_timing_read()
     _lib.kernel_timing(False)
+    prof = _lib.profile_read(ws.data_ptr(), n, stream.cuda_stream)  # the last step's path counters
     if world > 1:
         dist.barrier()
-        t = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+        t = torch.tensor([elapsed, kern_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
-        counts = slots.view(world, 2)[:, 0].sum().item()
+        elapsed, kern_ms_max = float(t[0].item()), float(t[1].item())
+        v = slots.view(world, 4)
+        counts = int(v[:, 0].sum().item())
+        psum = float(np.array(v[:, 1].cpu().numpy()).view(np.float64).sum())
+        assert int(v[:, 3].sum().item()) == total_pairs
     else:
         counts = int(res[0].item())
+        psum = float(np.array([res[1].item()], dtype=np.int64).view(np.float64)[0])
+        kern_ms_max = kern_ms
     ms_per_step = elapsed / args.steps
     value = total_pairs / (ms_per_step * 1e-3) / 1e9
 
-    # ---- end-to-end through the C-ABI host entry, pinned host buffer
-    pinned = torch.from_numpy(obj).pin_memory()
-    host_view = pinned.numpy()
-    bnd = [lo, hi]
+    # ---- end to end through the public API: a pageable numpy array in, the Python result out
     for _ in range(2):
-        _lib.pairs_host(host_view, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, bnd, tiling=_lib.PC_TILE_SORTED)
+        api_total = (se.spi_balanced(obj, se.inverse_square).total if world == 1 else
+                     D.spi_distributed(obj, se.inverse_square, device="cuda")[0])
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     e2e_launches = 0
     for _ in range(args.steps):
-        (r,) = _lib.pairs_host(host_view, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, bnd, tiling=_lib.PC_TILE_SORTED)
+        if world == 1:
+            api_total = se.spi_balanced(obj, se.inverse_square).total
+        else:
+            api_total = D.spi_distributed(obj, se.inverse_square, device="cuda")[0]
         e2e_launches += _lib.launches()
-        if world > 1:
-            t_slots = torch.zeros(2 * world, dtype=torch.int64, device="cuda")
-            t_slots[2 * rank] = int(r.count)
-            t_slots[2 * rank + 1] = int(np.array([r.sum]).view(np.int64)[0])
-            dist.all_reduce(t_slots)
     e2e_s = (time.perf_counter() - t0) / args.steps
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": total_pairs / e2e_s / 1e9, "unit": "Gpair/s", "h2d_bytes_per_step": int(host_view.nbytes),
-           "d2h_bytes_per_step": 40, "ms_per_step": e2e_s * 1e3,
-           "path": "pc_pairs_host (ctypes) from pinned host memory; one H2D + prep + sort + kernel + finalize + D2H "
-                   "per step"}
+    api_path = ("spi_engine.spi_balanced(points, inverse_square) on a pageable numpy (2^20, 3) float32 array: "
+                "ctypes pc_pairs_host = H2D + bbox + Morton sort + kernel + float64 kernel (idle) + finalize + D2H"
+                if world == 1 else
+                "distributed.spi_distributed(points, inverse_square, device='cuda'): pc_pairs_part_host per rank "
+                "(H2D + sort + this rank's row tiles + D2H) + one NCCL int64 all-reduce of the partials")
+    e2e = {"value": total_pairs / e2e_s / 1e9, "unit": "Gpair/s", "h2d_bytes_per_step": int(obj.nbytes),
+           "d2h_bytes_per_step": 40 + ctypes_sizeof_profile(), "ms_per_step": e2e_s * 1e3, "path": api_path,
+           "api_total": api_total, "device_launches_per_step": e2e_launches / max(1, args.steps)}
+
+    # ---- the north_star scaling config: 2^22 clustered spheres, count + sum (one pass per step)
+    cfg4 = scaling_leg(torch, dist, _lib, rank, world, stream, min(args.steps, 3))
 
     if rank != 0:
         dist.destroy_process_group()
         return 0
 
-    # ---- roofline of the dominant kernel (pairs_kernel, direct formula)
+    # ---- roofline of the dominant kernel (pairs_kernel SORTED, this rank's launches)
     kern_ms_avg = kern_ms / max(1, kern_launches)
-    rank_pairs = (hi - lo) * (n // 2)  # balanced rows own n//2 (odd) or n/2, n/2-1 (even) pairs
-    from paper_1901_11204_b200.pair_schedule import row_pairs
-    rank_pairs = row_pairs(n, lo, hi, "balanced")
-    achieved_tflops = FLOPS_PER_PAIR * rank_pairs / (kern_ms_avg * 1e-3) / 1e12
-    ffma_rate, _ = _lib.microbench(0)
+    rank_pairs = int(prof.pairs)
+    clocks = clk.summary()
+    clock_mhz = clocks.get("sm_mhz") or 1965.0
+    ffma_rate, _ = _lib.microbench(0)  # lane-FFMA/s over all SMs, measured live
     peak_tflops = 2.0 * ffma_rate / 1e12
-    traffic = None
-    tfile = ROOT / "profiles" / "kernel_traffic.json"
+    exe = executed_roofline(prof, kern_ms_avg * 1e-3, clock_mhz, sms)
+    norm_tflops = FLOPS_PER_PAIR * rank_pairs / (kern_ms_avg * 1e-3) / 1e12
     tinfo = {}
+    tfile = ROOT / "profiles" / "kernel_traffic.json"
     if tfile.exists():
         try:
             tinfo = json.loads(tfile.read_text())
-            traffic = tinfo.get("pairs_kernel_direct_flat_n2^20")
         except (ValueError, OSError):
-            traffic = None
-    clocks = clk.summary()
-    roofline = {"bound": "fp32", "achieved": achieved_tflops, "peak": peak_tflops, "unit": "TFLOP/s",
-                "frac": achieved_tflops / peak_tflops, "traffic": traffic,
-                "kernel": "pairs_kernel<128,8,256,DIRECT,FLAT,SORTED>", "kernel_ms": kern_ms_avg,
-                "flops_per_pair": FLOPS_PER_PAIR,
-                "peak_source": "measured live: pc_microbench FFMA stream x 2 flop (no FP32 entry in MEASURED_PEAKS.json)",
-                "pairs_per_s_kernel": rank_pairs / (kern_ms_avg * 1e-3),
-                # the pipe it is bound by: FMA-pipe lane operations per pair are 7.5 in the direct loop
-                # (15 FFMA2-class per 4 pairs) and 5.5 in the tile-local Gram loop (11 per 4); DESIGN.md §3
-                "fma_pipe": {"direct_loop_lane_ops_per_pair": 7.5, "gram_loop_lane_ops_per_pair": 5.5,
-                             "ncu_fma_pipe_active": tinfo.get("pairs_kernel_direct_fma_pipe_active")}}
+            tinfo = {}
+    pairs_s = rank_pairs / (kern_ms_avg * 1e-3)
+    # executed FMA-pipe work against the measured FFMA peak (lane-ops/s)
+    exec_lane_ops_s = (exe["fma_lane_ops_per_pair"] * pairs_s) if exe else None
+    roofline = {
+        "bound": "fp32 FMA pipe", "unit": "TFLOP/s",
+        "achieved": (exec_lane_ops_s * 2.0 / 1e12) if exe else norm_tflops,
+        "peak": peak_tflops,
+        "frac": (exec_lane_ops_s / ffma_rate) if exe else norm_tflops / peak_tflops,
+        "frac_basis": "executed FMA-pipe work (path counters of the timed step x per-pair SASS cost of each inner "
+                      "loop, profiles/sass_model.json) / the measured FFMA peak (pc_microbench, 2 flop per lane-FFMA)",
+        "traffic": tinfo.get("pairs_kernel_direct_flat_n2^20"),
+        "traffic_basis": "dram read+write bytes per launch of this kernel from the committed ncu --set full "
+                         "capture (profiles/kernel_traffic.json), not measured in this run",
+        "kernel": "pairs_kernel<4,8,256,DIRECT,FLAT,SORTED>", "kernel_ms": kern_ms_avg,
+        "pairs_per_s_kernel": pairs_s,
+        "executed": exe,
+        "normalised": {"flops_per_pair": FLOPS_PER_PAIR, "tflops": norm_tflops, "frac": norm_tflops / peak_tflops,
+                       "basis": "12 reference-formula flops per pair (3 sub, 3 mul, 2 add, cmp, add, div, acc); "
+                                "the kernel executes fewer (packed FP32, shared reciprocals, Gram form)"},
+        "survey_model": {"pairs_per_s_ceiling": 3.384e12, "ratio": pairs_s / 3.384e12,
+                         "basis": "SURVEY.md §8(d): 11 scalar instructions per pair at 1.965 GHz; the packed "
+                                  "loops issue fewer, so the ratio exceeds 1"},
+        "ncu_fma_pipe_active": tinfo.get("pairs_kernel_direct_fma_pipe_active"),
+    }
 
     line = {
         "metric": "G pair-tests/s at N=2^20 (contact count + inverse-square sum)",
@@ -596,13 +668,17 @@ def run_ours(args):
                                "inverse-square sum, balanced schedule on uniform tiles",
                    "n_points": n, "pairs_per_step": total_pairs, "schedule": "balanced",
                    "tiling": "flat, on Morton-sorted points (sort inside the step)",
-                   "parallelism": f"row slabs x{world}, one NCCL int64 all-reduce" if world > 1 else "1 GPU",
-                   "l2": "flushed between timed steps (256 MiB memset)", "contacts": int(counts)},
+                   "parallelism": (f"row tiles dealt round-robin over {world} ranks, one NCCL int64 all-reduce"
+                                   if world > 1 else "1 GPU"),
+                   "l2": "flushed between timed steps (256 MiB memset)", "contacts": counts, "inv_sum": psum},
         "roofline": roofline,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clocks,
+        "cfg4_clustered_n2^22": cfg4,
     }
+    if world > 1:
+        line["kernel_ms_max_over_ranks"] = kern_ms_max / max(1, kern_launches)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_leg(obj, args.cpu_rows_per_core)
     if world == 1 and not args.no_secondary:
@@ -611,6 +687,74 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def ctypes_sizeof_profile() -> int:
+    import ctypes
+
+    from paper_1901_11204_b200 import _lib
+
+    return ctypes.sizeof(_lib.PairsProfile)
+
+
+def scaling_leg(torch, dist, _lib, rank, world, stream, steps):
+    """north_star's scaling config (BASELINE config 4): N = 2^22 clustered fp32
+    spheres, one pass per step computing the exact contact count and the
+    inverse-square sum (PC_TILE_SORTED), rank r on row tiles r, r+N, ...; the
+    device time is the max over ranks.  Checked against golden_full.json."""
+    from paper_1901_11204_b200 import generators as gen
+
+    n4 = 2**22
+    obj4 = gen.clustered_spheres(n4).astype(np.float32)
+    d4 = torch.from_numpy(obj4).cuda()
+    ws4 = torch.empty(_lib.workspace_bytes(n4), dtype=torch.uint8, device="cuda")
+    res4 = torch.zeros(8, dtype=torch.int64, device="cuda")
+    slots4 = torch.zeros(4 * world, dtype=torch.int64, device="cuda")
+
+    def one():
+        _lib.pairs_part_async(d4.data_ptr(), _lib.PC_F32, n4, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, 0, n4,
+                              rank, world, ws4.data_ptr(), ws4.numel(), res4.data_ptr(), stream.cuda_stream,
+                              _lib.PC_TILE_SORTED)
+        slots4.zero_()
+        slots4[4 * rank: 4 * rank + 2].copy_(res4[0:2])
+        slots4[4 * rank + 3].copy_(res4[2])
+        if world > 1:
+            dist.all_reduce(slots4)
+
+    one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        one()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    v = slots4.view(world, 4).cpu().numpy()
+    count = int(v[:, 0].sum())
+    inv_sum = float(v[:, 1].copy().view(np.float64).sum())
+    pairs = n4 * (n4 - 1) // 2
+    gold = {}
+    gfile = ROOT / "tests" / "golden" / "golden_full.json"
+    if gfile.exists():
+        gold = json.loads(gfile.read_text()).get("cfg4c", {})
+    prof = _lib.profile_read(ws4.data_ptr(), n4, stream.cuda_stream)
+    del d4, ws4
+    return {"workload": "cfg4 clustered: 2^22 fp32 spheres (1024 Gaussian clusters), exact contact count + "
+                        "inverse-square sum in one sorted pass", "n_gpus": world, "ms_per_step": ms,
+            "Gpair_per_s": pairs / (ms * 1e-3) / 1e9, "steps": steps, "count": count, "inv_sum": inv_sum,
+            "count_matches_oracle": count == gold.get("count"),
+            "sum_rel_err_vs_oracle": (abs(inv_sum - gold["inv_sum"]) / gold["inv_sum"]) if gold else None,
+            "split": f"row tiles round-robin over {world} rank(s)",
+            "rank0_path_mix": {"gram": prof.chunks_gram, "near": prof.chunks_near, "far": prof.chunks_far,
+                               "edge": prof.chunks_edge, "rows_rescanned": prof.rows_rescanned,
+                               "exact_checks": prof.exact_checks}}
 
 
 def main():
