@@ -36,7 +36,7 @@ def test_linear_vs_quadratic_rows_and_append(tmp_path):
     disk = _read(out)
     assert list(disk[0].keys()) == CSV_COLUMNS
     for lin, quad in zip(disk[::2], disk[1::2]):
-        assert lin["algorithm"] == "linear-gpu" and quad["algorithm"] == "quadratic-gpu"
+        assert lin["algorithm"] == "linear" and quad["algorithm"] == "quadratic"
         assert lin["result"] == quad["result"]
     bench_cli.run_linear_vs_quadratic(cfg)
     with open(out) as fh:
@@ -54,7 +54,7 @@ def test_realloc_locality_spi(tmp_path):
     assert len(by_k) == 3 and len({tuple(v) for v in by_k.values()}) == 1
     rows = bench_cli.run_locality_sweep(BenchConfig(sizes=[100], vectors=2, reps=1, seed=5, std_devs=[1.0, 10.0],
                                                     out=out))
-    assert {r["algorithm"] for r in rows} == {"linear-gpu-std1", "linear-gpu-std10"}
+    assert {r["algorithm"] for r in rows} == {"linear-std1", "linear-std10"}
     rows = bench_cli.run_spi_compare(BenchConfig(sizes=[60, 61], vectors=1, reps=2, workers=3, out=out))
     for n in (60, 61):
         assert len({r["result"] for r in rows if r["n"] == n}) == 1
