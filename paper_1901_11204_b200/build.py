@@ -32,16 +32,24 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
+CHECKED_OUT = HERE.parent / "build" / "checked" / "libpaircount.so"
+
+
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> Path:
+    """The shipped library, or with ``checked`` the bounds-checked debug build
+    (-DPC_CHECKED=1, csrc/paircount.cu) used by scripts/sanitize_cases.py."""
+    out = CHECKED_OUT if checked else OUT
     newest = max([HDR.stat().st_mtime] + [f.stat().st_mtime for f in SRC.parent.iterdir() if f.is_file()])
-    if not force and OUT.exists() and OUT.stat().st_mtime >= newest:
-        return OUT
-    tmp = OUT.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), str(SRC), "-o", str(tmp)]
+    if not force and out.exists() and out.stat().st_mtime >= newest:
+        return out
+    out.parent.mkdir(parents=True, exist_ok=True)
+    tmp = out.with_suffix(".so.tmp")
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *(["-DPC_CHECKED=1"] if checked else []),
+           str(SRC), "-o", str(tmp)]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

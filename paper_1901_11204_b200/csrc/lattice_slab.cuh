@@ -360,6 +360,7 @@ __global__ void __launch_bounds__(1024, 1)
             __syncthreads();
             const unsigned s0 = sub_start[s], s1 = s0 + sub_n[s];
             for (unsigned i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+                PC_CHECK((unsigned long long)keys[i] >> kSlabShift == cell0 >> kSlabShift);  // key in this slab
                 const unsigned old = atomicAdd(&cnt[keys[i] & (kSlabCells - 1)], 1u);  // Alg. 1
                 acc += old;
                 first += old == 0u;
@@ -369,8 +370,12 @@ __global__ void __launch_bounds__(1024, 1)
             fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk copy
             __syncthreads();
             const unsigned vec_bytes = (ncell * 4u) & ~15u;
+            PC_CHECK(cell0 + vec_bytes / 4 <= cells);
             if (threadIdx.x == 0 && vec_bytes) bulk_store_s2g(grid + cell0, cnt, vec_bytes);
-            for (unsigned q = vec_bytes / 4 + threadIdx.x; q < ncell; q += blockDim.x) grid[cell0 + q] = cnt[q];
+            for (unsigned q = vec_bytes / 4 + threadIdx.x; q < ncell; q += blockDim.x) {
+                PC_CHECK(cell0 + q < cells);
+                grid[cell0 + q] = cnt[q];
+            }
             flip = flip + 1 == kSlabBufs ? 0 : flip + 1;
         }
     };

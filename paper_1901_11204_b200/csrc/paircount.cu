@@ -37,6 +37,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -80,6 +81,19 @@ int arg_fail(const char* what) {
     } while (0)
 
 constexpr int kPredSphere = 0, kPredCoincide = 1, kPredManhattan1 = 2;
+
+// Checked build (python -m paper_1901_11204_b200.build --checked -> build/checked/): device-side
+// bounds checks on every index the kernels compute for global memory and claim slots; a violation
+// traps (the call fails with PC_ERR_CUDA) instead of corrupting memory.  compute-sanitizer is
+// closed on the GPU pool, so scripts/sanitize_cases.py runs this build, with poisoned scratch
+// (PAIRCOUNT_POISON) and canaries around caller buffers, as the memory-safety evidence.
+#ifndef PC_CHECKED
+#define PC_CHECKED 0
+#endif
+#define PC_CHECK(cond)                         \
+    do {                                       \
+        if (PC_CHECKED && !(cond)) __trap();   \
+    } while (0)
 
 // ------------------------------------------------------------------------
 // small device helpers
@@ -512,6 +526,7 @@ __global__ void __launch_bounds__(256) pairs_f64_kernel(const PairsArgs a, int c
             for (long long s = 1; s <= m; ++s) {
                 long long j = i + s;
                 if (j >= a.n) j -= a.n;
+                PC_CHECK(j >= 0 && j < a.n && i < a.n);
                 const double dx = __dsub_rn(xi, coord_f64(a.xyz, a.dtype, j, 0));
                 const double dy = __dsub_rn(yi, coord_f64(a.xyz, a.dtype, j, 1));
                 const double dz = __dsub_rn(zi, coord_f64(a.xyz, a.dtype, j, 2));
@@ -1035,6 +1050,16 @@ struct Arena {
 };
 Arena g_arena[64];
 
+// PAIRCOUNT_POISON=<byte>: fill the scratch with that byte before every call (debug: a kernel that
+// reads scratch it did not write then gives different results for different poison bytes)
+int poison_byte() {
+    static const int v = [] {
+        const char* e = getenv("PAIRCOUNT_POISON");
+        return e && *e ? (int)(strtol(e, nullptr, 0) & 0xff) : -1;
+    }();
+    return v;
+}
+
 int arena_get(size_t bytes, Arena** out) {
     int dev = 0;
     CK(cudaGetDevice(&dev));
@@ -1047,6 +1072,10 @@ int arena_get(size_t bytes, Arena** out) {
         size_t want = align_up(bytes + bytes / 8, 1 << 20);
         CK(cudaMalloc(&ar.dev, want));
         ar.cap = want;
+    }
+    if (poison_byte() >= 0) {  // synchronous: callers may run the scratch on their own stream
+        CK(cudaMemsetAsync(ar.dev, poison_byte(), ar.cap, ar.stream));
+        CK(cudaStreamSynchronize(ar.stream));
     }
     *out = &ar;
     return PC_OK;

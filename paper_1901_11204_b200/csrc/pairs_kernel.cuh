@@ -228,6 +228,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
         return j;
     };
     auto pair_src = [&](int j) -> const float4* {  // pair (j, (j+1) mod n)
+        PC_CHECK(j >= 0 && j < n);
         return (j & 1 ? a.pts_odd : a.pts_even) + PS * (j >> 1);
     };
 
@@ -318,6 +319,8 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 const unsigned cb = cols_tma ? W / 2 * PS * 16 : 0u, rb = rows_tma ? T / 2 * PS * 16 : 0u;
                 const unsigned bar = bar_base + 8u * b;
                 mbar_expect_tx(bar, cb + rb);
+                PC_CHECK(!cols_tma || (jw >= 0 && jw + W <= n));
+                PC_CHECK(!rows_tma || (i0n >= 0 && i0n + T <= n));
                 if (cols_tma) bulk_g2s(sp0 + b * (W / 2 * PS), pair_src(jw), cb, bar);
                 if (rows_tma) bulk_g2s(rowbuf, pair_src(i0n), rb, bar);
             }
@@ -703,6 +706,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                         if (cand && k < wc && (unsigned)(off + k - rl) < (unsigned)lim) {
                             ++checks;
                             const int j = bal ? wrap(j0 + k) : j0 + k;
+                            PC_CHECK(i >= a.lo && i < a.hi && j >= 0 && j < n && j != i);
                             cnt += exact_pair_call(a.xyz, a.dtype, a.pred, i, j) ? 1ull : 0ull;
                         }
                     }
@@ -741,6 +745,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             if (c0 != c1 || nleft == 0) {
                 if (DIRECT) {
                     const double cs = warp_sum(sum);
+                    PC_CHECK(c0 >= 0 && c0 < a.st_c0[a.nstage]);
                     if (lane == 0) a.claim_sums[c0] = cs;
                     sum = 0.0;
                 }

@@ -416,6 +416,7 @@ __global__ void __launch_bounds__(256) tc_exact_kernel(const TcArgs a, Slot* __r
     unsigned long long cnt = 0, checks = 0;
     for (long long k = threadIdx.x; k < m; k += blockDim.x) {
         const uint2 p = q[k];
+        PC_CHECK((int)p.x < a.n && (int)p.y < a.n && p.x != p.y);
         ++checks;
         cnt += exact_pair(a.xyz, a.dtype, a.pred, (long long)p.x, (long long)p.y) ? 1ull : 0ull;
     }
