@@ -227,6 +227,10 @@ def executed_roofline(prof, kern_s, clock_mhz, sms, kernel="sorted_sum"):
             "exact_checks": prof.exact_checks, "claims": prof.claims}
 
 
+def clock_ghz():
+    return 1.965  # clocks.max.sm; the bench line's `clocks` records what the run saw
+
+
 def secondary(torch, lib, stream):
     """Config 2 (naive vs balanced at N=65,536) and config 5 (counting array)."""
     import ctypes
@@ -235,6 +239,7 @@ def secondary(torch, lib, stream):
     from paper_1901_11204_b200 import generators as gen
 
     out = {}
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     # ---- config 1: N=4,096 integer points, exact-coincidence count (the reference's naive oracle)
     from oracle import numpy_port as npo1
     from paper_1901_11204_b200 import lattice_counter as lc1
@@ -254,6 +259,51 @@ def secondary(torch, lib, stream):
         "api_path": "oracle_collisions(int64 host points): H2D, prep, all-pairs kernel with the exact int64 predicate, D2H",
         "cpu_oracle_ms": cpu_ms, "cpu": "numpy port of the reference's N x N coincidence matrix (1 core)",
         "matches_cpu": got1 == want1}
+
+    # ---- integer all-pairs predicates at scale (oracle_collisions / oracle_contacts, lattice_counter.py:
+    # 227-255) on 2^20 integer points: a normal cloud (std 64, so coordinates span < 1024 per axis)
+    ni = 2**20
+    cloud_i = gen.normal_cloud(ni, 64.0, 512, 3)
+    di = torch.from_numpy(cloud_i.astype(np.int32)).cuda()
+    wsi = torch.empty(_lib.workspace_bytes(ni), dtype=torch.uint8, device="cuda")
+    resi = torch.zeros(8, dtype=torch.int64, device="cuda")
+    pairs_i = ni * (ni - 1) // 2
+
+    def int_leg(inter, tiling, reps=3):
+        for _ in range(2):
+            _lib.pairs_async(di.data_ptr(), _lib.PC_I32, ni, inter, _lib.PC_BALANCED, np.array([0, ni]),
+                             wsi.data_ptr(), wsi.numel(), resi.data_ptr(), stream.cuda_stream, tiling)
+        torch.cuda.synchronize()
+        _lib.kernel_timing(True)
+        for _ in range(reps):
+            _lib.pairs_async(di.data_ptr(), _lib.PC_I32, ni, inter, _lib.PC_BALANCED, np.array([0, ni]),
+                             wsi.data_ptr(), wsi.numel(), resi.data_ptr(), stream.cuda_stream, tiling)
+        ms, cnt = _lib.kernel_timing_read()
+        _lib.kernel_timing(False)
+        torch.cuda.synchronize()
+        ms /= cnt
+        return {"kernel_ms": ms, "Tpair_per_s": pairs_i / (ms * 1e-3) / 1e12, "count": int(resi[0].item()),
+                "exact_checks": int(resi[3].item())}
+
+    _, occ = np.unique(cloud_i, axis=0, return_counts=True)
+    want_col = int((occ * (occ - 1) // 2).sum())
+    col = {"int32_key": int_leg(_lib.PC_COINCIDE, _lib.PC_TILE_KEY),
+           "fp32_gram_filter": int_leg(_lib.PC_COINCIDE, _lib.PC_TILE_FLAT),
+           "tensor_core_filter": int_leg(_lib.PC_COINCIDE, _lib.PC_TILE_TC)}
+    con = {"fp32_gram_filter": int_leg(_lib.PC_MANHATTAN1, _lib.PC_TILE_FLAT),
+           "tensor_core_filter": int_leg(_lib.PC_MANHATTAN1, _lib.PC_TILE_TC)}
+    alu_ceiling = sms * 64 * clock_ghz() * 1e9 / 1.0  # one ISETP.EQ.OR per pair on the 64-lane/clk/SM INT pipe
+    out["integer_predicates_n2^20"] = {
+        "input": "normal_cloud(2^20, std 64, half-extent 512, seed 3) as int32",
+        "oracle_collisions": col, "oracle_contacts": con, "coincidences_np_unique": want_col,
+        "counts_exact": all(v["count"] == want_col for v in col.values()),
+        "chosen": {"oracle_collisions": "int32_key when the bounding box spans <= 1023 per axis "
+                                        "(lattice_counter._integer_pairs), else the Gram filter",
+                   "oracle_contacts": "tensor-core filter (PC_TILE_AUTO) / FP32 Gram filter"},
+        "int32_key_frac_of_int_pipe": col["int32_key"]["Tpair_per_s"] * 1e12 / alu_ceiling,
+        "int_pipe_ceiling_basis": "1 ISETP.EQ.OR per pair (SASS of pairs_key_kernel's loop: 48 ISETP.EQ.OR + 8 LDG "
+                                  "per 48 pairs) at 64 lanes/clk/SM x 148 SMs x the sampled SM clock"}
+    del di, wsi
 
     # ---- config 2
     n2 = 65536

@@ -76,6 +76,10 @@ extern "C" {
                               ranges then index the SORTED order, so each range's result is a
                               partial of the same total (multi-GPU slabs), not the reference's
                               _run_outer over those input rows                                 */
+#define PC_TILE_KEY 5      /* exact coincidence counts (PC_COINCIDE, balanced) by comparing 30-bit
+                              packed keys on the INT32 pipe -- points whose bounding box spans
+                              <= 1023 per axis; else the result's error is PC_ERR_ARG.  The A/B
+                              alternative to the FP32 Gram filter            */
 
 typedef struct {
     int64_t count;         /* integer pair count (collisions / coincidences / contacts)           */

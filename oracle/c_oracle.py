@@ -19,6 +19,8 @@ def _lib():
     lib.orc_rows_f64.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int64,
                                  ctypes.c_int64, _i64p, _f64p, _i64p]
     lib.orc_int_pairs.argtypes = [ctypes.c_void_p, ctypes.c_int64, _i64p, _i64p]
+    lib.orc_int_rows.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
+                                 _i64p, _i64p]
     lib.orc_total_f64.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _i64p, _f64p]
     return lib
 
@@ -54,3 +56,13 @@ def total(obj, lo: int = 0, hi: int | None = None, lib=None):
     if L.orc_total_f64(arr.ctypes.data, len(arr), lo, hi, ctypes.byref(c), ctypes.byref(s)):
         raise ValueError("bad row range")
     return c.value, s.value
+
+
+def int_rows(beads, lo: int, hi: int, schedule: str):
+    """(exact-coincidence pairs, unit-Manhattan pairs) owned by rows [lo, hi)."""
+    arr = np.ascontiguousarray(np.asarray(beads, dtype=np.int64).reshape(-1, 3))
+    col, con = ctypes.c_int64(), ctypes.c_int64()
+    if _lib().orc_int_rows(arr.ctypes.data, len(arr), 1 if schedule == "balanced" else 0, lo, hi,
+                           ctypes.byref(col), ctypes.byref(con)):
+        raise ValueError("bad row range")
+    return col.value, con.value

@@ -85,6 +85,28 @@ int orc_int_pairs(const int64_t* xyz, int64_t n, int64_t* collisions_out, int64_
     return 0;
 }
 
+/* Row-range partial of the integer predicates under a schedule (the row
+ * ownership of orc_rows_f64; lattice_counter.py:238-255 predicates). */
+int orc_int_rows(const int64_t* xyz, int64_t n, int schedule, int64_t lo, int64_t hi, int64_t* collisions_out,
+                 int64_t* contacts_out) {
+    if (lo < 0 || hi > n || lo > hi) return 1;
+    int64_t col = 0, con = 0;
+    const uint64_t* u = (const uint64_t*)xyz;
+    #pragma omp parallel for schedule(dynamic, 16) reduction(+:col, con)
+    for (int64_t i = lo; i < hi; ++i) {
+        const int64_t m = schedule ? steps_for(n, i) : n - 1 - i;
+        for (int64_t k = 1; k <= m; ++k) {
+            const int64_t j = schedule ? (i + k) % n : i + k;
+            const uint64_t dx = u[3 * i] - u[3 * j], dy = u[3 * i + 1] - u[3 * j + 1], dz = u[3 * i + 2] - u[3 * j + 2];
+            if (dx == 0 && dy == 0 && dz == 0) ++col;
+            if (wrap_abs(dx) + wrap_abs(dy) + wrap_abs(dz) == 1) ++con;
+        }
+    }
+    *collisions_out = col;
+    *contacts_out = con;
+    return 0;
+}
+
 /* Whole-triangle totals for the headline sizes (2^20 / 2^22 points, 5.5e11 /
  * 8.8e12 pairs): the contact count and the inverse-square sum over every pair
  * i < j with i in [lo, hi) -- the standard schedule's rows, so [0, n) is the

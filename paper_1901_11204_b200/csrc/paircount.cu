@@ -392,6 +392,8 @@ struct Slot {
     unsigned pad[4];
 };
 static_assert(sizeof(Slot) == 64, "Slot is one 64-byte record");
+// kernel ids recorded in pc_pairs_profile.kernel
+constexpr int kKernGram = 1, kKernDirect = 2, kKernSorted = 3, kKernComp = 4, kKernTc = 5, kKernKey = 6;
 
 // FLAT work claims (guided self-scheduling): claim c of stage k covers columns
 // [b0[k] + (c - c0[k]) * s[k], + s[k]) of the flat (row tile, window column) space.  Stage k
@@ -441,6 +443,7 @@ __device__ __forceinline__ int steps_for_dev(int n, int i) {
 
 #include "pairs_kernel.cuh"
 #include "pairs_tc.cuh"
+#include "pairs_key.cuh"
 
 // Fixed-order sum of the CTA slots and the claim partials into one result record (one
 // block of 256 threads, a fixed partition and tree: the float64 sum is bit-reproducible),
@@ -485,6 +488,7 @@ __global__ void finalize_kernel(const Slot* __restrict__ slots, int nslots, cons
         // spi_engine.py:70-71); sums: the float64 kernel evaluated the reference's terms and a
         // NaN among them is AccumulationError (spi_engine.py:93-95)
         r.error = direct ? (isnan(ss[0]) ? PC_ERR_DOMAIN : PC_OK) : (st->nonfinite ? PC_ERR_DOMAIN : PC_OK);
+        if (kernel_id == kKernKey && st->pad) r.error = PC_ERR_ARG;  // span > 1023: no 30-bit key
         r.reserved = 0;
         *out = r;
         prof->chunks_gram += (long long)sp[kPathGram][0];
@@ -795,8 +799,6 @@ long long tile_sel_pairs(long long n, long long lo, long long hi, int T, TileSel
         p += row_pairs(n, lo + t * T, std::min(hi, lo + (t + 1) * T), sched);
     return p;
 }
-// kernel ids recorded in pc_pairs_profile.kernel
-constexpr int kKernGram = 1, kKernDirect = 2, kKernSorted = 3, kKernComp = 4, kKernTc = 5;
 
 template <int WARPS, int R, int W, bool DIRECT, bool COMP = false, bool SORTED = false>
 int dispatch_cfg(PairsArgs args, bool flat, TileSel ts, long long cap, int* nslots, int* nclaims, int* tile_rows,
@@ -892,6 +894,62 @@ int run_pairs_tc(const PairsArgs& p, char* ws, const WsLayout& lay, long long n,
     return PC_OK;
 }
 
+// Exact coincidence counts by 30-bit key compare (pairs_key.cuh; PC_TILE_KEY).
+int run_pairs_key(const PairsArgs& p, char* ws, const WsLayout& lay, long long n, long long cap, int nranges,
+                  const long long* bounds, pc_pairs_result* dres, pc_pairs_profile* prof, cudaStream_t s) {
+    constexpr int T = 32 * kKeyR;
+    unsigned* ext = (unsigned*)(ws + lay.tc_b);
+    const long long e = 2 * n + 2 * T;
+    if ((size_t)e * 4 > lay.tc_cand - lay.tc_b) return arg_fail("workspace too small for the key array");
+    const int pblocks = (int)std::min<long long>((e + 255) / 256, (long long)num_sms() * 8);
+    if (n > 0) {
+        prep_key_kernel<<<pblocks, 256, 0, s>>>(p.xyz, p.dtype, n, e, const_cast<PrepStats*>(p.st), ext);
+        CK_LAUNCH("prep_key_kernel");
+    }
+    KeyArgs a{};
+    a.ext = ext;
+    a.st = p.st;
+    a.slots = p.slots;
+    a.work_ctr = p.work_ctr;
+    a.n = (int)n;
+    a.L = T - 1 + (int)(n >> 1);
+    a.cpt = (a.L + kKeyW - 1) / kKeyW;
+    for (int k = 0; k < nranges; ++k) {
+        const long long lo = bounds[k], hi = bounds[k + 1];
+        int nslots = 0;
+        if (hi > lo && n >= 2) {
+            a.lo = (int)lo;
+            a.hi = (int)hi;
+            a.n_tiles = (int)((hi - lo + T - 1) / T);
+            a.units = (long long)a.n_tiles * a.cpt;
+            const long long want = (long long)num_sms() * 4;
+            const int grid = (int)std::max(1LL, std::min(want, (a.units + kKeyWarps - 1) / kKeyWarps));
+            a.group = (int)std::max(1LL, std::min(16LL, a.units / ((long long)grid * kKeyWarps * 8)));
+            if (grid > cap) return arg_fail("workspace too small for the CTA slots");
+            CK(cudaMemsetAsync(p.work_ctr, 0, sizeof(unsigned long long), s));
+            EvPair* ev = nullptr;
+            if (g_timing && g_ev_used < 4096) {
+                if (g_ev_used == g_ev_made) {
+                    CK(cudaEventCreate(&g_ev[g_ev_made].a));
+                    CK(cudaEventCreate(&g_ev[g_ev_made].b));
+                    ++g_ev_made;
+                }
+                ev = &g_ev[g_ev_used++];
+                CK(cudaEventRecord(ev->a, s));
+            }
+            pairs_key_kernel<<<grid, kKeyWarps * 32, 0, s>>>(a);
+            CK_LAUNCH("pairs_key_kernel");
+            if (ev) CK(cudaEventRecord(ev->b, s));
+            nslots = grid;
+        }
+        finalize_kernel<<<1, 256, 0, s>>>(p.slots, nslots, nullptr, 0, 0, p.st, p.dtype,
+                                          row_pairs(n, lo, hi, PC_BALANCED), 0, dres + k, prof, kKernKey,
+                                          (long long)T * kKeyW);
+        CK_LAUNCH("finalize_kernel");
+    }
+    return PC_OK;
+}
+
 int run_pairs(const void* xyz, int dtype, long long n, int interaction, int schedule, int tiling,
               int nranges, const long long* bounds, void* workspace, size_t wsb,
               pc_pairs_result* dres, cudaStream_t s, TileSel ts = TileSel{1, 0}) {
@@ -916,9 +974,12 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
                         (tiling == PC_TILE_TC || (tiling == PC_TILE_AUTO && PC_TC_AUTO && n >= kTcMinN &&
                                                   n < kTcMaxN && rows * 8 >= n));
     const bool auto_tiling = tiling == PC_TILE_AUTO, sorted_req = tiling == PC_TILE_SORTED;
+    const bool use_key = tiling == PC_TILE_KEY;
+    if (use_key && (interaction != PC_COINCIDE || schedule != PC_BALANCED || ts.tstride != 1))
+        return arg_fail("PC_TILE_KEY needs the coincidence count, the balanced schedule and no tile parts");
     if (sorted_req && (interaction != PC_COLLISION_INVSQ || dtype != PC_F32 || schedule != PC_BALANCED))
         return arg_fail("PC_TILE_SORTED needs the inverse-square sum on fp32 points and the balanced schedule");
-    if (tiling == PC_TILE_AUTO || tiling == PC_TILE_TC || tiling == PC_TILE_SORTED)
+    if (tiling == PC_TILE_AUTO || tiling == PC_TILE_TC || tiling == PC_TILE_SORTED || use_key)
         tiling = schedule == PC_BALANCED ? PC_TILE_FLAT : PC_TILE_PER_ROW_TILE;
     if (tiling == PC_TILE_FLAT && schedule != PC_BALANCED)
         return arg_fail("PC_TILE_FLAT needs the balanced schedule (equal windows per row tile)");
@@ -996,6 +1057,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     args.n = (int)n;
     const long long cap = max_slots(n);
     if (use_tc) return run_pairs_tc(args, ws, lay, n, cap, nranges, bounds, dres, prof, s);
+    if (use_key) return run_pairs_key(args, ws, lay, n, cap, nranges, bounds, dres, prof, s);
     const int kern_id = !direct ? kKernGram : comp ? kKernComp : sorted ? kKernSorted : kKernDirect;
     for (int k = 0; k < nranges; ++k) {
         const long long lo = bounds[k], hi = bounds[k + 1];

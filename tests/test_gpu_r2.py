@@ -190,3 +190,36 @@ def test_nccl_exchange_world_size_1():
         assert (counts, sums, flags, prs) == ([7], [0.5], [1], [3])
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [2, 3, 191, 192, 193, 5000, 40001, 70000])
+def test_int32_key_coincidence_counts(n):
+    """PC_TILE_KEY (packed 30-bit keys, INT32 compares) against the oracle, whole
+    range and row ranges, and through oracle_collisions (which routes there)."""
+    rng = np.random.default_rng(n)
+    pts = rng.integers(-6, 7, size=(n, 3)).astype(np.int64) * rng.integers(1, 3) + 300
+    want = c_oracle.int_pairs(pts)[0]
+    assert pc.oracle_collisions(pts) == want
+    assert _lib.last_profile().kernel == 6
+    for b in ([0, n], [0, n // 3, n // 2, n]):
+        rs = _lib.pairs_host(pts.astype(np.int32), _lib.PC_COINCIDE, _lib.PC_BALANCED, b, tiling=_lib.PC_TILE_KEY)
+        for (lo, hi), r in zip(zip(b[:-1], b[1:]), rs):
+            assert r.error == 0 and r.count == c_oracle.int_rows(pts, lo, hi, "balanced")[0], (lo, hi)
+        assert sum(r.count for r in rs) == want
+
+
+def test_int32_key_span_limits():
+    base = np.zeros((5000, 3), dtype=np.int64)
+    base[:, 0] = np.arange(5000) % 1024          # span 1023: keys fit
+    base[::7] = base[1::7][: len(base[::7])]      # plant coincidences
+    want = c_oracle.int_pairs(base)[0]
+    (r,) = _lib.pairs_host(base, _lib.PC_COINCIDE, _lib.PC_BALANCED, [0, 5000], tiling=_lib.PC_TILE_KEY)
+    assert r.error == 0 and r.count == want
+    wide = base.copy()
+    wide[0, 2] = 1024                             # span 1024: the key path refuses, AUTO still exact
+    (r,) = _lib.pairs_host(wide, _lib.PC_COINCIDE, _lib.PC_BALANCED, [0, 5000], tiling=_lib.PC_TILE_KEY)
+    assert r.error == _lib.PC_ERR_ARG
+    assert pc.oracle_collisions(wide) == c_oracle.int_pairs(wide)[0]
+    assert _lib.last_profile().kernel != 6
+    with pytest.raises(ValueError, match="PC_TILE_KEY"):
+        _lib.pairs_host(base, _lib.PC_MANHATTAN1, _lib.PC_BALANCED, [0, 5000], tiling=_lib.PC_TILE_KEY)

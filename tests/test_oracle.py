@@ -80,6 +80,11 @@ def test_lattice_port(golden_small):
         assert npo.oracle_contacts(beads) == case["oracle_contacts"], case["tag"]
         col, con = c_oracle.int_pairs(beads)
         assert (col, con) == (case["oracle_collisions"], case["oracle_contacts"]), case["tag"]
+        # the row-range integer oracle: any partition of the rows adds up, under both schedules
+        n = len(beads)
+        for sched in ("standard", "balanced"):
+            parts = [c_oracle.int_rows(beads, lo, hi, sched) for lo, hi in npo.partition(n, 3)]
+            assert (sum(p[0] for p in parts), sum(p[1] for p in parts)) == (col, con), case["tag"]
         if "count_collisions" in case:
             assert list(npo.count_collisions(beads, case["half_extent"])) == case["count_collisions"], case["tag"]
             cells = npo.new_dense_space(case["half_extent"])
