@@ -432,6 +432,8 @@ struct PairsArgs {
     int tile_rows;       // T of the launched kernel (the float64 kernel follows the same tiles)
     double* claim_sums;  // FLAT direct: one float64 partial per claim
     int nstage;          // FLAT: claim stages (see kMaxStages)
+    long long blk_cols;  // FLAT: columns per block of the transposed claim order (pairs_kernel.cuh)
+    long long win_blks;  // FLAT: blocks per tile window
     long long st_c0[kMaxStages + 1], st_b0[kMaxStages], st_s[kMaxStages];
 };
 
@@ -731,13 +733,19 @@ int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, int* nc
         const long long want = (long long)num_sms() * occ_cache[dev & 63];
         const long long chunks = (args.total + W - 1) / W;
         grid = (int)std::max(1LL, std::min(want, (chunks + WARPS - 1) / WARPS));
-        // claim stages: uniform claims of S chunks for the bulk (S <= PC_CLAIM_MAX, larger only to keep
-        // the claim count within kClaimsCap), then a guided tail -- P claims of (remaining / 2P) chunks,
-        // halving down to single chunks -- so the last claim to finish is one chunk
+        // claim stages over the block-transposed (tile, column) space (pairs_kernel.cuh claim()):
+        // uniform claims of S chunks (one block, S a power of two <= PC_CLAIM_MAX, larger only to
+        // keep the claim count within kClaimsCap) for the bulk, then a guided tail -- P claims of
+        // about (remaining / 2P) chunks, a power of two, halving down to single chunks
         const long long P = (long long)grid * WARPS;
-        long long S = std::max(1LL, std::min((long long)PC_CLAIM_MAX, chunks / (8 * P)));
-        S = std::max(S, (chunks + (kClaimsCap / 2) - 1) / (kClaimsCap / 2));
-        long long rem = chunks, c0 = 0, b0 = 0;
+        auto pow2_floor = [](long long v) { long long p2 = 1; while (p2 * 2 <= v) p2 *= 2; return p2; };
+        long long S = pow2_floor(std::max(1LL, std::min((long long)PC_CLAIM_MAX, chunks / (8 * P))));
+        while (S * (kClaimsCap / 2) < chunks) S *= 2;
+        args.blk_cols = S * W;
+        const long long nb = (args.L + args.blk_cols - 1) / args.blk_cols;  // blocks per window
+        args.win_blks = nb;
+        const long long vchunks = (long long)args.n_tiles * nb * S;         // incl. the windows' ragged ends
+        long long rem = vchunks, c0 = 0, b0 = 0;
         int ns = 0;
         auto add_stage = [&](long long sz, long long k) {
             args.st_c0[ns] = c0;
@@ -748,11 +756,11 @@ int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, int* nc
             rem -= k * sz;
             ++ns;
         };
-        const long long bulk = PC_GUIDED ? (chunks - std::min(chunks, 2 * P * S)) / S : chunks / S;
+        const long long bulk = PC_GUIDED ? (vchunks - std::min(vchunks, 2 * P * S)) / S : vchunks / S;
         if (bulk > 0) add_stage(S, bulk);
         while (rem > 0) {
             if (ns == kMaxStages) return arg_fail("too many claim stages");
-            const long long sz = std::max(1LL, std::min(S, rem / (2 * P)));
+            const long long sz = pow2_floor(std::max(1LL, std::min(S, rem / (2 * P))));
             add_stage(sz, sz == 1 ? rem : std::min(P, rem / sz));
         }
         args.st_c0[ns] = c0;

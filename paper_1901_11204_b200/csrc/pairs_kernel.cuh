@@ -152,6 +152,10 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const long long gw = (long long)blockIdx.x * WARPS + wid;
+#ifdef PC_TIMELINE  // debug: per-warp start / end (globaltimer ns) into the claim-sum area's tail
+    unsigned long long t_start = 0;
+    if (DIRECT && FLAT) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
 #ifndef PC_NO_F64EXIT
     if (DIRECT && f64_takes(*a.st, a.dtype, COMP)) {  // pairs_f64_kernel takes this call
         if (threadIdx.x == 0) a.slots[blockIdx.x] = Slot{};
@@ -177,26 +181,38 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     long long left = 0;
     // FLAT: warps claim work from one global counter in guided stages (kMaxStages), so
     // SM-to-SM speed differences and slow-path rescans cannot leave a tail.
+    // Claims index a block-transposed order of the (tile, window column) space: block b of blk_cols
+    // columns is window block b / n_tiles of tile b % n_tiles (window blocks ordered 0, last, 1, 2,
+    // ...), so every tile's leading block (the masked self chunk and, on sorted points, the near
+    // chunks with their rescans) and its trailing block (the ragged masked end of the window) are
+    // handed out before any far block, and the tail is uniform far work.  A claim never crosses a block
+    // (stage sizes are powers of two dividing the block); one that falls past a window's end is
+    // empty and skipped.
     auto claim = [&](int& t, int& o, long long& lft) {
-        unsigned long long c = 0;
-        if (lane == 0) c = atomicAdd(a.work_ctr, 1ull);
-        c = __shfl_sync(0xffffffffu, c, 0);
-        int k = 0;
-        while (k < a.nstage && (long long)c >= a.st_c0[k + 1]) ++k;
-        if (k == a.nstage) {
-            lft = 0;
+        for (;;) {
+            unsigned long long c = 0;
+            if (lane == 0) c = atomicAdd(a.work_ctr, 1ull);
+            c = __shfl_sync(0xffffffffu, c, 0);
+            int k = 0;
+            while (k < a.nstage && (long long)c >= a.st_c0[k + 1]) ++k;
+            if (k == a.nstage) {
+                lft = 0;
+                return;
+            }
+            const long long v = a.st_b0[k] + ((long long)c - a.st_c0[k]) * a.st_s[k];
+            const long long blk = v / a.blk_cols;
+            const int tt = (int)(blk % a.n_tiles);
+            long long ob = blk / a.n_tiles;  // window blocks in the order 0, last, 1, 2, ...: both ragged ends early
+            ob = ob == 0 ? 0 : ob == 1 ? a.win_blks - 1 : ob - 1;
+            const long long oo = ob * a.blk_cols + (v - blk * a.blk_cols);
+            const long long len = min(a.st_s[k], (long long)L - oo);
+            if (len <= 0) continue;  // past the end of the window
+            if (lane == 0) s_claim[wid][1] = (long long)c;  // the next chunk's claim
+            t = tt;
+            o = (int)oo;
+            lft = len;
             return;
         }
-        const long long base = a.st_b0[k] + ((long long)c - a.st_c0[k]) * a.st_s[k];
-        const long long e = base + a.st_s[k] < a.total ? base + a.st_s[k] : a.total;
-        if (base >= e) {
-            lft = 0;
-            return;
-        }
-        if (lane == 0) s_claim[wid][1] = (long long)c;  // the next chunk's claim
-        t = (int)(base / L);
-        o = (int)(base - (long long)t * L);
-        lft = e - base;
     };
     // first row of tile t of this call (tiles toff, toff + tstride, ... of [lo, hi))
     auto row0 = [&](int t) -> int { return a.lo + (t * a.tstride + a.toff) * T; };
@@ -760,6 +776,17 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
         buf ^= 1;
     }
 
+#ifdef PC_TIMELINE
+    if (DIRECT && FLAT && lane == 0) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        unsigned long long* tl = reinterpret_cast<unsigned long long*>(a.claim_sums + (kClaimsCap - 2 * 8192));
+        if (gw < 4096) {
+            tl[2 * gw] = t_start;
+            tl[2 * gw + 1] = t_end;
+        }
+    }
+#endif
     // ---- CTA reduction (the only CTA barrier): one slot per CTA ----
     cnt = warp_sum(cnt);
     checks = warp_sum(checks);
