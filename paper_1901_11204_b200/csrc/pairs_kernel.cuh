@@ -130,8 +130,10 @@ constexpr int pairs_smem_per_warp() {
 // evaluated in Gram form against tile-local origins, p = A_i + (B_j - 2 a_i.b_j), with
 // a_i = q_i - o, b_j = q_j - o, A_i = 1 + |a_i|^2, B_j = |b_j|^2: 4 packed ops per two
 // pairs instead of 6.  Taken only where the bound on the form's rounding error,
-// 5u (|a|max + |b|max)^2, is below 2e-6 (1 + dmin^2) -- every such term within 2e-6
-// relative, 5x inside the 1e-5 tolerance -- and dmin > 2, so the chunk holds no contact.
+// 8u (|a|max + |b|max)^2 (the subtractions a = q - o, b = q - o, the |b|^2 chain, three
+// FFMA2 and the FADD2), is below 3.2e-6 (1 + dmin^2) -- every such term within 3.2e-6
+// relative; with the in-chunk fp32 accumulation (gamma_64 = 3.8e-6) the total stays below
+// 1e-5 (DESIGN.md §3 "Error budget") -- and dmin > 2.12, so the chunk holds no contact.
 // The boxes also decide the contact test: more than 1.5 apart, none; closer, each row's
 // smallest p flags its candidates (the chunk-sum test would flag every row there).
 template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP = false, bool SORTED = false>
@@ -519,8 +521,9 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                     const float bb = fmaxf(fabsf(cl - o[k]), fabsf(ch - o[k]));
                     bm2 += bb * bb;
                 }
-                // 5u (|a| + |b|)^2 <= 2e-6 (1 + dmin^2), u = 2^-24: five roundings of terms of at
-                // most (|a| + |b|)^2 against p >= 1 + dmin^2
+                // 8u (|a| + |b|)^2 <= 3.2e-6 (1 + dmin^2), u = 2^-24 -- written as the same
+                // inequality 5u (..)^2 <= 2e-6 (..): eight roundings of terms of at most
+                // (|a| + |b|)^2 against p >= 1 + dmin^2
                 const float ab = sqrtf(rt2) + sqrtf(bm2);
                 gram = gap2 > 4.5f && 2.98023223876953125e-07f * ab * ab <= 2e-6f * (1.f + gap2);
                 // boxes more than 1.5 apart: no contact, so no rescan however large the chunk's

@@ -106,6 +106,35 @@ def check_tc(rng, stats):
             print(f"MISMATCH {name} n={n} span={span}: got {r.count} want {want}", flush=True)
 
 
+def check_parts(rng, stats):
+    # round 2: tile parts (pc_pairs_part_host) of a random range add up to the oracle's range
+    # result on the sorted / direct / Gram paths; sums bit-reproducible across repeats
+    n = int(rng.choice([2, 3, 257, 5000, 16385, 40001, 65537]))
+    pts, kind = random_points(rng, n)
+    pts = pts.astype(np.float32)
+    lo = int(rng.integers(0, n))
+    hi = int(rng.integers(lo, n + 1))
+    if rng.random() < 0.5:
+        lo, hi = 0, n
+    nparts = int(rng.integers(1, 9))
+    want_c, want_s, want_p = c_oracle.rows(pts, lo, hi, "balanced")
+    for inter, tiling in ((_lib.PC_COLLISION_INVSQ, _lib.PC_TILE_SORTED if (lo, hi) == (0, n) else _lib.PC_TILE_FLAT),
+                          (_lib.PC_COLLISION, _lib.PC_TILE_FLAT)):
+        parts = [_lib.pairs_part_host(pts, inter, _lib.PC_BALANCED, lo, hi, k, nparts, tiling) for k in range(nparts)]
+        c = sum(q.count for q in parts)
+        pr = sum(q.pairs for q in parts)
+        ok = c == want_c and pr == want_p and all(q.error == 0 for q in parts)
+        if inter == _lib.PC_COLLISION_INVSQ and want_p:
+            s = sum(q.sum for q in parts)
+            ok = ok and math.isclose(s, want_s, rel_tol=1e-6)
+            again = _lib.pairs_part_host(pts, inter, _lib.PC_BALANCED, lo, hi, 0, nparts, tiling)
+            ok = ok and again.sum == parts[0].sum
+        stats[(f"parts-{'sum' if inter == _lib.PC_COLLISION_INVSQ else 'count'}", ok)] += 1
+        if not ok:
+            print(f"MISMATCH parts n={n} {kind} [{lo},{hi}) x{nparts} inter={inter}: got {c} want {want_c}",
+                  flush=True)
+
+
 def check_int(rng, stats):
     n = int(rng.choice([1, 2, 5, 100, 1000, 4096, 5000, 20000]))
     span = int(rng.integers(1, 40))
@@ -161,6 +190,7 @@ def main():
         check_int(rng, stats)
         check_lattice(rng, stats)
         check_tc(rng, stats)
+        check_parts(rng, stats)
         if args.sorted:
             check_sorted(rng, stats)
         rounds += 1
