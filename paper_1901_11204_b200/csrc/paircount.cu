@@ -447,11 +447,31 @@ __device__ __forceinline__ int steps_for_dev(int n, int i) {
 #include "pairs_tc.cuh"
 #include "pairs_key.cuh"
 
+// First stage of the claim-sum reduction for large claim counts: block b adds claims
+// [b*per, (b+1)*per) in a fixed thread partition and tree -- a fixed association, so the
+// finalize's total stays bit-reproducible; one block for 2^18 claims took 0.3 ms.
+constexpr int kRedBlocks = 128;
+__global__ void claims_reduce_kernel(const double* __restrict__ claims, int nclaims, double* __restrict__ red) {
+    __shared__ double ss[256];
+    const int per = (nclaims + kRedBlocks - 1) / kRedBlocks;
+    const int b0 = blockIdx.x * per, b1 = min(nclaims, b0 + per);
+    double s = 0.0;
+    for (int q = b0 + threadIdx.x; q < b1; q += blockDim.x) s += claims[q];
+    ss[threadIdx.x] = s;
+    __syncthreads();
+    for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h) ss[threadIdx.x] += ss[threadIdx.x + h];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) red[blockIdx.x] = ss[0];
+}
+
 // Fixed-order sum of the CTA slots and the claim partials into one result record (one
 // block of 256 threads, a fixed partition and tree: the float64 sum is bit-reproducible),
 // and the call's path counters added into the workspace's profile record.
 __global__ void finalize_kernel(const Slot* __restrict__ slots, int nslots, const double* __restrict__ claims,
-                                int nclaims, int claims_hold_sums, const PrepStats* __restrict__ st, int dtype,
+                                int nclaims, int claims_hold_sums, int claims_total, const PrepStats* __restrict__ st,
+                                int dtype,
                                 long long pairs, int direct,
                                 pc_pairs_result* __restrict__ out, pc_pairs_profile* __restrict__ prof,
                                 int kernel_id, long long pairs_per_chunk) {
@@ -500,7 +520,7 @@ __global__ void finalize_kernel(const Slot* __restrict__ slots, int nslots, cons
         prof->chunks_edge += (long long)sp[kPathEdge][0];
         prof->rows_rescanned += (long long)sp[kNumPaths][0];
         prof->exact_checks += (long long)sk[0];
-        prof->claims += nclaims;
+        prof->claims += claims_total;
         prof->pairs += pairs;
         prof->pairs_per_chunk = pairs_per_chunk;
         prof->kernel = kernel_id;
@@ -659,7 +679,7 @@ __global__ void blk_box_kernel(const float* __restrict__ xyz, long long n, int n
 }
 
 struct WsLayout {
-    size_t pts, stats, prof, slots, claims, tc_a, tc_b, tc_cand, tc_cnt, srt, srt_temp, total;
+    size_t pts, stats, prof, red, slots, claims, tc_a, tc_b, tc_cand, tc_cnt, srt, srt_temp, total;
 };
 WsLayout ws_layout(long long n) {
     WsLayout l;
@@ -667,7 +687,8 @@ WsLayout ws_layout(long long n) {
     l.pts = 0;  // even pairs, then odd pairs
     l.stats = 2 * pair_bytes;
     l.prof = l.stats + 256;  // pc_pairs_profile of the last call
-    l.slots = l.prof + 256;
+    l.red = l.prof + 256;    // kRedBlocks float64 partials of the claim sums
+    l.slots = l.red + kRedBlocks * sizeof(double);
     l.claims = align_up(l.slots + (size_t)max_slots(n) * sizeof(Slot), 256);
     l.tc_a = align_up(l.claims + (size_t)kClaimsCap * sizeof(double), 1024);
     const TcGeom g = tc_geom(n < 0 ? 0 : n);  // tensor-core count kernel operands (64 B per staged point)
@@ -895,7 +916,7 @@ int run_pairs_tc(const PairsArgs& p, char* ws, const WsLayout& lay, long long n,
             if (ev) CK(cudaEventRecord(ev->b, s));
             nslots = 2 * grid;
         }
-        finalize_kernel<<<1, 256, 0, s>>>(p.slots, nslots, nullptr, 0, 0, p.st, p.dtype, row_pairs(n, lo, hi, PC_BALANCED),
+        finalize_kernel<<<1, 256, 0, s>>>(p.slots, nslots, nullptr, 0, 0, 0, p.st, p.dtype, row_pairs(n, lo, hi, PC_BALANCED),
                                           0, dres + k, prof, kKernTc, (long long)kTcM * kTcN);
         CK_LAUNCH("finalize_kernel");
     }
@@ -950,7 +971,7 @@ int run_pairs_key(const PairsArgs& p, char* ws, const WsLayout& lay, long long n
             if (ev) CK(cudaEventRecord(ev->b, s));
             nslots = grid;
         }
-        finalize_kernel<<<1, 256, 0, s>>>(p.slots, nslots, nullptr, 0, 0, p.st, p.dtype,
+        finalize_kernel<<<1, 256, 0, s>>>(p.slots, nslots, nullptr, 0, 0, 0, p.st, p.dtype,
                                           row_pairs(n, lo, hi, PC_BALANCED), 0, dres + k, prof, kKernKey,
                                           (long long)T * kKeyW);
         CK_LAUNCH("finalize_kernel");
@@ -1101,7 +1122,16 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
             }
         }
         const long long pr = hi > lo && n >= 2 ? tile_sel_pairs(n, lo, hi, trows, ts, schedule) : 0;
-        finalize_kernel<<<1, 256, 0, s>>>(slots, nslots, claims, nclaims, direct ? 1 : 0, st, dtype, pr,
+        const double* csum = claims;
+        int ncs = nclaims;
+        if (direct && nclaims > 8 * kRedBlocks) {
+            double* red = (double*)(ws + lay.red);
+            claims_reduce_kernel<<<kRedBlocks, 256, 0, s>>>(claims, nclaims, red);
+            CK_LAUNCH("claims_reduce_kernel");
+            csum = red;
+            ncs = kRedBlocks;
+        }
+        finalize_kernel<<<1, 256, 0, s>>>(slots, nslots, csum, ncs, direct ? 1 : 0, nclaims, st, dtype, pr,
                                           direct ? (comp ? 2 : 1) : 0,
                                           dres + k, prof, kern_id, ppc);
         CK_LAUNCH("finalize_kernel");
