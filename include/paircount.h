@@ -80,6 +80,11 @@ extern "C" {
                               packed keys on the INT32 pipe -- points whose bounding box spans
                               <= 1023 per axis; else the result's error is PC_ERR_ARG.  The A/B
                               alternative to the FP32 Gram filter            */
+#define PC_TILE_THREAD_ROW 6 /* the paper's own GPU scheme, literally: one
+                              thread per outer row in 1024-row blocks, columns through shared
+                              memory; with the standard schedule the straightforward kernel
+                              (block- and warp-level imbalance), with the balanced one Alg. 4.
+                              fp32 spheres; a baseline for the naive-vs-balanced comparison   */
 
 typedef struct {
     int64_t count;         /* integer pair count (collisions / coincidences / contacts)           */

@@ -30,6 +30,7 @@ PC_F32, PC_F64, PC_I32, PC_I64 = 0, 1, 2, 3
 PC_STANDARD, PC_BALANCED = 0, 1
 PC_COLLISION, PC_COLLISION_INVSQ, PC_COINCIDE, PC_MANHATTAN1 = 1, 2, 3, 4
 PC_TILE_AUTO, PC_TILE_PER_ROW_TILE, PC_TILE_FLAT, PC_TILE_TC, PC_TILE_SORTED, PC_TILE_KEY = 0, 1, 2, 3, 4, 5
+PC_TILE_THREAD_ROW = 6
 
 SCHEDULE_CODES = {"standard": PC_STANDARD, "balanced": PC_BALANCED}
 DTYPE_CODES = {np.dtype(np.float32): PC_F32, np.dtype(np.float64): PC_F64,

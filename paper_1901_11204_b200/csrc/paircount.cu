@@ -393,7 +393,8 @@ struct Slot {
 };
 static_assert(sizeof(Slot) == 64, "Slot is one 64-byte record");
 // kernel ids recorded in pc_pairs_profile.kernel
-constexpr int kKernGram = 1, kKernDirect = 2, kKernSorted = 3, kKernComp = 4, kKernTc = 5, kKernKey = 6;
+constexpr int kKernGram = 1, kKernDirect = 2, kKernSorted = 3, kKernComp = 4, kKernTc = 5, kKernKey = 6,
+              kKernRow = 7;
 
 // FLAT work claims (guided self-scheduling): claim c of stage k covers columns
 // [b0[k] + (c - c0[k]) * s[k], + s[k]) of the flat (row tile, window column) space.  Stage k
@@ -446,6 +447,7 @@ __device__ __forceinline__ int steps_for_dev(int n, int i) {
 #include "pairs_kernel.cuh"
 #include "pairs_tc.cuh"
 #include "pairs_key.cuh"
+#include "pairs_row.cuh"
 
 // First stage of the claim-sum reduction for large claim counts: block b adds claims
 // [b*per, (b+1)*per) in a fixed thread partition and tree -- a fixed association, so the
@@ -1004,11 +1006,15 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
                                                   n < kTcMaxN && rows * 8 >= n));
     const bool auto_tiling = tiling == PC_TILE_AUTO, sorted_req = tiling == PC_TILE_SORTED;
     const bool use_key = tiling == PC_TILE_KEY;
+    const bool use_row = tiling == PC_TILE_THREAD_ROW;
+    if (use_row && (dtype != PC_F32 || (interaction != PC_COLLISION && interaction != PC_COLLISION_INVSQ) ||
+                    ts.tstride != 1))
+        return arg_fail("PC_TILE_THREAD_ROW needs fp32 spheres (collision count or inverse-square sum), no tile parts");
     if (use_key && (interaction != PC_COINCIDE || schedule != PC_BALANCED || ts.tstride != 1))
         return arg_fail("PC_TILE_KEY needs the coincidence count, the balanced schedule and no tile parts");
     if (sorted_req && (interaction != PC_COLLISION_INVSQ || dtype != PC_F32 || schedule != PC_BALANCED))
         return arg_fail("PC_TILE_SORTED needs the inverse-square sum on fp32 points and the balanced schedule");
-    if (tiling == PC_TILE_AUTO || tiling == PC_TILE_TC || tiling == PC_TILE_SORTED || use_key)
+    if (tiling == PC_TILE_AUTO || tiling == PC_TILE_TC || tiling == PC_TILE_SORTED || use_key || use_row)
         tiling = schedule == PC_BALANCED ? PC_TILE_FLAT : PC_TILE_PER_ROW_TILE;
     if (tiling == PC_TILE_FLAT && schedule != PC_BALANCED)
         return arg_fail("PC_TILE_FLAT needs the balanced schedule (equal windows per row tile)");
@@ -1087,6 +1093,46 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     const long long cap = max_slots(n);
     if (use_tc) return run_pairs_tc(args, ws, lay, n, cap, nranges, bounds, dres, prof, s);
     if (use_key) return run_pairs_key(args, ws, lay, n, cap, nranges, bounds, dres, prof, s);
+    if (use_row) {  // the paper's thread-per-row schemes (pairs_row.cuh), a baseline
+        for (int k = 0; k < nranges; ++k) {
+            const long long lo = bounds[k], hi = bounds[k + 1];
+            int nslots = 0;
+            if (hi > lo && n >= 2) {
+                args.lo = (int)lo;
+                args.hi = (int)hi;
+                const int grid = (int)((hi - lo + kRowThreads - 1) / kRowThreads);
+                if (grid + num_sms() * 4 > cap) return arg_fail("workspace too small for the CTA slots");
+                EvPair* ev = nullptr;
+                if (g_timing && g_ev_used < 4096) {
+                    if (g_ev_used == g_ev_made) {
+                        CK(cudaEventCreate(&g_ev[g_ev_made].a));
+                        CK(cudaEventCreate(&g_ev[g_ev_made].b));
+                        ++g_ev_made;
+                    }
+                    ev = &g_ev[g_ev_used++];
+                    CK(cudaEventRecord(ev->a, s));
+                }
+                pairs_row_kernel<<<grid, kRowThreads, 0, s>>>(args, direct ? 1 : 0);
+                CK_LAUNCH("pairs_row_kernel");
+                if (ev) CK(cudaEventRecord(ev->b, s));
+                nslots = grid;
+                if (direct) {
+                    args.tstride = 1;
+                    args.toff = 0;
+                    args.tile_rows = kRowThreads;
+                    const int g2 = (int)std::min<long long>((hi - lo + 255) / 256, (long long)num_sms() * 4);
+                    pairs_f64_kernel<<<g2, 256, 0, s>>>(args, 0, slots + nslots);
+                    CK_LAUNCH("pairs_f64_kernel");
+                    nslots += g2;
+                }
+            }
+            finalize_kernel<<<1, 256, 0, s>>>(slots, nslots, nullptr, 0, 0, 0, st, dtype,
+                                              row_pairs(n, lo, hi, schedule), direct ? 1 : 0, dres + k, prof,
+                                              kKernRow, 0);
+            CK_LAUNCH("finalize_kernel");
+        }
+        return PC_OK;
+    }
     const int kern_id = !direct ? kKernGram : comp ? kKernComp : sorted ? kKernSorted : kKernDirect;
     for (int k = 0; k < nranges; ++k) {
         const long long lo = bounds[k], hi = bounds[k + 1];

@@ -525,7 +525,13 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 // inequality 5u (..)^2 <= 2e-6 (..): eight roundings of terms of at most
                 // (|a| + |b|)^2 against p >= 1 + dmin^2
                 const float ab = sqrtf(rt2) + sqrtf(bm2);
-                gram = gap2 > 4.5f && 2.98023223876953125e-07f * ab * ab <= 2e-6f * (1.f + gap2);
+#ifndef PC_GRAM_BUDGET
+#define PC_GRAM_BUDGET 2e-6f
+#endif
+#ifndef PC_GRAM_GAP2
+#define PC_GRAM_GAP2 4.5f
+#endif
+                gram = gap2 > PC_GRAM_GAP2 && 2.98023223876953125e-07f * ab * ab <= PC_GRAM_BUDGET * (1.f + gap2);
                 // boxes more than 1.5 apart: no contact, so no rescan however large the chunk's
                 // sums (on sorted points the chunks next to a tile have many near terms)
                 no_contact = gap2 > 2.25f;

@@ -223,3 +223,24 @@ def test_int32_key_span_limits():
     assert _lib.last_profile().kernel != 6
     with pytest.raises(ValueError, match="PC_TILE_KEY"):
         _lib.pairs_host(base, _lib.PC_MANHATTAN1, _lib.PC_BALANCED, [0, 5000], tiling=_lib.PC_TILE_KEY)
+
+
+@pytest.mark.parametrize("n", [2, 3, 1023, 1024, 1025, 5000, 20001])
+def test_paper_thread_row_schemes(n):
+    """PC_TILE_THREAD_ROW: the paper's thread-per-row kernels (standard = the
+    straightforward scheme, balanced = Alg. 4) against the oracle, whole range
+    and row ranges, counts exact and sums within 1e-6."""
+    x = _spheres(n, 12, scale=0.8)
+    for sched in ("standard", "balanced"):
+        for b in ([0, n], [0, n // 3, n - n // 4, n]):
+            for inter in (_lib.PC_COLLISION, _lib.PC_COLLISION_INVSQ):
+                rs = _lib.pairs_host(x, inter, _lib.SCHEDULE_CODES[sched], b, tiling=_lib.PC_TILE_THREAD_ROW)
+                for (lo, hi), r in zip(zip(b[:-1], b[1:]), rs):
+                    c, s, p = c_oracle.rows(x, lo, hi, sched)
+                    assert r.error == 0 and r.count == c and r.pairs == p, (sched, lo, hi, inter)
+                    if inter == _lib.PC_COLLISION_INVSQ and p:
+                        assert abs(r.sum - s) <= 1e-6 * s
+    assert _lib.last_profile().kernel == 7
+    with pytest.raises(ValueError, match="THREAD_ROW"):
+        _lib.pairs_host(x.astype(np.float64), _lib.PC_COLLISION, _lib.PC_BALANCED, [0, n],
+                        tiling=_lib.PC_TILE_THREAD_ROW)
