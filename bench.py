@@ -365,22 +365,38 @@ def secondary(torch, lib, stream):
         return ms / cnt, e0.elapsed_time(e1) / reps, int(res[0].item()), int(res[3].item())
 
     k_ffma, dev_ffma, count_ffma, checks_ffma = count_leg(_lib.PC_TILE_FLAT)
-    k_tc, dev_tc, count_tc, checks_tc = count_leg(_lib.PC_TILE_AUTO)  # 2^20: the tensor-core kernel
+    k_tc, dev_tc, count_tc, checks_tc = count_leg(_lib.PC_TILE_TC)
+    k_pr, dev_pr, count_pr, checks_pr = count_leg(_lib.PC_TILE_AUTO)  # whole range fp32: pruned sorted count
+    prof_pr = _lib.profile_read(ws3.data_ptr(), n3, stream.cuda_stream)
+    chunks_pr = (prof_pr.chunks_gram + prof_pr.chunks_main + prof_pr.chunks_near + prof_pr.chunks_far +
+                 prof_pr.chunks_edge)
+    evaluated_cells = (chunks_pr - prof_pr.chunks_far) * prof_pr.pairs_per_chunk
     t0 = time.perf_counter()
     r3 = se.spi_balanced(obj3, se.collision_indicator)
     api_ms = (time.perf_counter() - t0) * 1e3
     out["cfg3_collision_count_n2^20"] = {
-        "count": count_tc, "api_count": int(r3.total), "ffma_count": count_ffma,
+        "count": count_tc, "api_count": int(r3.total), "ffma_count": count_ffma, "pruned_count": count_pr,
         "kernel_ms": k_tc, "device_ms_per_call": dev_tc, "exact_checks": checks_tc,
         "Gpair_per_s_kernel": pairs3 / (k_tc * 1e-3) / 1e9,
-        "api_wall_ms": api_ms,
-        "api_path": "spi_balanced(points, collision_indicator): numpy (n,3) f32 -> ctypes pc_pairs_host "
-                    "(H2D, prep, tensor-core Gram filter, exact pass, finalize, D2H) -> SpiResult",
         "kernel": "pairs_tc_kernel (tcgen05.mma kind::tf32, 3xTF32 Gram filter, TMEM drained by 8 warps) + "
-                  "tc_exact_kernel",
+                  "tc_exact_kernel: every pair evaluated",
         "ffma_kernel": "pairs_kernel<128,12,192,GRAM,FLAT>", "ffma_kernel_ms": k_ffma,
         "ffma_device_ms_per_call": dev_ffma, "ffma_exact_checks": checks_ffma,
-        "ffma_Gpair_per_s_kernel": pairs3 / (k_ffma * 1e-3) / 1e9}
+        "ffma_Gpair_per_s_kernel": pairs3 / (k_ffma * 1e-3) / 1e9,
+        "pruned_sorted": {
+            "kernel": "pairs_kernel<128,12,192,GRAM,FLAT,SORTED>: Morton-sorted points, claims and chunks whose "
+                      "bounding boxes are beyond contact distance of the tile decided without evaluation "
+                      "(PAPER.md:443: the all-pairs count composed with pruning); PC_TILE_AUTO for whole-range "
+                      "fp32 counts from 2^15 points",
+            "kernel_ms": k_pr, "device_ms_per_call": dev_pr, "count": count_pr, "exact_checks": checks_pr,
+            "pairs_decided_by_boxes_not_evaluated": int(pairs3 - min(pairs3, evaluated_cells)),
+            "pair_cells_evaluated": int(evaluated_cells),
+            "evaluated_Gpair_per_s": evaluated_cells / (k_pr * 1e-3) / 1e9,
+            "note": "not a pair-test rate: most pairs are decided by their boxes, reported apart"},
+        "api_wall_ms": api_ms,
+        "api_path": "spi_balanced(points, collision_indicator): numpy (n,3) f32 -> ctypes pc_pairs_host "
+                    "(H2D, bbox, Morton sort, pruned Gram count, exact re-checks, finalize, D2H) -> SpiResult",
+    }
     ms_k, cnt_k = k_ffma, 1  # the naive comparison below is against the same FFMA inner code
     # the paper's comparison in its large-N regime (N > 525,000): the straightforward
     # scheme (standard schedule, one warp per row tile) on the same inner code
@@ -528,7 +544,19 @@ def secondary(torch, lib, stream):
     c4["Gpair_per_s_1gpu"] = pairs4 / (c4["kernel_ms_1gpu"] * 1e-3) / 1e9
     s4 = split_legs(d4, n4, ws4, res4, _lib.PC_COLLISION_INVSQ, _lib.PC_TILE_SORTED)
     s4["Gpair_per_s_1gpu"] = pairs4 / (s4["kernel_ms_1gpu"] * 1e-3) / 1e9
-    out["cfg4_clustered_n2^22"] = {"count_ffma_gram": c4, "count_plus_sum_sorted": s4}
+    _lib.kernel_timing(True)
+    for _ in range(2):
+        _lib.pairs_async(d4.data_ptr(), _lib.PC_F32, n4, _lib.PC_COLLISION, _lib.PC_BALANCED, np.array([0, n4]),
+                         ws4.data_ptr(), ws4.numel(), res4.data_ptr(), stream.cuda_stream, _lib.PC_TILE_AUTO)
+    ms_p4, cnt_p4 = _lib.kernel_timing_read()
+    _lib.kernel_timing(False)
+    torch.cuda.synchronize()
+    prof4 = _lib.profile_read(ws4.data_ptr(), n4, stream.cuda_stream)
+    tot4 = prof4.chunks_gram + prof4.chunks_main + prof4.chunks_near + prof4.chunks_far + prof4.chunks_edge
+    p4 = {"kernel_ms": ms_p4 / cnt_p4, "count": int(res4[0].item()), "exact_checks": int(res4[3].item()),
+          "chunks_decided_by_boxes": prof4.chunks_far, "chunks_total": tot4,
+          "note": "pruned sorted count (PC_TILE_AUTO): pairs decided by their boxes are not evaluated"}
+    out["cfg4_clustered_n2^22"] = {"count_ffma_gram": c4, "count_plus_sum_sorted": s4, "count_pruned_sorted": p4}
     del d4, ws4
 
     # ---- many small vectors: the paper's setting (1000 chain vectors per execution)

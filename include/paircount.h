@@ -71,11 +71,14 @@ extern "C" {
                               re-check); counts only, balanced schedule, any row ranges.
                               PC_TILE_AUTO picks it when 2^14 <= n < 2^21 and the ranges
                               cover at least n/8 rows                                          */
-#define PC_TILE_SORTED 4   /* the inverse-square sum on spatially sorted fp32 points (what
-                              PC_TILE_AUTO does for a whole-range call from 2^15 points): row
-                              ranges then index the SORTED order, so each range's result is a
-                              partial of the same total (multi-GPU slabs), not the reference's
-                              _run_outer over those input rows                                 */
+#define PC_TILE_SORTED 4   /* fp32 spheres on spatially (Morton) sorted points -- what
+                              PC_TILE_AUTO does for a whole-range call from 2^15 points: the
+                              inverse-square sum with far chunks in tile-local Gram form, and
+                              the contact count with box pruning (chunks beyond contact distance
+                              of the tile are decided by their boxes, not evaluated; reported in
+                              pc_pairs_profile.chunks_far).  Row ranges then index the SORTED
+                              order, so each range's result is a partial of the same total
+                              (multi-GPU slabs), not the reference's _run_outer over those rows */
 #define PC_TILE_KEY 5      /* exact coincidence counts (PC_COINCIDE, balanced) by comparing 30-bit
                               packed keys on the INT32 pipe -- points whose bounding box spans
                               <= 1023 per axis; else the result's error is PC_ERR_ARG.  The A/B
@@ -104,14 +107,16 @@ typedef struct {
     int64_t chunks_gram;     /* sum on sorted points, tile-local Gram form            */
     int64_t chunks_main;     /* unmasked main loop (direct sum / Gram count filter)    */
     int64_t chunks_near;     /* sorted sum, direct formula + per-row contact minimum   */
-    int64_t chunks_far;      /* sorted sum, direct formula, no contact test needed     */
+    int64_t chunks_far;      /* sorted sum: direct formula, no contact test needed;
+                                sorted count: chunks decided by their boxes (not evaluated) */
     int64_t chunks_edge;     /* masked per-pair chunks                                 */
     int64_t rows_rescanned;  /* flagged (row, chunk) re-tests by the slow path         */
     int64_t exact_checks;    /* pairs re-evaluated by the exact predicate              */
     int64_t claims;          /* FLAT work claims (float64 partial slots)               */
     int64_t pairs;           /* pairs owned by the call's rows                         */
     int64_t pairs_per_chunk; /* T x W of the kernel (0: tensor-core or no kernel)      */
-    int32_t kernel;          /* 1 Gram count, 2 direct sum, 3 sorted sum, 4 compensated sum, 5 tensor-core count */
+    int32_t kernel;          /* 1 Gram count, 2 direct sum, 3 sorted sum, 4 compensated sum, 5 tensor-core
+                                count, 6 INT32 key count, 7 thread-per-row (paper), 8 pruned sorted count */
     int32_t f64_taken;       /* 1: the float64 kernel evaluated the sum (non-finite / huge / wide input) */
 } pc_pairs_profile;
 

@@ -394,7 +394,7 @@ struct Slot {
 static_assert(sizeof(Slot) == 64, "Slot is one 64-byte record");
 // kernel ids recorded in pc_pairs_profile.kernel
 constexpr int kKernGram = 1, kKernDirect = 2, kKernSorted = 3, kKernComp = 4, kKernTc = 5, kKernKey = 6,
-              kKernRow = 7;
+              kKernRow = 7, kKernSortedCount = 8;
 
 // FLAT work claims (guided self-scheduling): claim c of stage k covers columns
 // [b0[k] + (c - c0[k]) * s[k], + s[k]) of the flat (row tile, window column) space.  Stage k
@@ -427,7 +427,8 @@ struct PairsArgs {
     int n_tiles;        // row tiles in [lo, hi)
     long long L;        // FLAT: window length shared by every row tile
     long long total;    // FLAT: n_tiles * L
-    const float4* blk_box;  // SORTED: per-32-point bounding boxes (min, max) of the sorted points
+    const float4* blk_box;   // SORTED: per-32-point bounding boxes (min, max) of the sorted points
+    const float4* blk2_box;  // SORTED count: per-1024-point boxes
     int nblk;
     int tstride, toff;   // row tiles of this call: toff, toff + tstride, ... (pc_pairs_part_async)
     int tile_rows;       // T of the launched kernel (the float64 kernel follows the same tiles)
@@ -598,6 +599,9 @@ constexpr KernelCfg kBig{4, PC_BIG_R, PC_BIG_W};  // direct (sum) kernel: warp t
 #ifndef PC_SORTED_SUM
 #define PC_SORTED_SUM 1  // whole-range fp32 balanced sums: spatial sort + tile-local Gram chunks
 #endif
+#ifndef PC_SORTED_COUNT
+#define PC_SORTED_COUNT 1  // whole-range fp32 balanced contact counts: spatial sort + box pruning
+#endif
 #ifndef PC_TC_AUTO
 #define PC_TC_AUTO 1  // balanced counts with kTcMinN <= n < kTcMaxN (rows >= n/8) take the tensor-core kernel
 #endif
@@ -663,6 +667,19 @@ __global__ void gather_sorted_kernel(const float* __restrict__ xyz, const unsign
         out[3 * i + 2] = xyz[3 * s + 2];
     }
 }
+// one thread per 1024-point block: the union of its 32 per-32-point boxes
+__global__ void blk2_box_kernel(const float4* __restrict__ box, int nblk, int nblk2, float4* __restrict__ box2) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nblk2; b += gridDim.x * blockDim.x) {
+        float4 lo = make_float4(INFINITY, INFINITY, INFINITY, 0.f), hi = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.f);
+        for (int q = 32 * b; q < min(nblk, 32 * b + 32); ++q) {
+            const float4 l = box[2 * q], h = box[2 * q + 1];
+            lo = make_float4(fminf(lo.x, l.x), fminf(lo.y, l.y), fminf(lo.z, l.z), 0.f);
+            hi = make_float4(fmaxf(hi.x, h.x), fmaxf(hi.y, h.y), fmaxf(hi.z, h.z), 0.f);
+        }
+        box2[2 * b] = lo;
+        box2[2 * b + 1] = hi;
+    }
+}
 // one thread per 32-point block: (min x, y, z, 0), (max x, y, z, 0)
 __global__ void blk_box_kernel(const float* __restrict__ xyz, long long n, int nblk, float4* __restrict__ box) {
     for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nblk; b += (long long)gridDim.x * blockDim.x) {
@@ -702,7 +719,7 @@ WsLayout ws_layout(long long n) {
     l.srt = align_up(l.tc_cnt + 4 * 1024, 256);
     const size_t nn = (size_t)(n < 0 ? 0 : n);
     l.srt_temp = align_up(l.srt + 4 * align_up(nn * 4, 256) + align_up(nn * 12, 256) +
-                          align_up((nn / 32 + 1) * 32, 256), 256);
+                          align_up((nn / 32 + 1) * 32, 256) + align_up((nn / 1024 + 1) * 32, 256), 256);
     l.total = align_up(l.srt_temp + kSortTempBytes(nn), 256);
     return l;
 }
@@ -1001,7 +1018,10 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     long long rows = 0;  // AUTO: ranges of a few tiles stay on the FFMA kernel (the staging is per call)
     for (int k = 0; k < nranges; ++k) rows += std::max(0LL, (long long)(bounds[k + 1] - bounds[k]));
     if (tiling == PC_TILE_TC && ts.tstride != 1) return arg_fail("PC_TILE_TC does not take tile parts");
-    const bool use_tc = tc_ok && ts.tstride == 1 &&
+    const bool whole = nranges == 1 && bounds[0] == 0 && bounds[1] == n;
+    const bool prune_auto = PC_SORTED_COUNT && tiling == PC_TILE_AUTO && whole && interaction == PC_COLLISION &&
+                            dtype == PC_F32 && schedule == PC_BALANCED && n >= kSortedMinN;
+    const bool use_tc = tc_ok && ts.tstride == 1 && !prune_auto &&
                         (tiling == PC_TILE_TC || (tiling == PC_TILE_AUTO && PC_TC_AUTO && n >= kTcMinN &&
                                                   n < kTcMaxN && rows * 8 >= n));
     const bool auto_tiling = tiling == PC_TILE_AUTO, sorted_req = tiling == PC_TILE_SORTED;
@@ -1012,8 +1032,10 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
         return arg_fail("PC_TILE_THREAD_ROW needs fp32 spheres (collision count or inverse-square sum), no tile parts");
     if (use_key && (interaction != PC_COINCIDE || schedule != PC_BALANCED || ts.tstride != 1))
         return arg_fail("PC_TILE_KEY needs the coincidence count, the balanced schedule and no tile parts");
-    if (sorted_req && (interaction != PC_COLLISION_INVSQ || dtype != PC_F32 || schedule != PC_BALANCED))
-        return arg_fail("PC_TILE_SORTED needs the inverse-square sum on fp32 points and the balanced schedule");
+    if (sorted_req && ((interaction != PC_COLLISION_INVSQ && interaction != PC_COLLISION) || dtype != PC_F32 ||
+                       schedule != PC_BALANCED))
+        return arg_fail("PC_TILE_SORTED needs fp32 spheres (inverse-square sum or contact count) and the balanced "
+                        "schedule");
     if (tiling == PC_TILE_AUTO || tiling == PC_TILE_TC || tiling == PC_TILE_SORTED || use_key || use_row)
         tiling = schedule == PC_BALANCED ? PC_TILE_FLAT : PC_TILE_PER_ROW_TILE;
     if (tiling == PC_TILE_FLAT && schedule != PC_BALANCED)
@@ -1041,13 +1063,18 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     const bool whole_range = nranges == 1 && bounds[0] == 0 && bounds[1] == n;
     const bool sorted = PC_SORTED_SUM && direct && !comp && schedule == PC_BALANCED && n >= kSortedMinN &&
                         ((auto_tiling && whole_range) || sorted_req);
+    // whole-range fp32 contact counts: the same sort, then the Gram count with box pruning (pairs_kernel.cuh)
+    const bool sorted_count = PC_SORTED_COUNT && interaction == PC_COLLISION && dtype == PC_F32 &&
+                              schedule == PC_BALANCED && n >= kSortedMinN && ts.tstride >= 1 &&
+                              ((auto_tiling && whole_range) || sorted_req);
     const float4* blk_box = nullptr;
+    const float4* blk2_box = nullptr;
     const int nblk = (int)((n + 31) / 32);
     if (n > 0) {
         const int blocks = (int)std::min<long long>((n + 255) / 256, (long long)num_sms() * 8);
         prep_bbox_kernel<<<blocks, 256, 0, s>>>(xyz, dtype, n, st);
         CK_LAUNCH("prep_bbox_kernel");
-        if (sorted) {
+        if (sorted || sorted_count) {
             const size_t kb = align_up((size_t)n * 4, 256);
             unsigned* k0 = (unsigned*)(ws + lay.srt);
             unsigned* k1 = (unsigned*)(ws + lay.srt + kb);
@@ -1067,6 +1094,15 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
             CK_LAUNCH("gather_sorted_kernel");
             blk_box_kernel<<<(nblk + 255) / 256, 256, 0, s>>>(xs, n, nblk, box);
             CK_LAUNCH("blk_box_kernel");
+            if (sorted_count) {
+                float4* box2 = box + 2 * (size_t)nblk;  // (n/32+1)*32 B reserved for box, then box2
+                box2 = (float4*)(ws + lay.srt + 4 * kb + align_up((size_t)n * 12, 256) +
+                                 align_up((size_t)(n / 32 + 1) * 32, 256));
+                const int nblk2 = (int)((n + 1023) / 1024);
+                blk2_box_kernel<<<(nblk2 + 255) / 256, 256, 0, s>>>(box, nblk, nblk2, box2);
+                CK_LAUNCH("blk2_box_kernel");
+                blk2_box = box2;
+            }
             xyz = xs;  // from here on the call works on the sorted points
             blk_box = box;
         }
@@ -1081,6 +1117,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     args.xyz = xyz;
     args.st = st;
     args.blk_box = blk_box;
+    args.blk2_box = blk2_box;
     args.nblk = nblk;
     args.slots = slots;
     args.claim_sums = claims;
@@ -1133,7 +1170,8 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
         }
         return PC_OK;
     }
-    const int kern_id = !direct ? kKernGram : comp ? kKernComp : sorted ? kKernSorted : kKernDirect;
+    const int kern_id = !direct ? (sorted_count ? kKernSortedCount : kKernGram)
+                                : comp ? kKernComp : sorted ? kKernSorted : kKernDirect;
     for (int k = 0; k < nranges; ++k) {
         const long long lo = bounds[k], hi = bounds[k + 1];
         int nslots = 0, nclaims = 0, trows = 1;
@@ -1153,6 +1191,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
                 rc = comp     ? PC_DISPATCH(kBigComp, true, true)
                      : sorted ? PC_DISPATCH(kBig, true, false, true)
                      : direct ? PC_DISPATCH(kBig, true)
+                     : sorted_count ? PC_DISPATCH(kBigGram, false, false, true)
                               : PC_DISPATCH(kBigGram, false);
 #undef PC_DISPATCH
             if (rc) return rc;

@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     // chunks per inner loop (kPath*) + rescanned rows, and the claim ids of the current / next chunk
     __shared__ unsigned s_path[WARPS][kNumPaths + 1];
     __shared__ long long s_claim[WARPS][2];
+    __shared__ float s_tbox[WARPS][6];  // SORTED count: the claimed tile's box (min xyz, max xyz), raw coordinates
     __shared__ __align__(8) unsigned long long s_bar[WARPS][2];  // per-warp TMA completion, one per column buffer
     __shared__ double s_sum[WARPS];
 
@@ -190,6 +191,67 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     // handed out before any far block, and the tail is uniform far work.  A claim never crosses a block
     // (stage sizes are powers of two dividing the block); one that falls past a window's end is
     // empty and skipped.
+    auto count_path = [&](int k, unsigned v) {
+#ifndef PC_NO_PATHS
+        if (lane == 0) s_path[wid][k] += v;
+#endif
+    };
+    // SORTED count (pruning, PAPER.md:443 -- the all-pairs count composed with a box test): the
+    // union box of sorted points [j, j + cnt) (mod n) from the per-32 (lvl 1) or per-1024 (lvl 2)
+    // boxes against the claimed tile's box; a gap beyond the contact distance decides every pair
+    // of the range (no contact) without evaluating it -- counted apart (kPathFar), never as
+    // evaluated pairs.
+    const float cull_gap2 = a.thr * 1.0001f;
+    auto union_far = [&](long long j, long long cnt, const float4* box, int shift) -> bool {
+        long long ja = j >= n ? j - n : j;
+        const long long je = ja + cnt - 1;  // last column before wrapping
+        const int b0 = (int)(ja >> shift), b1 = (int)(min(je, (long long)n - 1) >> shift);
+        const int nb1 = b1 - b0 + 1, nb2 = je >= n ? (int)((je - n) >> shift) + 1 : 0;
+        float g2 = 0.f;
+        for (int base = 0; base < nb1 + nb2; base += 32) {  // chunks: <= 8 boxes; claims: a few dozen
+            float cmn[3] = {INFINITY, INFINITY, INFINITY}, cmx[3] = {-INFINITY, -INFINITY, -INFINITY};
+            const int q = base + lane;
+            if (q < nb1 + nb2) {
+                const int b = q < nb1 ? b0 + q : q - nb1;
+                const float4 lo4 = box[2 * b], hi4 = box[2 * b + 1];
+                cmn[0] = lo4.x; cmn[1] = lo4.y; cmn[2] = lo4.z;
+                cmx[0] = hi4.x; cmx[1] = hi4.y; cmx[2] = hi4.z;
+            }
+            float gg = 0.f;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const float cl = warp_min_f(cmn[k]), ch = warp_max_f(cmx[k]);
+                const float gk = fmaxf(0.f, fmaxf(cl - s_tbox[wid][3 + k], s_tbox[wid][k] - ch));
+                gg += gk * gk;
+            }
+            if (base == 0) g2 = gg;
+            else g2 = fminf(g2, gg);  // a union over several passes: the nearest part decides
+        }
+        return g2 > cull_gap2;
+    };
+    auto tile_box = [&](int tt) {  // the rows of tile tt from the per-32 boxes
+        const int i0t = a.lo + (tt * a.tstride + a.toff) * T;
+        const int i1t = min(i0t + T, a.hi) - 1;
+        const int b0 = i0t >> 5, nb = (i1t >> 5) - b0 + 1;
+        float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+        if (lane < nb) {
+            const float4 lo4 = a.blk_box[2 * (b0 + lane)], hi4 = a.blk_box[2 * (b0 + lane) + 1];
+            mn[0] = lo4.x; mn[1] = lo4.y; mn[2] = lo4.z;
+            mx[0] = hi4.x; mx[1] = hi4.y; mx[2] = hi4.z;
+        }
+        float v[6];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            v[k] = warp_min_f(mn[k]);
+            v[3 + k] = warp_max_f(mx[k]);
+        }
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 6; ++k) s_tbox[wid][k] = v[k];
+        }
+        __syncwarp();
+    };
     auto claim = [&](int& t, int& o, long long& lft) {
         for (;;) {
             unsigned long long c = 0;
@@ -209,6 +271,14 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             const long long oo = ob * a.blk_cols + (v - blk * a.blk_cols);
             const long long len = min(a.st_s[k], (long long)L - oo);
             if (len <= 0) continue;  // past the end of the window
+            if (SORTED && !DIRECT) {
+                tile_box(tt);
+                const long long jc = (long long)a.lo + ((long long)tt * a.tstride + a.toff) * T + oo + 1;
+                if (union_far(jc, len, a.blk2_box, 10)) {
+                    count_path(kPathFar, (unsigned)((len + W - 1) / W));
+                    continue;  // every pair of the claim decided by its boxes
+                }
+            }
             if (lane == 0) s_claim[wid][1] = (long long)c;  // the next chunk's claim
             t = tt;
             o = (int)oo;
@@ -301,11 +371,6 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     unsigned valid_rows = 0;
     unsigned long long cnt = 0, checks = 0;
     double sum = 0.0;
-    auto count_path = [&](int k, unsigned v) {
-#ifndef PC_NO_PATHS
-        if (lane == 0) s_path[wid][k] += v;
-#endif
-    };
 
     // Staging of chunk (t, o, wcn) into column buffer b, with the tile's rows when asked.  A full
     // chunk whose window does not wrap is ONE contiguous run of pair entries, and a whole row tile
@@ -401,7 +466,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 rc[r] = ok ? (force ? -INFINITY : -v.w - half_tb) : INFINITY;
                 valid_rows |= (ok ? 1u : 0u) << r;
             }
-            if (SORTED) {
+            if (SORTED && DIRECT) {
                 float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
@@ -420,6 +485,10 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             __syncwarp();  // the row buffer may be restaged below
         }
 
+        // SORTED count: is this chunk beyond contact distance of its tile?  (decided before the next
+        // claim, which may load the next tile's box)
+        bool chunk_far = false;
+        if (SORTED && !DIRECT) chunk_far = union_far((long long)i0 + off + 1, wc, a.blk_box, 5);
         // next chunk's coordinates (incremental: no divisions in the loop); stage it now
         int ntile = tile, noff = off + wc;
         if (noff == L) {
@@ -454,8 +523,10 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             float m[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) m[r] = -INFINITY;
-            count_path(off + 1 >= T ? kPathMain : kPathEdge, 1u);
-            if (off + 1 >= T) {
+            count_path(chunk_far ? kPathFar : off + 1 >= T ? kPathMain : kPathEdge, 1u);
+            if (chunk_far) {
+                // no pair of this chunk can be in contact: nothing to evaluate
+            } else if (off + 1 >= T) {
                 // ---- Gram filter, packed: 3 FFMA2 + 1 FMNMX3 per two pairs.  Unowned
                 // cells past a row's window only cost a rescan if they are contacts.
 #pragma unroll kGramUnroll

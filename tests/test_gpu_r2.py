@@ -69,7 +69,8 @@ def test_profile_accounts_for_every_pair():
     for n, tiling, inter, kern in ((70000, _lib.PC_TILE_AUTO, _lib.PC_COLLISION_INVSQ, 3),
                                    (70000, _lib.PC_TILE_FLAT, _lib.PC_COLLISION_INVSQ, 2),
                                    (70000, _lib.PC_TILE_FLAT, _lib.PC_COLLISION, 1),
-                                   (70000, _lib.PC_TILE_AUTO, _lib.PC_COLLISION, 5),
+                                   (70000, _lib.PC_TILE_TC, _lib.PC_COLLISION, 5),
+                                   (70000, _lib.PC_TILE_AUTO, _lib.PC_COLLISION, 8),
                                    (9000, _lib.PC_TILE_PER_ROW_TILE, _lib.PC_COLLISION, 1)):
         x = _spheres(n, 3)
         (r,) = _lib.pairs_host(x, inter, _lib.PC_BALANCED, [0, n], tiling=tiling)
@@ -83,6 +84,8 @@ def test_profile_accounts_for_every_pair():
         assert (prof.claims > 0) == (tiling != _lib.PC_TILE_PER_ROW_TILE)
         if kern == 3:
             assert prof.chunks_gram > 0 and prof.chunks_near > 0
+        if kern == 8:  # pruned sorted count: most chunks decided by their boxes
+            assert prof.chunks_far > 0.5 * chunks
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64, np.int64])
@@ -244,3 +247,33 @@ def test_paper_thread_row_schemes(n):
     with pytest.raises(ValueError, match="THREAD_ROW"):
         _lib.pairs_host(x.astype(np.float64), _lib.PC_COLLISION, _lib.PC_BALANCED, [0, n],
                         tiling=_lib.PC_TILE_THREAD_ROW)
+
+
+@pytest.mark.parametrize("n", [32768, 40001, 65537])
+def test_pruned_sorted_count(n):
+    """Whole-range fp32 contact counts (spi_balanced / PC_TILE_AUTO) run on Morton-sorted
+    points with box pruning: exact against the oracle on distributions that stress the
+    box test (contacts at exactly distance 1 on a lattice, dense clusters, far-apart
+    clusters, a thin slab); the profile reports the pruned chunks apart."""
+    rng = np.random.default_rng(n)
+    box = (4.18879 * n) ** (1 / 3)
+    lat = rng.integers(0, int(box) + 1, size=(n, 3)).astype(np.float32)
+    cent = rng.random((64, 3)) * box * 2
+    cases = {
+        "uniform": _spheres(n, 3),
+        "lattice (d = 1 exactly)": lat,
+        "clustered": (cent[rng.integers(0, 64, n)] + rng.normal(size=(n, 3))).astype(np.float32),
+        "two far clusters": np.concatenate([rng.random((n // 2, 3)) * 12, rng.random((n - n // 2, 3)) * 12 + 1e4]
+                                           ).astype(np.float32),
+        "thin slab": (rng.random((n, 3)) * np.array([box * 6, box * 6, 0.8])).astype(np.float32),
+    }
+    for name, x in cases.items():
+        want = c_oracle.rows(x, 0, n, "balanced")[0]
+        assert se.spi_balanced(x, se.collision_indicator).total == want, name
+        prof = _lib.last_profile()
+        assert prof.kernel == 8 and prof.chunks_far > 0, name
+        (r,) = _lib.pairs_host(x, _lib.PC_COLLISION, _lib.PC_BALANCED, [0, n], tiling=_lib.PC_TILE_SORTED)
+        assert r.count == want, name
+        parts = [_lib.pairs_part_host(x, _lib.PC_COLLISION, _lib.PC_BALANCED, 0, n, k, 3, _lib.PC_TILE_SORTED)
+                 for k in range(3)]
+        assert sum(q.count for q in parts) == want, name

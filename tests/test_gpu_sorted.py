@@ -69,11 +69,15 @@ def test_sorted_ranges_are_partials_of_the_total():
 
 def test_sorted_argument_errors():
     pts = gen.random_spheres(40_000, 30.0, 1)
-    with pytest.raises(Exception, match="PC_TILE_SORTED"):
-        _lib.pairs_host(pts.astype(np.float32), _lib.PC_COLLISION, _lib.PC_BALANCED, [0, 40_000],
-                        tiling=_lib.PC_TILE_SORTED)
+    # fp32 contact counts take the sorted order too (the pruned count, round 2)
+    (r,) = _lib.pairs_host(pts.astype(np.float32), _lib.PC_COLLISION, _lib.PC_BALANCED, [0, 40_000],
+                           tiling=_lib.PC_TILE_SORTED)
+    assert r.count == c_oracle.rows(pts.astype(np.float32), 0, 40_000, "balanced")[0]
     with pytest.raises(Exception, match="PC_TILE_SORTED"):
         _lib.pairs_host(pts, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, 40_000], tiling=_lib.PC_TILE_SORTED)
+    with pytest.raises(Exception, match="PC_TILE_SORTED"):
+        _lib.pairs_host(pts.astype(np.float32), _lib.PC_COLLISION, _lib.PC_STANDARD, [0, 40_000],
+                        tiling=_lib.PC_TILE_SORTED)
 
 
 def test_sorted_path_non_finite_and_degenerate_inputs():

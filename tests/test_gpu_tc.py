@@ -75,15 +75,17 @@ def test_tc_integer_predicates(seed):
 
 
 def test_tc_auto_dispatch_at_config2_size(golden_configs):
-    # PC_TILE_AUTO sends balanced counts with 2^14 <= n < 2^21 (ranges covering >= n/8 rows) to the tensor
-    # cores: spi_balanced on config 2 keeps its golden count, and so do the summed
-    # spi_parallel partials and the FFMA kernel forced with PC_TILE_FLAT
+    # PC_TILE_AUTO sends balanced counts with 2^14 <= n < 2^21 over row ranges covering >= n/8 rows
+    # to the tensor cores (spi_parallel's workers here; a whole-range fp32 call from 2^15 points
+    # takes the pruned sorted count): config 2 keeps its golden count on every path, and so does
+    # the FFMA kernel forced with PC_TILE_FLAT
     from tests.helpers import config_input
 
     pts = config_input(golden_configs, "cfg2")
     want = golden_configs["cfg2"]["balanced"]["total"]
     assert se.spi_balanced(pts, se.collision_indicator).total == want
     assert sum(se.spi_parallel(pts, se.collision_indicator, workers=3, schedule="balanced").partials) == want
+    assert _lib.last_profile().kernel == 5  # the tensor cores took the workers' ranges
     (flat,) = _lib.pairs_host(np.ascontiguousarray(pts), _lib.PC_COLLISION, _lib.PC_BALANCED, [0, len(pts)],
                               tiling=_lib.PC_TILE_FLAT)
     assert flat.count == want
