@@ -10,15 +10,17 @@ ranks, both with no exchange but the final reduction:
   ``spi_parallel(workers=world).partials``.  Under the standard schedule rows
   own n-1-i pairs and the cuts r_g = n - n*sqrt(1 - g/G) equalise the work.
 * ``"tiles"`` -- the whole-range call's row tiles dealt round-robin
-  (``pc_pairs_part_*``): rank r runs tiles r, r+G, r+2G, ...  For the
-  inverse-square sum on fp32 points this is the path a single GPU takes
-  (spatially sorted points, PC_TILE_SORTED) split G ways; on sorted points
-  contiguous slabs are uneven (some regions of the sort order hold more
-  near-field chunks than others) and interleaved tiles are not.  The parts
-  add up to the whole-range result; they are not reference worker partials.
+  (``pc_pairs_part_*``): rank r runs tiles r, r+G, r+2G, ...  For fp32
+  spheres this is the path a single GPU takes (spatially sorted points,
+  PC_TILE_SORTED: the inverse-square sum with tile-local Gram chunks, the
+  contact count with box pruning) split G ways; on sorted points contiguous
+  slabs are uneven (some regions of the sort order hold more near-field
+  chunks than others) and interleaved tiles are not.  The parts add up to the
+  whole-range result; they are not reference worker partials.
 
-``"auto"`` takes tiles for fp32 inverse-square sums under the balanced
-schedule from 2^15 points (where one GPU would sort), slabs otherwise.
+``"auto"`` takes tiles for fp32 inverse-square sums and contact counts under
+the balanced schedule from 2^15 points (where one GPU would sort), slabs
+otherwise.
 
 The only exchange is the reduction: every rank writes (count, float64-sum
 bits, flags, pairs) into its own four slots of a zeroed int64 vector of
@@ -98,14 +100,19 @@ def allreduce_partials(count: int, total: float, group=None, device=None, is_flo
 
 def choose_split(obj: np.ndarray, f, schedule: str, split: str = "auto") -> str:
     """"tiles" or "slabs" for this problem (see the module docstring)."""
-    from . import spi_engine
+    from . import _lib, spi_engine
 
     if split not in SPLITS:
         raise ValueError(f"split must be one of {SPLITS}, got {split!r}")
     if split != "auto":
         return split
-    return ("tiles" if f is spi_engine.inverse_square and schedule == "balanced" and len(obj) >= SORTED_MIN_N
-            and getattr(obj, "dtype", None) == np.float32 and obj.ndim == 2 and obj.shape[1] == 3 else "slabs")
+    try:
+        code = spi_engine._interaction_code(f)
+    except TypeError:
+        return "slabs"  # the engines raise the reference's TypeError on their own
+    return ("tiles" if code in (_lib.PC_COLLISION, _lib.PC_COLLISION_INVSQ) and schedule == "balanced"
+            and len(obj) >= SORTED_MIN_N and getattr(obj, "dtype", None) == np.float32 and obj.ndim == 2
+            and obj.shape[1] == 3 else "slabs")
 
 
 def rank_partial(obj: np.ndarray, f, schedule: str, rank: int, world: int, split: str):
@@ -120,8 +127,9 @@ def rank_partial(obj: np.ndarray, f, schedule: str, rank: int, world: int, split
     if n < 2:
         return 0, 0
     code, xyz = spi_engine._prepare(obj, f, [(0, n)], schedule)
-    tiling = _lib.PC_TILE_SORTED if (code == _lib.PC_COLLISION_INVSQ and xyz.dtype == np.float32
-                                     and schedule == "balanced") else _lib.PC_TILE_AUTO
+    tiling = _lib.PC_TILE_SORTED if (code in (_lib.PC_COLLISION, _lib.PC_COLLISION_INVSQ)
+                                     and xyz.dtype == np.float32 and schedule == "balanced"
+                                     and n >= SORTED_MIN_N) else _lib.PC_TILE_AUTO
     sched = _lib.SCHEDULE_CODES[schedule]
 
     def run(x):

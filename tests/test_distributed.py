@@ -151,8 +151,9 @@ def _gpu_worker(rank, world, port, q):
         objs = gen.random_spheres(50_001, 30.0, 3).astype(np.float32)
         out = {}
         for sched in ("balanced", "standard"):
-            out[sched] = (D.spi_distributed(objs, se.collision_indicator, sched),
-                          D.spi_distributed(objs, se.inverse_square, sched))
+            out[sched] = (D.spi_distributed(objs, se.collision_indicator, sched, split="slabs"),
+                          D.spi_distributed(objs, se.inverse_square, sched),
+                          D.spi_distributed(objs, se.collision_indicator, sched))  # auto: tiles when balanced
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -180,11 +181,12 @@ def test_two_ranks_real_kernels_gloo():
     objs = gen.random_spheres(50_001, 30.0, 3).astype(np.float32)
     for sched in ("balanced", "standard"):
         want_c, want_s, _ = c_oracle.rows(objs, 0, len(objs), sched)
-        (tc, parts, pairs), (ts, _, _) = results[0][sched]
-        assert tc == want_c and ts == pytest.approx(want_s, rel=1e-5)
+        (tc, parts, pairs), (ts, _, _), (ta, aparts, apairs) = results[0][sched]
+        assert tc == want_c and ts == pytest.approx(want_s, rel=1e-5) and ta == want_c
+        assert sum(apairs) == len(objs) * (len(objs) - 1) // 2
         for (lo, hi), part in zip(D.row_slabs(len(objs), world, sched), parts):
-            assert part == c_oracle.rows(objs, lo, hi, sched)[0]
-        assert results[1][sched][0] == results[0][sched][0]
+            assert part == c_oracle.rows(objs, lo, hi, sched)[0]  # slabs: the reference workers' partials
+        assert results[1][sched][0] == results[0][sched][0] and results[1][sched][2] == results[0][sched][2]
 
 
 @pytest.mark.gpu
