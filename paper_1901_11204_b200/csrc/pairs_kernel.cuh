@@ -131,9 +131,10 @@ constexpr int pairs_smem_per_warp() {
 // a_i = q_i - o, b_j = q_j - o, A_i = 1 + |a_i|^2, B_j = |b_j|^2: 4 packed ops per two
 // pairs instead of 6.  Taken only where the bound on the form's rounding error,
 // 8u (|a|max + |b|max)^2 (the subtractions a = q - o, b = q - o, the |b|^2 chain, three
-// FFMA2 and the FADD2), is below 3.2e-6 (1 + dmin^2) -- every such term within 3.2e-6
-// relative; with the in-chunk fp32 accumulation (gamma_64 = 3.8e-6) the total stays below
-// 1e-5 (DESIGN.md §3 "Error budget") -- and dmin > 2.12, so the chunk holds no contact.
+// FFMA2 and the FADD2), is below 5e-6 (1 + dmin^2) -- every such term within 5e-6
+// relative; the chunk is accumulated in two fp32 halves (gamma_32 = 1.9e-6), so the total
+// stays below 1e-5 (DESIGN.md §3 "Error budget") -- and dmin > 2.12, so the chunk holds
+// no contact.
 // The boxes also decide the contact test: more than 1.5 apart, none; closer, each row's
 // smallest p flags its candidates (the chunk-sum test would flag every row there).
 template <int WARPS, int R, int W, bool DIRECT, bool FLAT, bool COMP = false, bool SORTED = false>
@@ -592,12 +593,15 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                     const float bb = fmaxf(fabsf(cl - o[k]), fabsf(ch - o[k]));
                     bm2 += bb * bb;
                 }
-                // 8u (|a| + |b|)^2 <= 3.2e-6 (1 + dmin^2), u = 2^-24 -- written as the same
-                // inequality 5u (..)^2 <= 2e-6 (..): eight roundings of terms of at most
+                // 8u (|a| + |b|)^2 <= 5e-6 (1 + dmin^2), u = 2^-24 -- written as the same
+                // inequality 5u (..)^2 <= 3.125e-6 (..): eight roundings of terms of at most
                 // (|a| + |b|)^2 against p >= 1 + dmin^2
                 const float ab = sqrtf(rt2) + sqrtf(bm2);
+#ifndef PC_GRAM_HALVES
+#define PC_GRAM_HALVES 1
+#endif
 #ifndef PC_GRAM_BUDGET
-#define PC_GRAM_BUDGET 2e-6f
+#define PC_GRAM_BUDGET (PC_GRAM_HALVES ? 3.125e-6f : 2e-6f)
 #endif
 #ifndef PC_GRAM_GAP2
 #define PC_GRAM_GAP2 4.5f
@@ -635,8 +639,25 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 float* gx = rx;
                 float* gy = ry;
                 float* gz = rz;
+#if PC_GRAM_HALVES
+                // two halves of W/2 columns, each row's fp32 partial flushed to float64 in between:
+                // the in-chunk accumulation error of a Gram chunk is gamma_32, not gamma_64, which
+                // pays for the wider Gram error budget (DESIGN.md §3 "Error budget")
+#pragma unroll 1
+                for (int half = 0; half < 2; ++half) {
+                if (half) {
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        sum += (double)(acc[r].x + acc[r].y);
+                        acc[r] = make_float2(0.f, 0.f);
+                    }
+                }
+#pragma unroll kDirectUnroll
+                for (int k = half * (W / 2); k < (half + 1) * (W / 2); k += 4) {
+#else
 #pragma unroll kDirectUnroll
                 for (int k = 0; k < W; k += 4) {
+#endif
                     const float4 A0 = sp[k], B0 = sp[k + 1], A1 = sp[k + 2], B1 = sp[k + 3];
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
@@ -652,6 +673,9 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                         acc[r] = __ffma2_rn(sm, make_float2(rcp_approx(pr.x), rcp_approx(pr.y)), acc[r]);
                     }
                 }
+#if PC_GRAM_HALVES
+                }
+#endif
             } else if (COMP && dense) {
                 // ---- compensated direct formula: dr = (hi_i - hi_j) + (lo_i - lo_j) keeps the
                 // separation to ~2u relative however far the points sit from the centre
