@@ -135,6 +135,29 @@ def check_parts(rng, stats):
                   flush=True)
 
 
+def check_pruned(rng, stats):
+    # round 2: whole-range fp32 contact counts take the pruned sorted count (n >= 2^15); the
+    # paper's thread-per-row kernels at random sizes
+    n = int(rng.integers(32768, 70000))
+    pts, kind = random_points(rng, n)
+    pts = pts.astype(np.float32)
+    want = c_oracle.rows(pts, 0, n, "balanced")[0]
+    got = se.spi_balanced(pts, se.collision_indicator).total
+    stats[("pruned-count", got == want)] += 1
+    if got != want:
+        print(f"MISMATCH pruned-count n={n} {kind}: got {got} want {want}", flush=True)
+    m = int(rng.integers(2, 6000))
+    sched = ("standard", "balanced")[int(rng.integers(0, 2))]
+    sub = pts[:m]
+    c, s_, p_ = c_oracle.rows(sub, 0, m, sched)
+    (r,) = _lib.pairs_host(np.ascontiguousarray(sub), _lib.PC_COLLISION_INVSQ, _lib.SCHEDULE_CODES[sched], [0, m],
+                           tiling=_lib.PC_TILE_THREAD_ROW)
+    ok = r.count == c and r.pairs == p_ and math.isclose(r.sum, s_, rel_tol=1e-6)
+    stats[("thread-row", ok)] += 1
+    if not ok:
+        print(f"MISMATCH thread-row m={m} {sched}: got {r.count} {r.sum!r} want {c} {s_!r}", flush=True)
+
+
 def check_int(rng, stats):
     n = int(rng.choice([1, 2, 5, 100, 1000, 4096, 5000, 20000]))
     span = int(rng.integers(1, 40))
@@ -191,6 +214,7 @@ def main():
         check_lattice(rng, stats)
         check_tc(rng, stats)
         check_parts(rng, stats)
+        check_pruned(rng, stats)
         if args.sorted:
             check_sorted(rng, stats)
         rounds += 1
