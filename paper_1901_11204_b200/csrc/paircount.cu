@@ -638,28 +638,30 @@ __device__ __forceinline__ unsigned spread10(unsigned v) {  // 10 bits -> every 
     v = (v | (v << 2)) & 0x09249249u;
     return v;
 }
-__global__ void morton_kernel(const float* __restrict__ xyz, long long n, const PrepStats* __restrict__ st,
+template <typename T>  // float (sums and counts) or double (pruned counts of float64 points)
+__global__ void morton_kernel(const T* __restrict__ xyz, long long n, const PrepStats* __restrict__ st,
                               unsigned* __restrict__ keys, unsigned* __restrict__ idx) {
-    float lo[3], sc[3];
+    T lo[3], sc[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const double mn = dec_f64(st->mn[k]), mx = dec_f64(st->mx[k]);
-        lo[k] = (float)mn;
-        sc[k] = mx > mn ? (float)(1023.0 / (mx - mn)) : 0.f;
+        lo[k] = (T)mn;
+        sc[k] = mx > mn ? (T)(1023.0 / (mx - mn)) : (T)0;
     }
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         unsigned c[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            const float v = (xyz[3 * i + k] - lo[k]) * sc[k];
+            const float v = (float)((xyz[3 * i + k] - lo[k]) * sc[k]);
             c[k] = (unsigned)fminf(fmaxf(v, 0.f), 1023.f);
         }
         keys[i] = spread10(c[0]) | (spread10(c[1]) << 1) | (spread10(c[2]) << 2);
         idx[i] = (unsigned)i;
     }
 }
-__global__ void gather_sorted_kernel(const float* __restrict__ xyz, const unsigned* __restrict__ idx, long long n,
-                                     float* __restrict__ out) {
+template <typename T>
+__global__ void gather_sorted_kernel(const T* __restrict__ xyz, const unsigned* __restrict__ idx, long long n,
+                                     T* __restrict__ out) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const long long s = idx[i];
         out[3 * i] = xyz[3 * s];
@@ -681,15 +683,21 @@ __global__ void blk2_box_kernel(const float4* __restrict__ box, int nblk, int nb
     }
 }
 // one thread per 32-point block: (min x, y, z, 0), (max x, y, z, 0)
-__global__ void blk_box_kernel(const float* __restrict__ xyz, long long n, int nblk, float4* __restrict__ box) {
+__device__ __forceinline__ float round_down_f(float v) { return v; }
+__device__ __forceinline__ float round_up_f(float v) { return v; }
+__device__ __forceinline__ float round_down_f(double v) { return __double2float_rd(v); }
+__device__ __forceinline__ float round_up_f(double v) { return __double2float_ru(v); }
+// float64 points: boxes rounded outward to fp32, so they still contain their points
+template <typename T>
+__global__ void blk_box_kernel(const T* __restrict__ xyz, long long n, int nblk, float4* __restrict__ box) {
     for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nblk; b += (long long)gridDim.x * blockDim.x) {
         float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
         const long long e = min(n, 32 * b + 32);
         for (long long i = 32 * b; i < e; ++i) {
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
-                mn[k] = fminf(mn[k], xyz[3 * i + k]);
-                mx[k] = fmaxf(mx[k], xyz[3 * i + k]);
+                mn[k] = fminf(mn[k], round_down_f(xyz[3 * i + k]));
+                mx[k] = fmaxf(mx[k], round_up_f(xyz[3 * i + k]));
             }
         }
         box[2 * b] = make_float4(mn[0], mn[1], mn[2], 0.f);
@@ -718,7 +726,7 @@ WsLayout ws_layout(long long n) {
     // sorted points, per-32-point boxes, radix-sort scratch
     l.srt = align_up(l.tc_cnt + 4 * 1024, 256);
     const size_t nn = (size_t)(n < 0 ? 0 : n);
-    l.srt_temp = align_up(l.srt + 4 * align_up(nn * 4, 256) + align_up(nn * 12, 256) +
+    l.srt_temp = align_up(l.srt + 4 * align_up(nn * 4, 256) + align_up(nn * 24, 256) +
                           align_up((nn / 32 + 1) * 32, 256) + align_up((nn / 1024 + 1) * 32, 256), 256);
     l.total = align_up(l.srt_temp + kSortTempBytes(nn), 256);
     return l;
@@ -1020,7 +1028,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     if (tiling == PC_TILE_TC && ts.tstride != 1) return arg_fail("PC_TILE_TC does not take tile parts");
     const bool whole = nranges == 1 && bounds[0] == 0 && bounds[1] == n;
     const bool prune_auto = PC_SORTED_COUNT && tiling == PC_TILE_AUTO && whole && interaction == PC_COLLISION &&
-                            dtype == PC_F32 && schedule == PC_BALANCED && n >= kSortedMinN;
+                            (dtype == PC_F32 || dtype == PC_F64) && schedule == PC_BALANCED && n >= kSortedMinN;
     const bool use_tc = tc_ok && ts.tstride == 1 && !prune_auto &&
                         (tiling == PC_TILE_TC || (tiling == PC_TILE_AUTO && PC_TC_AUTO && n >= kTcMinN &&
                                                   n < kTcMaxN && rows * 8 >= n));
@@ -1032,10 +1040,11 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
         return arg_fail("PC_TILE_THREAD_ROW needs fp32 spheres (collision count or inverse-square sum), no tile parts");
     if (use_key && (interaction != PC_COINCIDE || schedule != PC_BALANCED || ts.tstride != 1))
         return arg_fail("PC_TILE_KEY needs the coincidence count, the balanced schedule and no tile parts");
-    if (sorted_req && ((interaction != PC_COLLISION_INVSQ && interaction != PC_COLLISION) || dtype != PC_F32 ||
-                       schedule != PC_BALANCED))
-        return arg_fail("PC_TILE_SORTED needs fp32 spheres (inverse-square sum or contact count) and the balanced "
-                        "schedule");
+    if (sorted_req && ((interaction == PC_COLLISION_INVSQ && dtype != PC_F32) ||
+                       (interaction == PC_COLLISION && dtype != PC_F32 && dtype != PC_F64) ||
+                       (interaction != PC_COLLISION_INVSQ && interaction != PC_COLLISION) || schedule != PC_BALANCED))
+        return arg_fail("PC_TILE_SORTED needs spheres -- the inverse-square sum on fp32 points or the contact count "
+                        "on fp32 / fp64 points -- and the balanced schedule");
     if (tiling == PC_TILE_AUTO || tiling == PC_TILE_TC || tiling == PC_TILE_SORTED || use_key || use_row)
         tiling = schedule == PC_BALANCED ? PC_TILE_FLAT : PC_TILE_PER_ROW_TILE;
     if (tiling == PC_TILE_FLAT && schedule != PC_BALANCED)
@@ -1064,7 +1073,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     const bool sorted = PC_SORTED_SUM && direct && !comp && schedule == PC_BALANCED && n >= kSortedMinN &&
                         ((auto_tiling && whole_range) || sorted_req);
     // whole-range fp32 contact counts: the same sort, then the Gram count with box pruning (pairs_kernel.cuh)
-    const bool sorted_count = PC_SORTED_COUNT && interaction == PC_COLLISION && dtype == PC_F32 &&
+    const bool sorted_count = PC_SORTED_COUNT && interaction == PC_COLLISION && (dtype == PC_F32 || dtype == PC_F64) &&
                               schedule == PC_BALANCED && n >= kSortedMinN && ts.tstride >= 1 &&
                               ((auto_tiling && whole_range) || sorted_req);
     const float4* blk_box = nullptr;
@@ -1080,9 +1089,11 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
             unsigned* k1 = (unsigned*)(ws + lay.srt + kb);
             unsigned* v0 = (unsigned*)(ws + lay.srt + 2 * kb);
             unsigned* v1 = (unsigned*)(ws + lay.srt + 3 * kb);
-            float* xs = (float*)(ws + lay.srt + 4 * kb);
-            float4* box = (float4*)(ws + lay.srt + 4 * kb + align_up((size_t)n * 12, 256));
-            morton_kernel<<<blocks, 256, 0, s>>>((const float*)xyz, n, st, k0, v0);
+            void* xs = ws + lay.srt + 4 * kb;  // sorted copy of the points (12 or 24 B each)
+            float4* box = (float4*)(ws + lay.srt + 4 * kb + align_up((size_t)n * 24, 256));
+            const bool f64 = dtype == PC_F64;
+            if (f64) morton_kernel<double><<<blocks, 256, 0, s>>>((const double*)xyz, n, st, k0, v0);
+            else morton_kernel<float><<<blocks, 256, 0, s>>>((const float*)xyz, n, st, k0, v0);
             CK_LAUNCH("morton_kernel");
             cub::DoubleBuffer<unsigned> dk(k0, k1), dv(v0, v1);
             size_t tb = 0;
@@ -1090,14 +1101,16 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
             if (tb > kSortTempBytes((size_t)n)) return arg_fail("radix-sort scratch exceeds its reservation");
             CK(cub::DeviceRadixSort::SortPairs(ws + lay.srt_temp, tb, dk, dv, (int)n, 0, 30, s));
             // (the radix sort's kernels are CUB's, not counted in g_launches)
-            gather_sorted_kernel<<<blocks, 256, 0, s>>>((const float*)xyz, dv.Current(), n, xs);
+            if (f64) gather_sorted_kernel<double><<<blocks, 256, 0, s>>>((const double*)xyz, dv.Current(), n, (double*)xs);
+            else gather_sorted_kernel<float><<<blocks, 256, 0, s>>>((const float*)xyz, dv.Current(), n, (float*)xs);
             CK_LAUNCH("gather_sorted_kernel");
-            blk_box_kernel<<<(nblk + 255) / 256, 256, 0, s>>>(xs, n, nblk, box);
+            if (f64) blk_box_kernel<double><<<(nblk + 255) / 256, 256, 0, s>>>((const double*)xs, n, nblk, box);
+            else blk_box_kernel<float><<<(nblk + 255) / 256, 256, 0, s>>>((const float*)xs, n, nblk, box);
             CK_LAUNCH("blk_box_kernel");
             if (sorted_count) {
-                float4* box2 = box + 2 * (size_t)nblk;  // (n/32+1)*32 B reserved for box, then box2
-                box2 = (float4*)(ws + lay.srt + 4 * kb + align_up((size_t)n * 12, 256) +
-                                 align_up((size_t)(n / 32 + 1) * 32, 256));
+                // the per-1024 boxes follow the (n/32+1)*32 B of per-32 boxes
+                float4* box2 = (float4*)(ws + lay.srt + 4 * kb + align_up((size_t)n * 24, 256) +
+                                         align_up((size_t)(n / 32 + 1) * 32, 256));
                 const int nblk2 = (int)((n + 1023) / 1024);
                 blk2_box_kernel<<<(nblk2 + 255) / 256, 256, 0, s>>>(box, nblk, nblk2, box2);
                 CK_LAUNCH("blk2_box_kernel");

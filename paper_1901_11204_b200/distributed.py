@@ -110,9 +110,10 @@ def choose_split(obj: np.ndarray, f, schedule: str, split: str = "auto") -> str:
         code = spi_engine._interaction_code(f)
     except TypeError:
         return "slabs"  # the engines raise the reference's TypeError on their own
+    dt = getattr(obj, "dtype", None)
+    sortable = dt == np.float32 or (dt == np.float64 and code == _lib.PC_COLLISION)  # the sorted kernels' inputs
     return ("tiles" if code in (_lib.PC_COLLISION, _lib.PC_COLLISION_INVSQ) and schedule == "balanced"
-            and len(obj) >= SORTED_MIN_N and getattr(obj, "dtype", None) == np.float32 and obj.ndim == 2
-            and obj.shape[1] == 3 else "slabs")
+            and len(obj) >= SORTED_MIN_N and sortable and obj.ndim == 2 and obj.shape[1] == 3 else "slabs")
 
 
 def rank_partial(obj: np.ndarray, f, schedule: str, rank: int, world: int, split: str):
@@ -127,9 +128,9 @@ def rank_partial(obj: np.ndarray, f, schedule: str, rank: int, world: int, split
     if n < 2:
         return 0, 0
     code, xyz = spi_engine._prepare(obj, f, [(0, n)], schedule)
-    tiling = _lib.PC_TILE_SORTED if (code in (_lib.PC_COLLISION, _lib.PC_COLLISION_INVSQ)
-                                     and xyz.dtype == np.float32 and schedule == "balanced"
-                                     and n >= SORTED_MIN_N) else _lib.PC_TILE_AUTO
+    sortable = xyz.dtype == np.float32 or (xyz.dtype == np.float64 and code == _lib.PC_COLLISION)
+    tiling = _lib.PC_TILE_SORTED if (code in (_lib.PC_COLLISION, _lib.PC_COLLISION_INVSQ) and sortable
+                                     and schedule == "balanced" and n >= SORTED_MIN_N) else _lib.PC_TILE_AUTO
     sched = _lib.SCHEDULE_CODES[schedule]
 
     def run(x):

@@ -249,8 +249,9 @@ def test_paper_thread_row_schemes(n):
                         tiling=_lib.PC_TILE_THREAD_ROW)
 
 
-@pytest.mark.parametrize("n", [32768, 40001, 65537])
-def test_pruned_sorted_count(n):
+@pytest.mark.parametrize("n,dtype", [(32768, np.float32), (40001, np.float32), (65537, np.float32),
+                                     (40001, np.float64)])
+def test_pruned_sorted_count(n, dtype):
     """Whole-range fp32 contact counts (spi_balanced / PC_TILE_AUTO) run on Morton-sorted
     points with box pruning: exact against the oracle on distributions that stress the
     box test (contacts at exactly distance 1 on a lattice, dense clusters, far-apart
@@ -267,6 +268,10 @@ def test_pruned_sorted_count(n):
                                            ).astype(np.float32),
         "thin slab": (rng.random((n, 3)) * np.array([box * 6, box * 6, 0.8])).astype(np.float32),
     }
+    if dtype == np.float64:  # float64 points: boxes rounded outward, Gram staging from float64
+        cases = {k: v.astype(np.float64) + (1e-7 if k != "lattice (d = 1 exactly)" else 0.0)
+                 for k, v in cases.items()}
+        cases["offset 1e5"] = cases["uniform"] + 1e5
     for name, x in cases.items():
         want = c_oracle.rows(x, 0, n, "balanced")[0]
         assert se.spi_balanced(x, se.collision_indicator).total == want, name
