@@ -394,7 +394,7 @@ struct Slot {
 static_assert(sizeof(Slot) == 64, "Slot is one 64-byte record");
 // kernel ids recorded in pc_pairs_profile.kernel
 constexpr int kKernGram = 1, kKernDirect = 2, kKernSorted = 3, kKernComp = 4, kKernTc = 5, kKernKey = 6,
-              kKernRow = 7, kKernSortedCount = 8;
+              kKernRow = 7, kKernSortedCount = 8, kKernCompSorted = 9;
 
 // FLAT work claims (guided self-scheduling): claim c of stage k covers columns
 // [b0[k] + (c - c0[k]) * s[k], + s[k]) of the flat (row tile, window column) space.  Stage k
@@ -616,6 +616,13 @@ constexpr KernelCfg kBig{4, PC_BIG_R, PC_BIG_W};  // direct (sum) kernel: warp t
 #endif
 constexpr KernelCfg kBigGram{4, PC_GRAM_R, PC_GRAM_W};  // count kernel: 384-row warp tiles measured 6% faster than 256
 constexpr KernelCfg kBigComp{4, 4, PC_COMP_W};          // compensated sum kernel (non-f32 input): 6 row registers per row
+#ifndef PC_COMP_SORTED_R
+#define PC_COMP_SORTED_R 6
+#endif
+#ifndef PC_COMP_SORTED_W
+#define PC_COMP_SORTED_W 192
+#endif
+constexpr KernelCfg kBigCompSorted{4, PC_COMP_SORTED_R, PC_COMP_SORTED_W};  // float64 points, sorted
 constexpr KernelCfg kSmall{4, 2, 64};  // warp tile 64 rows, for n < kSmallN
 constexpr int kSmallN = 16384;
 
@@ -667,6 +674,29 @@ __global__ void gather_sorted_kernel(const T* __restrict__ xyz, const unsigned* 
         out[3 * i] = xyz[3 * s];
         out[3 * i + 1] = xyz[3 * s + 1];
         out[3 * i + 2] = xyz[3 * s + 2];
+    }
+}
+// one thread per 32-point block of sorted float64 points: the box of their centred fp32 high
+// parts fl32(p - c) (c the bounding-box centre), the coordinates the compensated sum kernel
+// holds in its row registers and stages as column highs
+__global__ void blk_box_centred_kernel(const double* __restrict__ xyz, long long n, int nblk,
+                                       const PrepStats* __restrict__ st, float4* __restrict__ box) {
+    double c[3];
+    long long ci[3];
+    bbox_centre(*st, PC_F64, c, ci);
+    for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < nblk; b += (long long)gridDim.x * blockDim.x) {
+        float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+        const long long e = min(n, 32 * b + 32);
+        for (long long i = 32 * b; i < e; ++i) {
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const float h = (float)(xyz[3 * i + k] - c[k]);
+                mn[k] = fminf(mn[k], h);
+                mx[k] = fmaxf(mx[k], h);
+            }
+        }
+        box[2 * b] = make_float4(mn[0], mn[1], mn[2], 0.f);
+        box[2 * b + 1] = make_float4(mx[0], mx[1], mx[2], 0.f);
     }
 }
 // one thread per 1024-point block: the union of its 32 per-32-point boxes
@@ -1040,11 +1070,11 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
         return arg_fail("PC_TILE_THREAD_ROW needs fp32 spheres (collision count or inverse-square sum), no tile parts");
     if (use_key && (interaction != PC_COINCIDE || schedule != PC_BALANCED || ts.tstride != 1))
         return arg_fail("PC_TILE_KEY needs the coincidence count, the balanced schedule and no tile parts");
-    if (sorted_req && ((interaction == PC_COLLISION_INVSQ && dtype != PC_F32) ||
+    if (sorted_req && ((interaction == PC_COLLISION_INVSQ && dtype != PC_F32 && dtype != PC_F64) ||
                        (interaction == PC_COLLISION && dtype != PC_F32 && dtype != PC_F64) ||
                        (interaction != PC_COLLISION_INVSQ && interaction != PC_COLLISION) || schedule != PC_BALANCED))
-        return arg_fail("PC_TILE_SORTED needs spheres -- the inverse-square sum on fp32 points or the contact count "
-                        "on fp32 / fp64 points -- and the balanced schedule");
+        return arg_fail("PC_TILE_SORTED needs spheres -- the inverse-square sum or the contact count on fp32 / fp64 "
+                        "points -- and the balanced schedule");
     if (tiling == PC_TILE_AUTO || tiling == PC_TILE_TC || tiling == PC_TILE_SORTED || use_key || use_row)
         tiling = schedule == PC_BALANCED ? PC_TILE_FLAT : PC_TILE_PER_ROW_TILE;
     if (tiling == PC_TILE_FLAT && schedule != PC_BALANCED)
@@ -1070,8 +1100,8 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     // (PC_TILE_AUTO on the whole range, or PC_TILE_SORTED for row ranges of the sorted
     // order; PC_TILE_FLAT keeps the input order, the plain kernel)
     const bool whole_range = nranges == 1 && bounds[0] == 0 && bounds[1] == n;
-    const bool sorted = PC_SORTED_SUM && direct && !comp && schedule == PC_BALANCED && n >= kSortedMinN &&
-                        ((auto_tiling && whole_range) || sorted_req);
+    const bool sorted = PC_SORTED_SUM && direct && (!comp || dtype == PC_F64) && schedule == PC_BALANCED &&
+                        n >= kSortedMinN && ((auto_tiling && whole_range) || sorted_req);
     // whole-range fp32 contact counts: the same sort, then the Gram count with box pruning (pairs_kernel.cuh)
     const bool sorted_count = PC_SORTED_COUNT && interaction == PC_COLLISION && (dtype == PC_F32 || dtype == PC_F64) &&
                               schedule == PC_BALANCED && n >= kSortedMinN && ts.tstride >= 1 &&
@@ -1104,7 +1134,9 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
             if (f64) gather_sorted_kernel<double><<<blocks, 256, 0, s>>>((const double*)xyz, dv.Current(), n, (double*)xs);
             else gather_sorted_kernel<float><<<blocks, 256, 0, s>>>((const float*)xyz, dv.Current(), n, (float*)xs);
             CK_LAUNCH("gather_sorted_kernel");
-            if (f64) blk_box_kernel<double><<<(nblk + 255) / 256, 256, 0, s>>>((const double*)xs, n, nblk, box);
+            if (f64 && comp)  // the compensated sum works on centred high parts
+                blk_box_centred_kernel<<<(nblk + 255) / 256, 256, 0, s>>>((const double*)xs, n, nblk, st, box);
+            else if (f64) blk_box_kernel<double><<<(nblk + 255) / 256, 256, 0, s>>>((const double*)xs, n, nblk, box);
             else blk_box_kernel<float><<<(nblk + 255) / 256, 256, 0, s>>>((const float*)xs, n, nblk, box);
             CK_LAUNCH("blk_box_kernel");
             if (sorted_count) {
@@ -1184,7 +1216,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
         return PC_OK;
     }
     const int kern_id = !direct ? (sorted_count ? kKernSortedCount : kKernGram)
-                                : comp ? kKernComp : sorted ? kKernSorted : kKernDirect;
+                                : comp ? (sorted ? kKernCompSorted : kKernComp) : sorted ? kKernSorted : kKernDirect;
     for (int k = 0; k < nranges; ++k) {
         const long long lo = bounds[k], hi = bounds[k + 1];
         int nslots = 0, nclaims = 0, trows = 1;
@@ -1201,7 +1233,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
                      : direct ? PC_DISPATCH(kSmall, true)
                               : PC_DISPATCH(kSmall, false);
             else
-                rc = comp     ? PC_DISPATCH(kBigComp, true, true)
+                rc = comp     ? (sorted ? PC_DISPATCH(kBigCompSorted, true, true, true) : PC_DISPATCH(kBigComp, true, true))
                      : sorted ? PC_DISPATCH(kBig, true, false, true)
                      : direct ? PC_DISPATCH(kBig, true)
                      : sorted_count ? PC_DISPATCH(kBigGram, false, false, true)

@@ -606,23 +606,30 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
 #ifndef PC_GRAM_GAP2
 #define PC_GRAM_GAP2 4.5f
 #endif
-                gram = gap2 > PC_GRAM_GAP2 && 2.98023223876953125e-07f * ab * ab <= PC_GRAM_BUDGET * (1.f + gap2);
+                // compensated (float64) points: a = (hi - o) + lo rounds once more: 10u instead of 8u
+                constexpr float kGramU = COMP ? 3.725290298461914e-07f : 2.98023223876953125e-07f;
+                gram = gap2 > PC_GRAM_GAP2 && kGramU * ab * ab <= PC_GRAM_BUDGET * (1.f + gap2);
                 // boxes more than 1.5 apart: no contact, so no rescan however large the chunk's
                 // sums (on sorted points the chunks next to a tile have many near terms)
                 no_contact = gap2 > 2.25f;
             }
             if (SORTED && gram) {
                 // columns to tile-local form in place: (bx, by, bz, B = |b|^2) per point
+                // (compensated entries: b = (hi - o) + lo, written over the entry's first two float4)
                 float4* spw = const_cast<float4*>(sp);
 #pragma unroll
                 for (int q = 0; q < W / 64; ++q) {
                     const int e = q * 32 + lane;  // pair entry: points 2e, 2e+1 of the chunk
-                    const float4 A = spw[2 * e], B = spw[2 * e + 1];
-                    const float bx0 = A.x - o[0], bx1 = A.y - o[0], by0 = A.z - o[1], by1 = A.w - o[1];
-                    const float bz0 = B.x - o[2], bz1 = B.y - o[2];
-                    spw[2 * e] = make_float4(bx0, bx1, by0, by1);
-                    spw[2 * e + 1] = make_float4(bz0, bz1, fmaf(bz0, bz0, fmaf(by0, by0, bx0 * bx0)),
-                                                 fmaf(bz1, bz1, fmaf(by1, by1, bx1 * bx1)));
+                    const float4 A = spw[PS * e], B = spw[PS * e + 1];
+                    float bx0 = A.x - o[0], bx1 = A.y - o[0], by0 = A.z - o[1], by1 = A.w - o[1];
+                    float bz0 = B.x - o[2], bz1 = B.y - o[2];
+                    if (COMP) {
+                        const float4 C = spw[PS * e + 2];
+                        bx0 += B.z; bx1 += B.w; by0 += C.x; by1 += C.y; bz0 += C.z; bz1 += C.w;
+                    }
+                    spw[PS * e] = make_float4(bx0, bx1, by0, by1);
+                    spw[PS * e + 1] = make_float4(bz0, bz1, fmaf(bz0, bz0, fmaf(by0, by0, bx0 * bx0)),
+                                                  fmaf(bz1, bz1, fmaf(by1, by1, bx1 * bx1)));
                 }
                 __syncwarp();
                 // rows in Gram form in the row registers themselves (restored from the row
@@ -630,7 +637,12 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 float ga[R];
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    const float ax = rx[r] - o[0], ay = ry[r] - o[1], az = rz[r] - o[2];
+                    float ax = rx[r] - o[0], ay = ry[r] - o[1], az = rz[r] - o[2];
+                    if (COMP) {
+                        ax += rxl[r];
+                        ay += ryl[r];
+                        az += rzl[r];
+                    }
                     rx[r] = -2.f * ax;
                     ry[r] = -2.f * ay;
                     rz[r] = -2.f * az;
@@ -658,7 +670,8 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
 #pragma unroll kDirectUnroll
                 for (int k = 0; k < W; k += 4) {
 #endif
-                    const float4 A0 = sp[k], B0 = sp[k + 1], A1 = sp[k + 2], B1 = sp[k + 3];
+                    const float4* E = sp + PS * (k >> 1);  // entries of columns k, k+1 and k+2, k+3
+                    const float4 A0 = E[0], B0 = E[1], A1 = E[PS], B1 = E[PS + 1];
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
                         float2 t0 = f2_fma(gx[r], make_float2(A0.x, A0.y), make_float2(B0.z, B0.w));
@@ -777,10 +790,11 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             }
             count_path((SORTED && gram) ? kPathGram
                        : !dense ? kPathEdge
-                       : (SORTED && !no_contact) ? kPathNear
+                       : (SORTED && !COMP && !no_contact) ? kPathNear
+                       : (SORTED && COMP) ? (no_contact ? kPathFar : kPathMain)
                        : SORTED ? kPathFar : kPathMain, 1u);
             if (SORTED && no_contact) fl = 0;  // also covers the Gram chunks, whose columns were rewritten
-            if (SORTED && dense && !no_contact) fl = near_fl;  // exact candidates, not chunk sums
+            if (SORTED && !COMP && dense && !no_contact) fl = near_fl;  // exact candidates, not chunk sums
             if (SORTED && gram && staged_tile == tile) {
                 // back to the raw rows for the tile's next chunks (a new tile reloads them anyway)
 #pragma unroll

@@ -49,6 +49,28 @@ def test_sorted_sum_matches_oracle(n):
         assert abs(res.total - want_s) <= 1e-6 * want_s, name
 
 
+@pytest.mark.parametrize("n", [32768, 40001, 65537])
+def test_sorted_sum_float64_points(n):
+    """Float64 points on the sorted path (round 2): Morton sort of the float64 array, the
+    compensated hi + lo staging, Gram chunks formed from b = (hi - o) + lo."""
+    for name, pts in _inputs(n, n + 1).items():
+        want_c, want_s, pairs = c_oracle.rows(pts, 0, n, "balanced")
+        (r,) = _lib.pairs_host(pts, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, n])  # AUTO: sorted
+        prof = _lib.last_profile()
+        assert prof.kernel == 9 and prof.chunks_gram > 0, name
+        assert (r.count, r.pairs, r.error) == (want_c, pairs, 0), name
+        assert abs(r.sum - want_s) <= 1e-6 * want_s, (name, r.sum, want_s)
+        assert se.spi_balanced(pts, se.inverse_square).total == r.sum, name
+    # far from the origin and two clusters 1e6 apart: the centred hi + lo keeps separations exact
+    rng = np.random.default_rng(n)
+    for name, pts in (("offset 1e6", rng.random((n, 3)) * 40 + 1e6),
+                      ("clusters 1e6 apart", np.concatenate([rng.random((n // 2, 3)) * 20,
+                                                             rng.random((n - n // 2, 3)) * 20 + 1e6]))):
+        want_c, want_s, _ = c_oracle.rows(pts, 0, n, "balanced")
+        (r,) = _lib.pairs_host(pts, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, n])
+        assert r.count == want_c and abs(r.sum - want_s) <= 1e-6 * want_s, (name, r.sum, want_s)
+
+
 def test_sorted_ranges_are_partials_of_the_total():
     # PC_TILE_SORTED row ranges index the sorted order (the multi-GPU slabs): each is a
     # partial of the same total, not the reference's _run_outer over those input rows
@@ -74,7 +96,8 @@ def test_sorted_argument_errors():
                            tiling=_lib.PC_TILE_SORTED)
     assert r.count == c_oracle.rows(pts.astype(np.float32), 0, 40_000, "balanced")[0]
     with pytest.raises(Exception, match="PC_TILE_SORTED"):
-        _lib.pairs_host(pts, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, 40_000], tiling=_lib.PC_TILE_SORTED)
+        _lib.pairs_host(pts.astype(np.int64), _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, 40_000],
+                        tiling=_lib.PC_TILE_SORTED)
     with pytest.raises(Exception, match="PC_TILE_SORTED"):
         _lib.pairs_host(pts.astype(np.float32), _lib.PC_COLLISION, _lib.PC_STANDARD, [0, 40_000],
                         tiling=_lib.PC_TILE_SORTED)
