@@ -305,6 +305,29 @@ def secondary(torch, lib, stream):
                                   "per 48 pairs) at 64 lanes/clk/SM x 148 SMs x the sampled SM clock"}
     del di, wsi
 
+    # ---- float64 input (the reference generators' own dtype): the sum on the input order
+    # (compensated hi + lo) vs on Morton-sorted points (what spi_balanced takes from 2^15 points)
+    x64 = gen.random_spheres(2**20, gen.contact_box_edge(2**20), 1)
+    d64 = torch.from_numpy(x64).cuda()
+    ws64 = torch.empty(_lib.workspace_bytes(2**20), dtype=torch.uint8, device="cuda")
+    res = torch.zeros(8, dtype=torch.int64, device="cuda")
+    f64leg = {}
+    for label, tiling in (("input_order_compensated", _lib.PC_TILE_FLAT), ("sorted_compensated", _lib.PC_TILE_AUTO)):
+        _lib.pairs_async(d64.data_ptr(), _lib.PC_F64, 2**20, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED,
+                         np.array([0, 2**20]), ws64.data_ptr(), ws64.numel(), res.data_ptr(), stream.cuda_stream, tiling)
+        _lib.kernel_timing(True)
+        for _ in range(2):
+            _lib.pairs_async(d64.data_ptr(), _lib.PC_F64, 2**20, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED,
+                             np.array([0, 2**20]), ws64.data_ptr(), ws64.numel(), res.data_ptr(), stream.cuda_stream,
+                             tiling)
+        ms64, c64 = _lib.kernel_timing_read()
+        _lib.kernel_timing(False)
+        torch.cuda.synchronize()
+        f64leg[label] = {"kernel_ms": ms64 / c64, "count": int(res[0].item()),
+                         "Gpair_per_s": (2**20) * (2**20 - 1) / 2 / (ms64 / c64 * 1e-3) / 1e9}
+    out["float64_points_sum_n2^20"] = f64leg
+    del d64, ws64
+
     # ---- config 2
     n2 = 65536
     obj2 = gen.random_spheres(n2, gen.contact_box_edge(n2), 0).astype(np.float32)
