@@ -45,27 +45,6 @@ size_t batch_tail_bytes(int32_t nvec) {
     return align_up((size_t)(nvec + 1) * 8, 256) + align_up((size_t)nvec * 24, 256);
 }
 
-// Pinned host staging for pc_lattice_collisions_vectors (per device, guarded by the arena lock).
-struct Pinned {
-    void* p = nullptr;
-    size_t cap = 0;
-};
-Pinned g_pinned[64];
-
-int pinned_get(int dev, size_t bytes, void** out) {
-    Pinned& pn = g_pinned[dev & 63];
-    if (pn.cap < bytes) {
-        if (pn.p) CK(cudaFreeHost(pn.p));
-        pn.p = nullptr;
-        pn.cap = 0;
-        const size_t want = align_up(bytes + bytes / 4, 1 << 20);
-        CK(cudaHostAlloc(&pn.p, want, cudaHostAllocDefault));
-        pn.cap = want;
-    }
-    *out = pn.p;
-    return PC_OK;
-}
-
 // Gather vectors [v0, v1) into dst as int32, mapping any coordinate outside
 // [-a, a] to INT32_MAX (itself outside [-a, a], so the kernel still reports
 // the first bad bead of that vector -- narrowing can never wrap a bad bead

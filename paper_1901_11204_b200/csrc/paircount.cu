@@ -1313,6 +1313,31 @@ int arena_get(size_t bytes, Arena** out) {
 
 size_t dtype_bytes(int dtype) { return dtype == PC_F32 || dtype == PC_I32 ? 4 : 8; }
 
+// Pinned host staging for pc_lattice_collisions_vectors / pc_pairs_batch (per device, guarded
+// by the arena lock).  Not used by pc_pairs_host: staging 12 MB through it measured ~1 ms
+// slower than one pageable cudaMemcpy (scripts/time_e2e.py, r2).
+struct Pinned {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+Pinned g_pinned[64];
+
+int pinned_get(int dev, size_t bytes, void** out) {
+    Pinned& pn = g_pinned[dev & 63];
+    if (pn.cap < bytes) {
+        if (pn.p) CK(cudaFreeHost(pn.p));
+        pn.p = nullptr;
+        pn.cap = 0;
+        const size_t want = align_up(bytes + bytes / 4, 1 << 20);
+        CK(cudaHostAlloc(&pn.p, want, cudaHostAllocDefault));
+        pn.cap = want;
+    }
+    *out = pn.p;
+    return PC_OK;
+}
+
+
+
 #include "lattice.cuh"
 
 // ------------------------------------------------------------------------
