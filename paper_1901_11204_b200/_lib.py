@@ -67,7 +67,8 @@ class PairsProfile(ctypes.Structure):
     _fields_ = [("chunks_gram", ctypes.c_int64), ("chunks_main", ctypes.c_int64), ("chunks_near", ctypes.c_int64),
                 ("chunks_far", ctypes.c_int64), ("chunks_edge", ctypes.c_int64), ("rows_rescanned", ctypes.c_int64),
                 ("exact_checks", ctypes.c_int64), ("claims", ctypes.c_int64), ("pairs", ctypes.c_int64),
-                ("pairs_per_chunk", ctypes.c_int64), ("kernel", ctypes.c_int32), ("f64_taken", ctypes.c_int32)]
+                ("pairs_per_chunk", ctypes.c_int64), ("kernel", ctypes.c_int32), ("f64_taken", ctypes.c_int32),
+                ("chunks_tc", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {name: int(getattr(self, name)) for name, _ in self._fields_}

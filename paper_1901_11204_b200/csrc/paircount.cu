@@ -389,12 +389,12 @@ struct Slot {
     double sum;
     unsigned path[kNumPaths];
     unsigned rescans;
-    unsigned pad[4];
+    unsigned pad[4];  // pad[0]: chunks the tensor-core sum kernel evaluated
 };
 static_assert(sizeof(Slot) == 64, "Slot is one 64-byte record");
 // kernel ids recorded in pc_pairs_profile.kernel
 constexpr int kKernGram = 1, kKernDirect = 2, kKernSorted = 3, kKernComp = 4, kKernTc = 5, kKernKey = 6,
-              kKernRow = 7, kKernSortedCount = 8, kKernCompSorted = 9;
+              kKernRow = 7, kKernSortedCount = 8, kKernCompSorted = 9, kKernSortedTc = 10;
 
 // FLAT work claims (guided self-scheduling): claim c of stage k covers columns
 // [b0[k] + (c - c0[k]) * s[k], + s[k]) of the flat (row tile, window column) space.  Stage k
@@ -437,6 +437,7 @@ struct PairsArgs {
     long long blk_cols;  // FLAT: columns per block of the transposed claim order (pairs_kernel.cuh)
     long long win_blks;  // FLAT: blocks per tile window
     long long st_c0[kMaxStages + 1], st_b0[kMaxStages], st_s[kMaxStages];
+    int tc_split;        // SORTED sum: the dense chunks tcs_takes() accepts are left to pairs_tcs_kernel
 };
 
 __device__ __forceinline__ int steps_for_dev(int n, int i) {
@@ -447,6 +448,7 @@ __device__ __forceinline__ int steps_for_dev(int n, int i) {
 
 #include "pairs_kernel.cuh"
 #include "pairs_tc.cuh"
+#include "pairs_tcsum.cuh"
 #include "pairs_key.cuh"
 #include "pairs_row.cuh"
 
@@ -480,7 +482,8 @@ __global__ void finalize_kernel(const Slot* __restrict__ slots, int nslots, cons
                                 int kernel_id, long long pairs_per_chunk) {
     __shared__ unsigned long long sc[256], sk[256], sp[kNumPaths + 1][256];
     __shared__ double ss[256];
-    unsigned long long c = 0, k = 0, pth[kNumPaths + 1] = {0, 0, 0, 0, 0, 0};
+    __shared__ unsigned long long stc[256];
+    unsigned long long c = 0, k = 0, pth[kNumPaths + 1] = {0, 0, 0, 0, 0, 0}, tcc = 0;
     double s = 0.0;
     for (int q = threadIdx.x; q < nslots; q += blockDim.x) {
         c += slots[q].count;
@@ -488,15 +491,17 @@ __global__ void finalize_kernel(const Slot* __restrict__ slots, int nslots, cons
         s += slots[q].sum;
         for (int u = 0; u < kNumPaths; ++u) pth[u] += slots[q].path[u];
         pth[kNumPaths] += slots[q].rescans;
+        tcc += slots[q].pad[0];
     }
     if (claims_hold_sums)
         for (int q = threadIdx.x; q < nclaims; q += blockDim.x) s += claims[q];
-    sc[threadIdx.x] = c; sk[threadIdx.x] = k; ss[threadIdx.x] = s;
+    sc[threadIdx.x] = c; sk[threadIdx.x] = k; ss[threadIdx.x] = s; stc[threadIdx.x] = tcc;
     for (int u = 0; u <= kNumPaths; ++u) sp[u][threadIdx.x] = pth[u];
     __syncthreads();
     for (int h = blockDim.x / 2; h > 0; h >>= 1) {
         if (threadIdx.x < h) {
             sc[threadIdx.x] += sc[threadIdx.x + h];
+            stc[threadIdx.x] += stc[threadIdx.x + h];
             sk[threadIdx.x] += sk[threadIdx.x + h];
             ss[threadIdx.x] += ss[threadIdx.x + h];
             for (int u = 0; u <= kNumPaths; ++u) sp[u][threadIdx.x] += sp[u][threadIdx.x + h];
@@ -521,6 +526,7 @@ __global__ void finalize_kernel(const Slot* __restrict__ slots, int nslots, cons
         prof->chunks_near += (long long)sp[kPathNear][0];
         prof->chunks_far += (long long)sp[kPathFar][0];
         prof->chunks_edge += (long long)sp[kPathEdge][0];
+        prof->chunks_tc += (long long)stc[0];
         prof->rows_rescanned += (long long)sp[kNumPaths][0];
         prof->exact_checks += (long long)sk[0];
         prof->claims += claims_total;
@@ -736,7 +742,7 @@ __global__ void blk_box_kernel(const T* __restrict__ xyz, long long n, int nblk,
 }
 
 struct WsLayout {
-    size_t pts, stats, prof, red, slots, claims, tc_a, tc_b, tc_cand, tc_cnt, srt, srt_temp, total;
+    size_t pts, stats, prof, red, slots, claims, claims_tc, tc_a, tc_b, tc_cand, tc_cnt, srt, srt_temp, total;
 };
 WsLayout ws_layout(long long n) {
     WsLayout l;
@@ -745,9 +751,10 @@ WsLayout ws_layout(long long n) {
     l.stats = 2 * pair_bytes;
     l.prof = l.stats + 256;  // pc_pairs_profile of the last call
     l.red = l.prof + 256;    // kRedBlocks float64 partials of the claim sums
-    l.slots = l.red + kRedBlocks * sizeof(double);
+    l.slots = l.red + 2 * kRedBlocks * sizeof(double);  // FFMA claims, then tensor-core claims
     l.claims = align_up(l.slots + (size_t)max_slots(n) * sizeof(Slot), 256);
-    l.tc_a = align_up(l.claims + (size_t)kClaimsCap * sizeof(double), 1024);
+    l.claims_tc = align_up(l.claims + (size_t)kClaimsCap * sizeof(double), 256);
+    l.tc_a = align_up(l.claims_tc + (size_t)kClaimsCap * sizeof(double), 1024);
     const TcGeom g = tc_geom(n < 0 ? 0 : n);  // tensor-core count kernel operands (64 B per staged point)
     l.tc_b = align_up(l.tc_a + (size_t)g.n_rows * 64, 1024);
     l.tc_cand = align_up(l.tc_b + (size_t)g.n_ext * 64, 256);
@@ -907,6 +914,76 @@ int dispatch_cfg(PairsArgs args, bool flat, TileSel ts, long long cap, int* nslo
         return launch_pairs<WARPS, R, W, DIRECT, true, COMP, SORTED>(args, cap, nslots, nclaims, s);
     }
     return launch_pairs<WARPS, R, W, DIRECT, false, COMP>(args, cap, nslots, nclaims, s);
+}
+
+// The tensor-core Gram chunks of a sorted fp32 sum (pairs_tcsum.cuh): launched after the
+// FFMA sorted kernel (which left these chunks alone) over the same tiles.  PAIRCOUNT_TCSUM=0
+// in the environment keeps every chunk on the FFMA kernel (A/B runs).
+#ifndef PC_TCSUM
+#define PC_TCSUM 1
+#endif
+bool tcs_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("PAIRCOUNT_TCSUM");
+        return PC_TCSUM && !(e && e[0] == '0');
+    }();
+    return on && 32 * kBig.r == kTcsT && kBig.w == kTcsW;
+}
+int launch_tcs(const PairsArgs& p, TileSel ts, double* claims_tc, Slot* slots, long long cap, int* nslots,
+               int* nparts, cudaStream_t s) {
+    TcsArgs a{};
+    a.xyz = (const float*)p.xyz;
+    a.blk_box = p.blk_box;
+    a.st = p.st;
+    a.slots = slots;
+    a.claim_sums = claims_tc;
+    a.work_ctr = p.work_ctr;
+    a.dtype = p.dtype;
+    a.n = p.n;
+    a.lo = p.lo;
+    a.hi = p.hi;
+    a.tstride = ts.tstride;
+    a.toff = ts.toff;
+    a.n_tiles = tiles_of(p.lo, p.hi, kTcsT, ts);
+    a.L = (long long)(kTcsT - 1) + (p.n >> 1);
+    a.cpw = (a.L + kTcsW - 1) / kTcsW;
+    a.items = (long long)a.n_tiles * a.cpw;
+    // items per claim: the smallest power of two keeping the float64 partials (kTcsParts per
+    // claim) within kClaimsCap
+    const int grid = num_sms();
+    long long S = 1;
+    while (S * (kClaimsCap / kTcsParts) < a.items) S *= 2;
+    a.S = S;
+    a.nclaims = (a.items + S - 1) / S;
+    *nslots = 0;
+    *nparts = 0;
+    if (a.n_tiles == 0) return PC_OK;
+    if (grid > cap) return arg_fail("workspace too small for the CTA slots");
+    static thread_local bool attr_set[64] = {false};
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (!attr_set[dev & 63]) {
+        CK(cudaFuncSetAttribute(pairs_tcs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcsSmem));
+        attr_set[dev & 63] = true;
+    }
+    CK(cudaMemsetAsync(a.work_ctr, 0, sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(claims_tc, 0, (size_t)a.nclaims * kTcsParts * sizeof(double), s));
+    EvPair* ev = nullptr;
+    if (g_timing && g_ev_used < 4096) {
+        if (g_ev_used == g_ev_made) {
+            CK(cudaEventCreate(&g_ev[g_ev_made].a));
+            CK(cudaEventCreate(&g_ev[g_ev_made].b));
+            ++g_ev_made;
+        }
+        ev = &g_ev[g_ev_used++];
+        CK(cudaEventRecord(ev->a, s));
+    }
+    pairs_tcs_kernel<<<grid, kTcsWarps * 32, kTcsSmem, s>>>(a);
+    CK_LAUNCH("pairs_tcs_kernel");
+    if (ev) CK(cudaEventRecord(ev->b, s));
+    *nslots = grid;
+    *nparts = (int)(a.nclaims * kTcsParts);
+    return PC_OK;
 }
 
 // Balanced counts on the tensor cores (pairs_tc.cuh): operands staged once per call,
@@ -1215,11 +1292,18 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
         }
         return PC_OK;
     }
-    const int kern_id = !direct ? (sorted_count ? kKernSortedCount : kKernGram)
-                                : comp ? (sorted ? kKernCompSorted : kKernComp) : sorted ? kKernSorted : kKernDirect;
+    // sorted fp32 sums: the Gram chunks the tensor cores can take go to pairs_tcs_kernel (ranges
+    // starting on a 32-point block, so both kernels see the same per-32 boxes of every tile)
+    const bool use_tcs_call = sorted && !comp && n >= kSmallN && tcs_enabled();
+    double* claims_tc = (double*)(ws + lay.claims_tc);
     for (int k = 0; k < nranges; ++k) {
         const long long lo = bounds[k], hi = bounds[k + 1];
-        int nslots = 0, nclaims = 0, trows = 1;
+        const bool use_tcs = use_tcs_call && lo % 32 == 0;
+        args.tc_split = use_tcs ? 1 : 0;
+        const int kern_id = !direct ? (sorted_count ? kKernSortedCount : kKernGram)
+                                    : comp ? (sorted ? kKernCompSorted : kKernComp)
+                                           : sorted ? (use_tcs ? kKernSortedTc : kKernSorted) : kKernDirect;
+        int nslots = 0, nclaims = 0, trows = 1, ntcparts = 0;
         long long ppc = 0;
         if (hi > lo && n >= 2) {
             args.lo = (int)lo;
@@ -1250,18 +1334,31 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
                 CK_LAUNCH("pairs_f64_kernel");
                 nslots += g2;
             }
+            if (use_tcs) {
+                int ntc = 0;
+                rc = launch_tcs(args, ts, claims_tc, slots + nslots, cap - nslots, &ntc, &ntcparts, s);
+                if (rc) return rc;
+                nslots += ntc;
+            }
         }
         const long long pr = hi > lo && n >= 2 ? tile_sel_pairs(n, lo, hi, trows, ts, schedule) : 0;
         const double* csum = claims;
         int ncs = nclaims;
-        if (direct && nclaims > 8 * kRedBlocks) {
+        if (direct && (nclaims > 8 * kRedBlocks || ntcparts > 0)) {
+            // fixed-order two-stage reduction: FFMA claims into red[0, 128), tensor-core claim
+            // partials into red[128, 256)
             double* red = (double*)(ws + lay.red);
             claims_reduce_kernel<<<kRedBlocks, 256, 0, s>>>(claims, nclaims, red);
             CK_LAUNCH("claims_reduce_kernel");
             csum = red;
             ncs = kRedBlocks;
+            if (ntcparts > 0) {
+                claims_reduce_kernel<<<kRedBlocks, 256, 0, s>>>(claims_tc, ntcparts, red + kRedBlocks);
+                CK_LAUNCH("claims_reduce_kernel");
+                ncs = 2 * kRedBlocks;
+            }
         }
-        finalize_kernel<<<1, 256, 0, s>>>(slots, nslots, csum, ncs, direct ? 1 : 0, nclaims, st, dtype, pr,
+        finalize_kernel<<<1, 256, 0, s>>>(slots, nslots, csum, ncs, direct ? 1 : 0, nclaims + ntcparts / (int)kTcsParts, st, dtype, pr,
                                           direct ? (comp ? 2 : 1) : 0,
                                           dres + k, prof, kern_id, ppc);
         CK_LAUNCH("finalize_kernel");

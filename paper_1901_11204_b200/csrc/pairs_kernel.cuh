@@ -53,6 +53,37 @@ __device__ __forceinline__ float2 f2_rsub(float a, float2 b) {  // a - b, a broa
     return *reinterpret_cast<float2*>(&dd);
 }
 
+// The sorted sum's per-chunk geometry: tile centre o, squared box gap, |a|max + |b|max.
+// Shared by the FFMA kernel and the producers here, with explicit round-to-nearest
+// operations so both compile to the same arithmetic and agree on every chunk.
+struct ChunkGeom {
+    float o[3];
+    float gap2, ab;
+};
+__device__ __forceinline__ ChunkGeom chunk_geom(const float tmin[3], const float tmax[3], const float cl[3],
+                                                const float ch[3]) {
+    ChunkGeom g;
+    float gap2 = 0.f, rt2 = 0.f, bm2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        g.o[k] = __fmul_rn(0.5f, __fadd_rn(tmin[k], tmax[k]));
+        const float d = fmaxf(0.f, fmaxf(__fsub_rn(cl[k], tmax[k]), __fsub_rn(tmin[k], ch[k])));
+        gap2 = __fadd_rn(gap2, __fmul_rn(d, d));
+        const float ht = __fmul_rn(0.5f, __fsub_rn(tmax[k], tmin[k]));
+        rt2 = __fadd_rn(rt2, __fmul_rn(ht, ht));
+        const float bb = fmaxf(fabsf(__fsub_rn(cl[k], g.o[k])), fabsf(__fsub_rn(ch[k], g.o[k])));
+        bm2 = __fadd_rn(bm2, __fmul_rn(bb, bb));
+    }
+    g.gap2 = gap2;
+    g.ab = __fadd_rn(__fsqrt_rn(rt2), __fsqrt_rn(bm2));
+    return g;
+}
+// a dense chunk the tensor-core sum kernel takes (pairs_tcsum.cuh)
+__device__ __forceinline__ bool tcs_takes(const ChunkGeom& g) {
+    return g.gap2 > 4.5f && g.ab <= 3e4f &&
+           __fmul_rn(7.152557373046875e-07f, __fmul_rn(g.ab, g.ab)) <= __fmul_rn(3.125e-6f, __fadd_rn(1.f, g.gap2));
+}
+
 // Pair-buffer layouts (one entry per column pair k, k+1):
 //   PS = 2 float4: (x, x', y, y')(z, z', w, w')                       Gram / direct
 //   PS = 3 float4: (x, x', y, y')(z, z', xl, xl')(yl, yl', zl, zl')   compensated direct:
@@ -564,7 +595,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             float2 acc[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) acc[r] = make_float2(0.f, 0.f);
-            bool gram = false, no_contact = false;
+            bool gram = false, no_contact = false, tc_skip = false;
             unsigned near_fl = 0;  // SORTED near chunks: rows with some p < thr2
             float o[3] = {0.f, 0.f, 0.f};
             if (SORTED && dense) {
@@ -581,22 +612,21 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                     cmn[0] = lo4.x; cmn[1] = lo4.y; cmn[2] = lo4.z;
                     cmx[0] = hi4.x; cmx[1] = hi4.y; cmx[2] = hi4.z;
                 }
-                float gap2 = 0.f, rt2 = 0.f, bm2 = 0.f;
+                float cl[3], ch[3];
 #pragma unroll
                 for (int k = 0; k < 3; ++k) {
-                    const float cl = warp_min_f(cmn[k]), ch = warp_max_f(cmx[k]);
-                    o[k] = 0.5f * (tmin[k] + tmax[k]);
-                    const float g = fmaxf(0.f, fmaxf(cl - tmax[k], tmin[k] - ch));
-                    gap2 += g * g;
-                    const float ht = 0.5f * (tmax[k] - tmin[k]);
-                    rt2 += ht * ht;
-                    const float bb = fmaxf(fabsf(cl - o[k]), fabsf(ch - o[k]));
-                    bm2 += bb * bb;
+                    cl[k] = warp_min_f(cmn[k]);
+                    ch[k] = warp_max_f(cmx[k]);
                 }
+                const ChunkGeom cg = chunk_geom(tmin, tmax, cl, ch);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) o[k] = cg.o[k];
+                const float gap2 = cg.gap2, ab = cg.ab;
+                // a chunk the tensor-core kernel evaluates (pairs_tcsum.cuh): nothing to do here
+                tc_skip = !COMP && a.tc_split && tcs_takes(cg);
                 // 8u (|a| + |b|)^2 <= 5e-6 (1 + dmin^2), u = 2^-24 -- written as the same
                 // inequality 5u (..)^2 <= 3.125e-6 (..): eight roundings of terms of at most
                 // (|a| + |b|)^2 against p >= 1 + dmin^2
-                const float ab = sqrtf(rt2) + sqrtf(bm2);
 #ifndef PC_GRAM_HALVES
 #define PC_GRAM_HALVES 1
 #endif
@@ -608,12 +638,14 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
 #endif
                 // compensated (float64) points: a = (hi - o) + lo rounds once more: 10u instead of 8u
                 constexpr float kGramU = COMP ? 3.725290298461914e-07f : 2.98023223876953125e-07f;
-                gram = gap2 > PC_GRAM_GAP2 && kGramU * ab * ab <= PC_GRAM_BUDGET * (1.f + gap2);
+                gram = !tc_skip && gap2 > PC_GRAM_GAP2 && kGramU * ab * ab <= PC_GRAM_BUDGET * (1.f + gap2);
                 // boxes more than 1.5 apart: no contact, so no rescan however large the chunk's
                 // sums (on sorted points the chunks next to a tile have many near terms)
                 no_contact = gap2 > 2.25f;
             }
-            if (SORTED && gram) {
+            if (SORTED && tc_skip) {
+                // evaluated on the tensor cores (no contact: gap > 2.12)
+            } else if (SORTED && gram) {
                 // columns to tile-local form in place: (bx, by, bz, B = |b|^2) per point
                 // (compensated entries: b = (hi - o) + lo, written over the entry's first two float4)
                 float4* spw = const_cast<float4*>(sp);
@@ -788,11 +820,13 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 sum += (double)cs;
                 fl |= (cs > sum_flag ? 1u : 0u) << r;  // conservative: a contact's term alone exceeds it
             }
-            count_path((SORTED && gram) ? kPathGram
-                       : !dense ? kPathEdge
-                       : (SORTED && !COMP && !no_contact) ? kPathNear
-                       : (SORTED && COMP) ? (no_contact ? kPathFar : kPathMain)
-                       : SORTED ? kPathFar : kPathMain, 1u);
+            if (!(SORTED && tc_skip)) {
+                count_path((SORTED && gram) ? kPathGram
+                           : !dense ? kPathEdge
+                           : (SORTED && !COMP && !no_contact) ? kPathNear
+                           : (SORTED && COMP) ? (no_contact ? kPathFar : kPathMain)
+                           : SORTED ? kPathFar : kPathMain, 1u);
+            }
             if (SORTED && no_contact) fl = 0;  // also covers the Gram chunks, whose columns were rewritten
             if (SORTED && !COMP && dense && !no_contact) fl = near_fl;  // exact candidates, not chunk sums
             if (SORTED && gram && staged_tile == tile) {

@@ -1,0 +1,531 @@
+// Tensor-core Gram chunks of the sorted inverse-square sum (included by paircount.cu
+// inside its anonymous namespace, after pairs_tc.cuh).
+//
+// The sorted sum kernel (pairs_kernel.cuh, SORTED + DIRECT) evaluates most of its
+// chunks in tile-local Gram form, p = A_i + B_j - 2 a_i.b_j with a = q_i - o,
+// b = q_j - o about the row tile's centre o: a matrix product plus a per-pair
+// epilogue.  Here that product runs on the 5th-generation tensor cores and the
+// FFMA pipe is left with the epilogue alone:
+//   * tcgen05.mma kind::tf32, M = 128 rows, N = 128 columns, K = 24: every operand
+//     split three ways into exact tf32 pieces x = h + m + l (h, m the
+//     round-to-nearest tf32 of x and of x - h, l = x - h - m), products
+//       a_h b_h + a_h b_m + a_m b_h + a_h b_l + a_m b_m + a_l b_h   (the b side carries -2)
+//       + (A_h + A_m + A_l) + (B_h + B_m + B_l)
+//     all exact in fp32 (dropped terms <= 2^-33 |a||b|); what remains is the tensor
+//     core's fp32 accumulation, measured at <= 3.2u (1 + (|a| + |b|)^2) on 300k pairs of
+//     nine geometries (scripts/tc_prec_proto.cu: 2.1-3.2u; the FFMA2 Gram form measures
+//     2.2-4.0u there).  Bound used for a chunk (DESIGN.md §3 "Error budget"): A_i and
+//     B_j roundings 4u|a|^2 + 3u|b|^2, the subtractions a = q - o, b = q - o 2u(|a|+|b|)^2,
+//     the accumulation taken as 6u (1 + (|a|+|b|)^2): <= 6u + 12u (|a|max + |b|max)^2.
+//   * epilogue: the accumulator's p values, eight terms per two reciprocals, packed:
+//     1/a + 1/c + 1/e + 1/g = ((a+c) eg + (e+g) ac) / (ac eg) in the x lanes (even
+//     columns) and the y lanes (odd columns) -- 8 FFMA2/FMUL2/FADD2 + 2 MUFU per eight
+//     pairs, against 11 + 2 for the FFMA2 Gram loop without the product.
+// Which chunks: the dense chunks (every cell owned) of whole 256-row tiles whose boxes
+// satisfy tcs_takes() -- 12u (|a|+|b|)^2 <= 3.125e-6 (1 + dmin^2), dmin^2 > 4.5 (no
+// contact in the chunk, so no contact test here), |a|+|b| <= 3e4 (the four-term products
+// stay finite).  The FFMA sorted kernel runs first over the same (tile, chunk) space and
+// skips exactly these chunks: both evaluate chunk_geom() on the same boxes with explicit
+// round-to-nearest operations, so every chunk has one owner.
+//
+// Work: items (row tile, chunk) of the FFMA kernel's 256 x 256 geometry in tile-major
+// order, claimed S at a time from one counter.  Each item is four accumulators of
+// 128 x 128: (row half h, column half q).  CTA = 13 warps, one per SM:
+//   warp 0       MMA issuer (one elected thread)
+//   warps 1-4    producers: claim items, classify them (chunk_geom on the per-32 boxes),
+//                build the row operand A (256 rows, on a tile change) and the column
+//                operand B (256 columns, every item) in shared memory from the sorted
+//                points -- K-major no-swizzle layout, 768 B per 8 points
+//   warps 5-12   epilogue: group h = (w - 5) / 4 drains the row-half-h accumulators
+//                (TMEM lanes 32 (w % 4) ..), one column half at a time: 128 values into
+//                registers, the accumulator released, then the arithmetic -- so the
+//                next MMA, the other column half's drain and this arithmetic overlap.
+// Sums: each epilogue warp keeps a float64 partial per claim (its rows and columns of
+// the claim's items, in item order) and writes it to claim_sums[claim * 8 + warp]: the
+// claim's composition is fixed by its index, so the float64 total is bit-reproducible.
+
+constexpr int kTcsT = 256, kTcsW = 256;           // the FFMA sorted kernel's tile and chunk
+#ifndef PC_TCS_BF16
+#define PC_TCS_BF16 1  // operands as three bf16 pieces, kind::f16, K = 32 (0: three tf32 pieces, kind::tf32, K = 24)
+#endif
+#if PC_TCS_BF16
+#define PC_TCS_KIND "f16"
+#else
+#define PC_TCS_KIND "tf32"
+#endif
+constexpr int kTcsKC = PC_TCS_BF16 ? 4 : 6;        // 16-byte K-chunks per point
+constexpr int kTcsGroup = kTcsKC * 128;            // bytes per 8 points
+constexpr int kTcsOp = 256 / 8 * kTcsGroup;        // bytes per 256-point operand (16 KB bf16, 24 KB tf32)
+constexpr int kTcsHalf = kTcsOp / 2;               // 128 points
+#ifndef PC_TCS_NQ
+#define PC_TCS_NQ 1  // column pieces per row half: accumulators of 256 / NQ columns, 2 NQ of them in TMEM
+#endif
+constexpr int kTcsNQ = PC_TCS_NQ, kTcsNP = 256 / kTcsNQ, kTcsNAcc = 2 * kTcsNQ;
+#ifndef PC_TCS_ROUND
+#define PC_TCS_ROUND 128  // accumulator columns per drain round (loaded before the accumulator is released)
+#endif
+constexpr int kTcsRound = PC_TCS_ROUND;
+static_assert(kTcsNAcc * kTcsNP == 512 && kTcsNP % kTcsRound == 0 && kTcsRound % 32 == 0, "TMEM: 512 columns");
+#ifndef PC_TCS_STAGES
+#define PC_TCS_STAGES 5
+#endif
+constexpr int kTcsStages = PC_TCS_STAGES;
+#ifndef PC_TCS_KSTEPS  // K-steps per accumulator (K = 16 bf16 / 8 tf32 each); a debug knob for A/B of the MMA cost
+#define PC_TCS_KSTEPS (PC_TCS_BF16 ? 2 : 3)
+#endif
+#ifndef PC_TCS_PROD
+#define PC_TCS_PROD 4  // producer warps (13 warps: 16 warp slots of 128 registers; 3 and 7 measured slower)
+#endif
+constexpr int kTcsProd = PC_TCS_PROD, kTcsEpi = 8, kTcsWarps = 1 + kTcsProd + kTcsEpi;
+constexpr int kTcsPT = kTcsProd * 32, kTcsPR = (256 + kTcsPT - 1) / kTcsPT;  // producer threads, points per thread
+constexpr int kTcsSmem = 2 * kTcsOp + kTcsStages * kTcsOp + 1024;
+constexpr long long kTcsParts = kTcsEpi;           // float64 partials per claim
+// instruction descriptor: D f32, A/B bf16 (f16 kind) or tf32, both K-major, N = kTcsNP, M = 128
+constexpr uint32_t kTcsIdesc = (1u << 4) | ((PC_TCS_BF16 ? 1u : 2u) << 7) | ((PC_TCS_BF16 ? 1u : 2u) << 10) |
+                               ((uint32_t)(kTcsNP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+
+// exact three-way splits x = h + m + l: tf32 (round to nearest, ties away) or bf16 (nearest even)
+__device__ __forceinline__ float bf16r(float x) {  // round to nearest even on the integer pipe (finite x)
+    const unsigned u = __float_as_uint(x);
+    return __uint_as_float((u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u);
+}
+__device__ __forceinline__ void split3(float x, float& h, float& m, float& l) {
+    h = PC_TCS_BF16 ? bf16r(x) : tf32_rna(x);
+    const float r = __fsub_rn(x, h);
+    m = PC_TCS_BF16 ? bf16r(r) : tf32_rna(r);
+    l = PC_TCS_BF16 ? bf16r(__fsub_rn(r, m)) : __fsub_rn(r, m);  // exact either way (<= 8 / 2 significant bits)
+}
+__device__ __forceinline__ unsigned bf2(float lo, float hi) {  // two exact bf16 values, lo at the lower address
+    return (__float_as_uint(hi) & 0xffff0000u) | (__float_as_uint(lo) >> 16);
+}
+__device__ __forceinline__ unsigned tcs_off(int p, int kc) { return (unsigned)((p >> 3) * kTcsGroup + kc * 128 + (p & 7) * 16); }
+// smem matrix descriptor, K-major no swizzle: K-chunks 128 B apart (LBO), 8-point groups kTcsGroup B apart (SBO)
+__device__ __forceinline__ uint64_t tcs_desc(unsigned saddr) {
+    return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(128u >> 4) << 16) | ((uint64_t)((unsigned)kTcsGroup >> 4) << 32) |
+           (1ull << 46);
+}
+// Row p of the A operand: a = q - o and A = 1 + |a|^2, split.  K order (bf16, 32):
+//   a_h a_h a_h a_m a_m a_m a_l a_l | A_h A_m A_l | 1 1 1 | 0 0     (each a_* three coordinates)
+// against the B order  b_h b_m b_l b_h b_m b_l b_h b_m | 1 1 1 | B_h B_m B_l | 0 0:
+// a_h.b_{h,m,l} + a_m.b_{h,m,l} + a_l.b_{h,m} + A + B (only a_l.b_l, <= 2^-32 |a||b|, dropped).
+// tf32 (24): a_h a_h a_m a_h a_m a_l | A_h A_m A_l | 1 1 1 against b_h b_m b_h b_l b_m b_h | 1 1 1 | B_h B_m B_l.
+__device__ __forceinline__ void tcs_write_row(unsigned char* d, int p, float ax, float ay, float az, float A) {
+    float xh, xm, xl, yh, ym, yl, zh, zm, zl, Ah, Am, Al;
+    split3(ax, xh, xm, xl);
+    split3(ay, yh, ym, yl);
+    split3(az, zh, zm, zl);
+    split3(A, Ah, Am, Al);
+#if PC_TCS_BF16
+    const float one = 1.f;
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 0)) = make_uint4(bf2(xh, yh), bf2(zh, xh), bf2(yh, zh), bf2(xh, yh));
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 1)) = make_uint4(bf2(zh, xm), bf2(ym, zm), bf2(xm, ym), bf2(zm, xm));
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 2)) = make_uint4(bf2(ym, zm), bf2(xl, yl), bf2(zl, xl), bf2(yl, zl));
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 3)) = make_uint4(bf2(Ah, Am), bf2(Al, one), bf2(one, one), 0u);
+#else
+    *reinterpret_cast<float4*>(d + tcs_off(p, 0)) = make_float4(xh, yh, zh, xh);
+    *reinterpret_cast<float4*>(d + tcs_off(p, 1)) = make_float4(yh, zh, xm, ym);
+    *reinterpret_cast<float4*>(d + tcs_off(p, 2)) = make_float4(zm, xh, yh, zh);
+    *reinterpret_cast<float4*>(d + tcs_off(p, 3)) = make_float4(xm, ym, zm, xl);
+    *reinterpret_cast<float4*>(d + tcs_off(p, 4)) = make_float4(yl, zl, Ah, Am);
+    *reinterpret_cast<float4*>(d + tcs_off(p, 5)) = make_float4(Al, 1.f, 1.f, 1.f);
+#endif
+}
+// Column p of the B operand from -2b and B = |b|^2
+__device__ __forceinline__ void tcs_write_col(unsigned char* d, int p, float bx, float by, float bz, float B) {
+    float xh, xm, xl, yh, ym, yl, zh, zm, zl, Bh, Bm, Bl;
+    split3(bx, xh, xm, xl);
+    split3(by, yh, ym, yl);
+    split3(bz, zh, zm, zl);
+    split3(B, Bh, Bm, Bl);
+#if PC_TCS_BF16
+    const float one = 1.f;
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 0)) = make_uint4(bf2(xh, yh), bf2(zh, xm), bf2(ym, zm), bf2(xl, yl));
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 1)) = make_uint4(bf2(zl, xh), bf2(yh, zh), bf2(xm, ym), bf2(zm, xl));
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 2)) = make_uint4(bf2(yl, zl), bf2(xh, yh), bf2(zh, xm), bf2(ym, zm));
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 3)) = make_uint4(bf2(one, one), bf2(one, Bh), bf2(Bm, Bl), 0u);
+#else
+    *reinterpret_cast<float4*>(d + tcs_off(p, 0)) = make_float4(xh, yh, zh, xm);
+    *reinterpret_cast<float4*>(d + tcs_off(p, 1)) = make_float4(ym, zm, xh, yh);
+    *reinterpret_cast<float4*>(d + tcs_off(p, 2)) = make_float4(zh, xl, yl, zl);
+    *reinterpret_cast<float4*>(d + tcs_off(p, 3)) = make_float4(xm, ym, zm, xh);
+    *reinterpret_cast<float4*>(d + tcs_off(p, 4)) = make_float4(yh, zh, 1.f, 1.f);
+    *reinterpret_cast<float4*>(d + tcs_off(p, 5)) = make_float4(1.f, Bh, Bm, Bl);
+#endif
+}
+
+struct TcsArgs {
+    const float* xyz;  // sorted points (fp32, 12 B each)
+    const float4* blk_box;
+    const PrepStats* st;
+    Slot* slots;
+    double* claim_sums;  // kTcsParts per claim
+    unsigned long long* work_ctr;
+    int dtype, n, lo, hi;
+    int tstride, toff, n_tiles;
+    long long L;       // window length (T - 1 + n/2)
+    long long cpw;     // chunks per window
+    long long items;   // n_tiles * cpw
+    long long S;       // items per claim
+    long long nclaims;
+};
+
+__global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs a) {
+    extern __shared__ __align__(1024) unsigned char tcs_smem[];
+    unsigned char* base = (unsigned char*)(((uintptr_t)tcs_smem + 1023) & ~(uintptr_t)1023);
+    unsigned char* sA = base;              // [2][kTcsOp]
+    unsigned char* sB = base + 2 * kTcsOp; // [kTcsStages][kTcsOp]
+    __shared__ __align__(8) unsigned long long bar_bfull[kTcsStages], bar_bempty[kTcsStages];
+    __shared__ __align__(8) unsigned long long bar_afull[2], bar_aempty[2];
+    __shared__ __align__(8) unsigned long long bar_accfull[kTcsNAcc], bar_accempty[kTcsNAcc];  // index h NQ + q
+    __shared__ long long s_item[kTcsStages];  // claim << 2 | abuf << 1 | new tile; -1 = done
+    __shared__ long long s_meta[kTcsNAcc];    // MMA -> epilogue: the accumulator's claim (-1 = done)
+    __shared__ long long s_pclaim[2];
+    __shared__ unsigned s_tmem;
+    __shared__ unsigned s_items;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool skip = f64_takes(*a.st, a.dtype, false);  // the float64 kernel takes this call
+    if (skip || a.n_tiles == 0) {
+        if (threadIdx.x == 0) a.slots[blockIdx.x] = Slot{};
+        return;
+    }
+    const unsigned b_full = (unsigned)__cvta_generic_to_shared(bar_bfull);
+    const unsigned b_empty = (unsigned)__cvta_generic_to_shared(bar_bempty);
+    const unsigned a_full = (unsigned)__cvta_generic_to_shared(bar_afull);
+    const unsigned a_empty = (unsigned)__cvta_generic_to_shared(bar_aempty);
+    const unsigned acc_full = (unsigned)__cvta_generic_to_shared(bar_accfull);
+    const unsigned acc_empty = (unsigned)__cvta_generic_to_shared(bar_accempty);
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < kTcsStages; ++k) {
+            mbar_init(b_full + 8 * k, kTcsProd);
+            mbar_init(b_empty + 8 * k, 1);
+        }
+        for (int k = 0; k < 2; ++k) {
+            mbar_init(a_full + 8 * k, kTcsProd);
+            mbar_init(a_empty + 8 * k, 1);
+        }
+        for (int k = 0; k < kTcsNAcc; ++k) {
+            mbar_init(acc_full + 8 * k, 2);  // the MMA thread's hand-off + the MMAs' commit
+            mbar_init(acc_empty + 8 * k, 4);
+        }
+        mbar_init_fence();
+        s_items = 0;
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            (unsigned)__cvta_generic_to_shared(&s_tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const unsigned tmem = s_tmem;
+    const int n = a.n;
+    const int steps_min = (n & 1) ? (n - 1) >> 1 : (n >> 1) - 1;
+    double sum = 0.0;
+
+    if (warp == 0) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            long long it = 0;
+            long long aloads[2] = {0, 0};
+            int cur_abuf = -1, sg = 0;
+            unsigned items = 0;
+            // (the operands stay inside the 256 KB window of the 14-bit address field: offsets add)
+            const uint64_t dA0 = tcs_desc((unsigned)__cvta_generic_to_shared(sA));
+            const uint64_t dB0 = tcs_desc((unsigned)__cvta_generic_to_shared(sB));
+            for (;; ++it, sg = sg + 1 == kTcsStages ? 0 : sg + 1) {
+                mbar_wait(b_full + 8 * sg, (unsigned)((it / kTcsStages) & 1));
+                const long long tag = s_item[sg];
+                if (tag < 0) {
+                    for (int k = 0; k < kTcsNAcc; ++k) {
+                        if (it >= 1) mbar_wait(acc_empty + 8 * k, (unsigned)((it - 1) & 1));
+                        s_meta[k] = -1;
+                        mbar_arrive_plain(acc_full + 8 * k);
+                        mbar_arrive_plain(acc_full + 8 * k);
+                    }
+                    break;
+                }
+                ++items;
+                const int ab = (int)((tag >> 1) & 1);
+                if (tag & 1) {  // first item of a tile: its A landed; the previous A is free after the MMAs so far
+                    if (cur_abuf >= 0) tc_commit(a_empty + 8 * cur_abuf);
+                    mbar_wait(a_full + 8 * ab, (unsigned)(aloads[ab] & 1));
+                    ++aloads[ab];
+                    cur_abuf = ab;
+                }
+                // descriptors: the base descriptor plus the 16-byte-unit offset (start address field)
+                const uint64_t da0 = dA0 + (uint64_t)((ab * kTcsOp) >> 4), db0 = dB0 + (uint64_t)((sg * kTcsOp) >> 4);
+#pragma unroll
+                for (int kk = 0; kk < kTcsNAcc; ++kk) {
+                    // accumulator k = (row half h, column piece q) = h NQ + q, in the order the two
+                    // epilogue groups release them: (0,0), (1,0), (0,1), (1,1), ...
+                    const int h = kk & 1, q = kk >> 1, k = h * kTcsNQ + q;
+                    if (it >= 1) mbar_wait(acc_empty + 8 * k, (unsigned)((it - 1) & 1));
+                    s_meta[k] = tag >> 2;
+                    mbar_arrive_plain(acc_full + 8 * k);  // release: the epilogue reads s_meta after its wait
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint64_t da = da0 + (uint64_t)((h * kTcsHalf) >> 4),
+                                   db = db0 + (uint64_t)((q * (kTcsNP / 8) * kTcsGroup) >> 4);
+#pragma unroll
+                    for (int ks = 0; ks < PC_TCS_KSTEPS; ++ks) {
+                        asm volatile(
+                            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                            " tcgen05.mma.cta_group::1.kind::" PC_TCS_KIND " [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (unsigned)(k * kTcsNP)),
+                            "l"(da + (uint64_t)(16 * ks)), "l"(db + (uint64_t)(16 * ks)), "r"(kTcsIdesc), "r"(ks));
+                    }
+                    tc_commit(acc_full + 8 * k);
+                }
+                tc_commit(b_empty + 8 * sg);
+            }
+            s_items = items;
+        }
+    } else if (warp <= kTcsProd) {
+        // ---------------- producers: claims, classification, operands
+        // Per claim: the items are classified 32 at a time (lane l takes item ub + l: its tile's
+        // and chunk's per-32 boxes -- the same union of boxes the FFMA kernel reduces across its
+        // lanes, min/max being exact -- then chunk_geom / tcs_takes), and the eligible ones are
+        // built in order with the next one's column coordinates already in flight.
+        const int pw = warp - 1, tid = pw * 32 + lane;
+        long long it = 0, nclaim = 0;
+        int sg = 0, abuf = 1;
+        long long aloads[2] = {0, 0};
+        int a_tile = -1, o_tile = -1;
+        float o[3] = {0.f, 0.f, 0.f};
+        const long long C = a.cpw;
+        auto item_tile = [&](long long u, long long& off) -> int {
+            const long long t = u / C;
+            off = (u - t * C) * kTcsW;
+            return (int)t;
+        };
+        auto row0t = [&](int tt) -> int { return a.lo + (tt * a.tstride + a.toff) * kTcsT; };
+        auto first_col = [&](int tt, long long off) -> int {  // first column of the chunk, wrapped
+            const int j0 = row0t(tt) + (int)off + 1;
+            return j0 >= n ? j0 - n : j0;
+        };
+        auto load_cols = [&](int jw, float (&q)[3 * kTcsPR]) {
+#pragma unroll
+            for (int h = 0; h < kTcsPR; ++h) {
+                int j = jw + min(tid + kTcsPT * h, 255);
+                if (j >= n) j -= n;
+                const float* src = a.xyz + 3ll * j;
+                q[3 * h] = __ldg(src);
+                q[3 * h + 1] = __ldg(src + 1);
+                q[3 * h + 2] = __ldg(src + 2);
+            }
+        };
+        for (;; ++nclaim) {
+            if (tid == 0) s_pclaim[nclaim & 1] = (long long)atomicAdd(a.work_ctr, 1ull);
+            asm volatile("bar.sync 1, %0;" ::"r"(kTcsProd * 32) : "memory");
+            const long long c = s_pclaim[nclaim & 1];
+            if (c >= a.nclaims) break;
+            const long long u0 = c * a.S, u1 = min(u0 + a.S, a.items);
+            for (long long ub = u0; ub < u1; ub += 32) {
+                // ---- classification, one item per lane
+                bool take = false;
+                {
+                    const long long u = ub + lane;
+                    if (u < u1) {
+                        long long off;
+                        const int tt = item_tile(u, off);
+                        const int i0 = row0t(tt);
+                        if (off + kTcsW <= a.L && i0 + kTcsT <= a.hi && off + 1 >= kTcsT && off + kTcsW <= steps_min) {
+                            float tmin[3] = {INFINITY, INFINITY, INFINITY}, tmax[3] = {-INFINITY, -INFINITY, -INFINITY};
+                            for (int q = 0; q < kTcsT / 32; ++q) {
+                                const float4 lo4 = a.blk_box[2 * ((i0 >> 5) + q)], hi4 = a.blk_box[2 * ((i0 >> 5) + q) + 1];
+                                tmin[0] = fminf(tmin[0], lo4.x); tmin[1] = fminf(tmin[1], lo4.y); tmin[2] = fminf(tmin[2], lo4.z);
+                                tmax[0] = fmaxf(tmax[0], hi4.x); tmax[1] = fmaxf(tmax[1], hi4.y); tmax[2] = fmaxf(tmax[2], hi4.z);
+                            }
+                            // the chunk's box: one or two runs of per-32 boxes (the FFMA kernel's blocks)
+                            const int jw = first_col(tt, off);
+                            const int jend = jw + kTcsW - 1;
+                            const int nb1 = (min(jend, n - 1) >> 5) - (jw >> 5) + 1;
+                            const int nb2 = jend >= n ? ((jend - n) >> 5) + 1 : 0;
+                            float cl[3] = {INFINITY, INFINITY, INFINITY}, ch[3] = {-INFINITY, -INFINITY, -INFINITY};
+                            for (int q = 0; q < nb1 + nb2; ++q) {
+                                const int bq = q < nb1 ? (jw >> 5) + q : q - nb1;
+                                const float4 lo4 = a.blk_box[2 * bq], hi4 = a.blk_box[2 * bq + 1];
+                                cl[0] = fminf(cl[0], lo4.x); cl[1] = fminf(cl[1], lo4.y); cl[2] = fminf(cl[2], lo4.z);
+                                ch[0] = fmaxf(ch[0], hi4.x); ch[1] = fmaxf(ch[1], hi4.y); ch[2] = fmaxf(ch[2], hi4.z);
+                            }
+                            take = tcs_takes(chunk_geom(tmin, tmax, cl, ch));
+                        }
+                    }
+                }
+                unsigned mask = __ballot_sync(0xffffffffu, take);
+                if (!mask) continue;
+                // ---- the eligible items, in order, one ahead in flight
+                float cur[3 * kTcsPR], nxt[3 * kTcsPR];
+                int e = __ffs(mask) - 1;
+                mask &= mask - 1;
+                long long eoff;
+                int ett = item_tile(ub + e, eoff);
+                load_cols(first_col(ett, eoff), cur);
+                for (;;) {
+                    const int e2 = mask ? __ffs(mask) - 1 : -1;
+                    if (mask) mask &= mask - 1;
+                    long long noff = 0;
+                    int ntt = 0;
+                    if (e2 >= 0) {
+                        ntt = item_tile(ub + e2, noff);
+                        load_cols(first_col(ntt, noff), nxt);
+                    }
+                    long long flag = 0;
+                    if (ett != o_tile) {  // the tile's centre (the FFMA kernel's o: its rows' box)
+                        o_tile = ett;
+                        const int i0 = row0t(ett);
+                        float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+                        if (lane < kTcsT / 32) {
+                            const float4 lo4 = a.blk_box[2 * ((i0 >> 5) + lane)], hi4 = a.blk_box[2 * ((i0 >> 5) + lane) + 1];
+                            mn[0] = lo4.x; mn[1] = lo4.y; mn[2] = lo4.z;
+                            mx[0] = hi4.x; mx[1] = hi4.y; mx[2] = hi4.z;
+                        }
+                        float tmin[3], tmax[3];
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) {
+                            tmin[k] = warp_min_f(mn[k]);
+                            tmax[k] = warp_max_f(mx[k]);
+                        }
+                        const ChunkGeom g = chunk_geom(tmin, tmax, tmin, tmax);
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) o[k] = g.o[k];
+                    }
+                    if (ett != a_tile) {
+                        // the row operand of the new tile: a = q - o, A = 1 + |a|^2, three-way splits
+                        abuf ^= 1;
+                        if (aloads[abuf] > 0) mbar_wait(a_empty + 8 * abuf, (unsigned)((aloads[abuf] - 1) & 1));
+                        unsigned char* dA = sA + abuf * kTcsOp;
+                        const int i0 = row0t(ett);
+#pragma unroll
+                        for (int h = 0; h < kTcsPR; ++h) {
+                            const int p = tid + kTcsPT * h;
+                            if (p >= 256) break;
+                            const float* q = a.xyz + 3ll * (i0 + p);
+                            const float ax = __fsub_rn(q[0], o[0]), ay = __fsub_rn(q[1], o[1]), az = __fsub_rn(q[2], o[2]);
+                            const float A = __fadd_rn(1.f, fmaf(az, az, fmaf(ay, ay, __fmul_rn(ax, ax))));
+                            tcs_write_row(dA, p, ax, ay, az, A);
+                        }
+                        fence_proxy_async_shared();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_plain(a_full + 8 * abuf);
+                        ++aloads[abuf];
+                        a_tile = ett;
+                        flag = 1;
+                    }
+                    // the column operand: b = q - o (carrying -2), B = |b|^2
+                    if (it >= kTcsStages) mbar_wait(b_empty + 8 * sg, (unsigned)(((it / kTcsStages) - 1) & 1));
+                    unsigned char* dB = sB + sg * kTcsOp;
+#ifdef PC_TCS_DBG_NOBUILD  // debug (timing only): keep whatever the stage holds
+                    if (it < kTcsStages)
+#endif
+#pragma unroll
+                    for (int h = 0; h < kTcsPR; ++h) {
+                        const int p = tid + kTcsPT * h;
+                        if (p >= 256) break;
+                        const float bx = __fsub_rn(cur[3 * h], o[0]), by = __fsub_rn(cur[3 * h + 1], o[1]),
+                                    bz = __fsub_rn(cur[3 * h + 2], o[2]);
+                        const float B = fmaf(bz, bz, fmaf(by, by, __fmul_rn(bx, bx)));
+                        tcs_write_col(dB, p, -2.f * bx, -2.f * by, -2.f * bz, B);
+                    }
+                    fence_proxy_async_shared();
+                    __syncwarp();
+                    if (tid == 0) s_item[sg] = (c << 2) | ((long long)abuf << 1) | flag;
+                    if (lane == 0) mbar_arrive_plain(b_full + 8 * sg);
+                    ++it;
+                    sg = sg + 1 == kTcsStages ? 0 : sg + 1;
+                    if (e2 < 0) break;
+                    e = e2;
+                    ett = ntt;
+                    eoff = noff;
+#pragma unroll
+                    for (int k = 0; k < 3 * kTcsPR; ++k) cur[k] = nxt[k];
+                }
+            }
+        }
+        // end of the work: a sentinel item
+        if (it >= kTcsStages) mbar_wait(b_empty + 8 * sg, (unsigned)(((it / kTcsStages) - 1) & 1));
+        if (tid == 0) s_item[sg] = -1;
+        if (lane == 0) mbar_arrive_plain(b_full + 8 * sg);
+    } else {
+        // ---------------- epilogue: group h drains accumulators (h, 0) and (h, 1), lane quadrant warp % 4
+        const int ew = warp - 1 - kTcsProd, h = ew >> 2, quad = warp & 3;
+        long long cur = -1;
+        for (long long it = 0;; ++it) {
+            bool done = false;
+#pragma unroll 1
+            for (int q = 0; q < kTcsNQ; ++q) {
+                const int k = h * kTcsNQ + q;
+                mbar_wait(acc_full + 8 * k, (unsigned)(it & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const long long claim = s_meta[k];
+                if (claim < 0) {
+                    done = true;
+                    break;
+                }
+                if (claim != cur) {
+                    if (cur >= 0) {
+                        const double cs = warp_sum(sum);
+                        if (lane == 0) a.claim_sums[cur * kTcsParts + ew] = cs;
+                        sum = 0.0;
+                    }
+                    cur = claim;
+                }
+                // the accumulator in rounds of kTcsRound columns; released after the last round's loads
+                const unsigned tbase = tmem + ((unsigned)(quad * 32) << 16) + (unsigned)(k * kTcsNP);
+                float2 acc = make_float2(0.f, 0.f), acc2 = make_float2(0.f, 0.f);  // two chains
+#pragma unroll 1
+                for (int rd = 0; rd < kTcsNP / kTcsRound; ++rd) {
+                    unsigned v[kTcsRound / 32][32];
+#pragma unroll
+                    for (int w = 0; w < kTcsRound / 32; ++w) PC_TC_LD32(v[w], tbase + (unsigned)(kTcsRound * rd) + 32u * w);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (rd == kTcsNP / kTcsRound - 1) {
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_plain(acc_empty + 8 * k);
+                    }
+#ifdef PC_TCS_DBG_LIGHT  // debug (timing only): the drain without the arithmetic
+#pragma unroll
+                    for (int w = 0; w < kTcsRound / 32; ++w) acc.x += __uint_as_float(v[w][w]);
+#else
+#pragma unroll
+                    for (int w = 0; w < kTcsRound / 32; ++w) {
+#pragma unroll
+                        for (int e = 0; e < 32; e += 8) {
+                            const float2 p1 = make_float2(__uint_as_float(v[w][e]), __uint_as_float(v[w][e + 1]));
+                            const float2 p2 = make_float2(__uint_as_float(v[w][e + 2]), __uint_as_float(v[w][e + 3]));
+                            const float2 p3 = make_float2(__uint_as_float(v[w][e + 4]), __uint_as_float(v[w][e + 5]));
+                            const float2 p4 = make_float2(__uint_as_float(v[w][e + 6]), __uint_as_float(v[w][e + 7]));
+                            const float2 m12 = __fmul2_rn(p1, p2), s12 = __fadd2_rn(p1, p2);
+                            const float2 m34 = __fmul2_rn(p3, p4), s34 = __fadd2_rn(p3, p4);
+                            const float2 P = __fmul2_rn(m12, m34);
+                            const float2 Nn = __ffma2_rn(s34, m12, __fmul2_rn(s12, m34));
+                            if (e & 8) acc2 = __ffma2_rn(Nn, make_float2(rcp_approx(P.x), rcp_approx(P.y)), acc2);
+                            else acc = __ffma2_rn(Nn, make_float2(rcp_approx(P.x), rcp_approx(P.y)), acc);
+                        }
+                    }
+#endif
+                }
+                acc = __fadd2_rn(acc, acc2);
+                sum += (double)(acc.x + acc.y);
+            }
+            if (done) break;
+        }
+        if (cur >= 0) {
+            const double cs = warp_sum(sum);
+            if (lane == 0) a.claim_sums[cur * kTcsParts + ew] = cs;
+        }
+        sum = 0.0;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Slot sl{};
+        sl.pad[0] = s_items;  // items (chunks) evaluated on the tensor cores
+        a.slots[blockIdx.x] = sl;
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}

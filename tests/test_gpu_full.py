@@ -71,7 +71,9 @@ def test_full_totals_every_path(inputs, name):
     r = _host(x, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED)
     assert r.count == g["count"] and r.sum == s and r.pairs == g["pairs"]
     prof = _lib.last_profile()
-    assert prof.kernel == 3 and prof.f64_taken == 0 and prof.chunks_gram > 0
+    # the sorted FFMA kernel plus the tensor-core Gram chunks (kernel 10; 3 with PAIRCOUNT_TCSUM=0)
+    assert prof.kernel in (3, 10) and prof.f64_taken == 0 and prof.chunks_gram + prof.chunks_tc > 0
+    assert (prof.chunks_tc > 0) == (prof.kernel == 10)
     # input-order sum kernel
     r = _host(x, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, _lib.PC_TILE_FLAT)
     assert r.count == g["count"] and abs(r.sum - g["inv_sum"]) <= REL * g["inv_sum"]

@@ -4,6 +4,8 @@ NCCL exchange at world size 1, device-count defaults."""
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -66,7 +68,8 @@ def test_sorted_tile_parts_on_clustered_points():
 def test_profile_accounts_for_every_pair():
     """pc_pairs_profile: the chunks of each inner loop cover the call's pairs;
     the kernel ids follow the dispatch; claims only on FLAT tilings."""
-    for n, tiling, inter, kern in ((70000, _lib.PC_TILE_AUTO, _lib.PC_COLLISION_INVSQ, 3),
+    tcs = os.environ.get("PAIRCOUNT_TCSUM", "1") != "0"
+    for n, tiling, inter, kern in ((70000, _lib.PC_TILE_AUTO, _lib.PC_COLLISION_INVSQ, 10 if tcs else 3),
                                    (70000, _lib.PC_TILE_FLAT, _lib.PC_COLLISION_INVSQ, 2),
                                    (70000, _lib.PC_TILE_FLAT, _lib.PC_COLLISION, 1),
                                    (70000, _lib.PC_TILE_TC, _lib.PC_COLLISION, 5),
@@ -79,11 +82,18 @@ def test_profile_accounts_for_every_pair():
         assert prof.exact_checks == r.exact_checks
         if kern == 5:
             continue
-        chunks = prof.chunks_gram + prof.chunks_main + prof.chunks_near + prof.chunks_far + prof.chunks_edge
+        chunks = (prof.chunks_gram + prof.chunks_main + prof.chunks_near + prof.chunks_far + prof.chunks_edge +
+                   prof.chunks_tc)
         assert chunks * prof.pairs_per_chunk >= r.pairs  # edge chunks are partly masked
         assert (prof.claims > 0) == (tiling != _lib.PC_TILE_PER_ROW_TILE)
-        if kern == 3:
-            assert prof.chunks_gram > 0 and prof.chunks_near > 0
+        if kern in (3, 10):
+            assert prof.chunks_gram + prof.chunks_tc > 0 and prof.chunks_near > 0
+            # every (tile, chunk) of the window space evaluated once, by one of the two kernels
+            T = W = 256
+            tiles = -(-n // T)
+            assert chunks == tiles * -(-(T - 1 + n // 2) // W)
+        if kern == 10:
+            assert prof.chunks_tc > 0
         if kern == 8:  # pruned sorted count: most chunks decided by their boxes
             assert prof.chunks_far > 0.5 * chunks
 
