@@ -227,6 +227,9 @@ int32_t pc_last_launch_count(void);
  * recorded events and returns the summed kernel time and launch count. */
 int pc_kernel_timing(int32_t enable);
 int pc_kernel_timing_read(double* total_ms, int32_t* launches);
+/* The same events split by kernel: ms[0] / launches[0] the FFMA all-pairs kernels, ms[1] /
+   launches[1] the tensor-core sum kernel (pairs_tcs_kernel); both arrays of 2.  Resets. */
+int pc_kernel_timing_read_split(double* ms, int32_t* launches);
 
 /* -------------------------------------------------- counting array ---- */
 /* Dense occupancy grid of side 2a+3 per axis (one zero padding cell per

@@ -42,7 +42,7 @@ EXPORTED = (
     "pc_device_free", "pc_memcpy_h2d", "pc_memcpy_d2h", "pc_stream_sync",
     "pc_pairs_workspace_bytes", "pc_pairs", "pc_pairs_async", "pc_pairs_host", "pc_pairs_multi", "pc_pairs_batch",
     "pc_pairs_part_async", "pc_pairs_part_host", "pc_pairs_last_profile", "pc_pairs_profile_read",
-    "pc_last_launch_count", "pc_kernel_timing", "pc_kernel_timing_read", "pc_lattice_grid_cells", "pc_lattice_key_bytes",
+    "pc_last_launch_count", "pc_kernel_timing", "pc_kernel_timing_read", "pc_kernel_timing_read_split", "pc_lattice_grid_cells", "pc_lattice_key_bytes",
     "pc_lattice_collisions", "pc_lattice_contacts", "pc_lattice_reset_keys", "pc_lattice_clear",
     "pc_lattice_collisions_batch", "pc_lattice_collisions_vectors", "pc_lattice_collisions_multi",
     "pc_lattice_reset_beads", "pc_grid_count_nonzero", "pc_microbench",
@@ -105,6 +105,7 @@ _SIGS = {
     "pc_last_launch_count": ([], _i32),
     "pc_kernel_timing": ([_i32], ctypes.c_int),
     "pc_kernel_timing_read": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i32)], ctypes.c_int),
+    "pc_kernel_timing_read_split": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i32)], ctypes.c_int),
     "pc_lattice_grid_cells": ([_i64], _i64),
     "pc_lattice_key_bytes": ([_i64], _i32),
     "pc_lattice_collisions": ([_vp, _i32, _i32, _i64, _i64, _vp, _vp, _i32, _vp, _vp], ctypes.c_int),
@@ -289,6 +290,14 @@ def workspace_bytes(n: int, nranges: int = 1) -> int:
 
 def kernel_timing(enable: bool) -> None:
     check(load().pc_kernel_timing(1 if enable else 0))
+
+
+def kernel_timing_read_split():
+    """((FFMA kernels ms, launches), (tensor-core sum kernel ms, launches)) since kernel_timing(True)."""
+    ms = (ctypes.c_double * 2)()
+    cnt = (_i32 * 2)()
+    check(load().pc_kernel_timing_read_split(ms, cnt))
+    return (ms[0], cnt[0]), (ms[1], cnt[1])
 
 
 def kernel_timing_read():

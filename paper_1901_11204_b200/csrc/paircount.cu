@@ -54,6 +54,7 @@ thread_local int g_launches = 0;
 // roofline needs that kernel's own duration, on the stream it runs on).
 struct EvPair {
     cudaEvent_t a, b;
+    int kind;  // 0: FFMA all-pairs kernels, 1: the tensor-core sum kernel (pairs_tcs_kernel)
 };
 thread_local bool g_timing = false;
 thread_local EvPair g_ev[4096];
@@ -866,6 +867,7 @@ int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, int* nc
             ++g_ev_made;
         }
         ev = &g_ev[g_ev_used++];
+        ev->kind = 0;
         CK(cudaEventRecord(ev->a, s));
     }
     kern<<<grid, WARPS * 32, smem, s>>>(args);
@@ -976,6 +978,7 @@ int launch_tcs(const PairsArgs& p, TileSel ts, double* claims_tc, Slot* slots, l
             ++g_ev_made;
         }
         ev = &g_ev[g_ev_used++];
+        ev->kind = 1;
         CK(cudaEventRecord(ev->a, s));
     }
     pairs_tcs_kernel<<<grid, kTcsWarps * 32, kTcsSmem, s>>>(a);
@@ -1041,6 +1044,7 @@ int run_pairs_tc(const PairsArgs& p, char* ws, const WsLayout& lay, long long n,
                     ++g_ev_made;
                 }
                 ev = &g_ev[g_ev_used++];
+                ev->kind = 0;
                 CK(cudaEventRecord(ev->a, s));
             }
             pairs_tc_kernel<<<grid, kTcWarps * 32, kTcSmem, s>>>(a);
@@ -1098,6 +1102,7 @@ int run_pairs_key(const PairsArgs& p, char* ws, const WsLayout& lay, long long n
                     ++g_ev_made;
                 }
                 ev = &g_ev[g_ev_used++];
+                ev->kind = 0;
                 CK(cudaEventRecord(ev->a, s));
             }
             pairs_key_kernel<<<grid, kKeyWarps * 32, 0, s>>>(a);
@@ -1269,6 +1274,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
                         ++g_ev_made;
                     }
                     ev = &g_ev[g_ev_used++];
+                    ev->kind = 0;
                     CK(cudaEventRecord(ev->a, s));
                 }
                 pairs_row_kernel<<<grid, kRowThreads, 0, s>>>(args, direct ? 1 : 0);
@@ -1793,6 +1799,21 @@ int32_t pc_last_launch_count(void) { return g_launches; }
 
 int pc_kernel_timing(int32_t enable) {
     g_timing = enable != 0;
+    g_ev_used = 0;
+    return PC_OK;
+}
+
+int pc_kernel_timing_read_split(double* ms, int32_t* launches) {
+    ms[0] = ms[1] = 0.0;
+    launches[0] = launches[1] = 0;
+    for (int k = 0; k < g_ev_used; ++k) {
+        CK(cudaEventSynchronize(g_ev[k].b));
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, g_ev[k].a, g_ev[k].b));
+        const int kd = g_ev[k].kind == 1 ? 1 : 0;
+        ms[kd] += t;
+        ++launches[kd];
+    }
     g_ev_used = 0;
     return PC_OK;
 }

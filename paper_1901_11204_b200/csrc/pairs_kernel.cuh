@@ -78,10 +78,12 @@ __device__ __forceinline__ ChunkGeom chunk_geom(const float tmin[3], const float
     g.ab = __fadd_rn(__fsqrt_rn(rt2), __fsqrt_rn(bm2));
     return g;
 }
-// a dense chunk the tensor-core sum kernel takes (pairs_tcsum.cuh)
+// a dense chunk the tensor-core sum kernel takes (pairs_tcsum.cuh): the Gram test below, 8u (|a|+|b|)^2
+// <= 5e-6 (1 + dmin^2) written as 5u (..)^2 <= 3.125e-6 (..), dmin^2 > 4.5, and |a|+|b| <= 3e4 (the
+// epilogue's four-term products stay finite)
 __device__ __forceinline__ bool tcs_takes(const ChunkGeom& g) {
     return g.gap2 > 4.5f && g.ab <= 3e4f &&
-           __fmul_rn(7.152557373046875e-07f, __fmul_rn(g.ab, g.ab)) <= __fmul_rn(3.125e-6f, __fadd_rn(1.f, g.gap2));
+           __fmul_rn(2.98023223876953125e-07f, __fmul_rn(g.ab, g.ab)) <= __fmul_rn(3.125e-6f, __fadd_rn(1.f, g.gap2));
 }
 
 // Pair-buffer layouts (one entry per column pair k, k+1):

@@ -45,17 +45,9 @@
 // claim's composition is fixed by its index, so the float64 total is bit-reproducible.
 
 constexpr int kTcsT = 256, kTcsW = 256;           // the FFMA sorted kernel's tile and chunk
-#ifndef PC_TCS_BF16
-#define PC_TCS_BF16 1  // operands as three bf16 pieces, kind::f16, K = 32 (0: three tf32 pieces, kind::tf32, K = 24)
-#endif
-#if PC_TCS_BF16
-#define PC_TCS_KIND "f16"
-#else
-#define PC_TCS_KIND "tf32"
-#endif
-constexpr int kTcsKC = PC_TCS_BF16 ? 4 : 6;        // 16-byte K-chunks per point
+constexpr int kTcsKC = 4;                          // K = 32 bf16: four 16-byte K-chunks per point
 constexpr int kTcsGroup = kTcsKC * 128;            // bytes per 8 points
-constexpr int kTcsOp = 256 / 8 * kTcsGroup;        // bytes per 256-point operand (16 KB bf16, 24 KB tf32)
+constexpr int kTcsOp = 256 / 8 * kTcsGroup;        // bytes per 256-point operand (16 KB)
 constexpr int kTcsHalf = kTcsOp / 2;               // 128 points
 #ifndef PC_TCS_NQ
 #define PC_TCS_NQ 1  // column pieces per row half: accumulators of 256 / NQ columns, 2 NQ of them in TMEM
@@ -70,30 +62,35 @@ static_assert(kTcsNAcc * kTcsNP == 512 && kTcsNP % kTcsRound == 0 && kTcsRound %
 #define PC_TCS_STAGES 5
 #endif
 constexpr int kTcsStages = PC_TCS_STAGES;
-#ifndef PC_TCS_KSTEPS  // K-steps per accumulator (K = 16 bf16 / 8 tf32 each); a debug knob for A/B of the MMA cost
-#define PC_TCS_KSTEPS (PC_TCS_BF16 ? 2 : 3)
+#ifndef PC_TCS_KSTEPS  // K = 16 steps per accumulator; a debug knob for A/B of the MMA cost
+#define PC_TCS_KSTEPS 2
 #endif
 #ifndef PC_TCS_PROD
 #define PC_TCS_PROD 4  // producer warps (13 warps: 16 warp slots of 128 registers; 3 and 7 measured slower)
 #endif
-constexpr int kTcsProd = PC_TCS_PROD, kTcsEpi = 8, kTcsWarps = 1 + kTcsProd + kTcsEpi;
+#ifndef PC_TCS_EPI
+#define PC_TCS_EPI 8  // epilogue warps: 4 per accumulator (each all its columns) or 8 (half the columns each)
+#endif
+constexpr int kTcsProd = PC_TCS_PROD, kTcsEpi = PC_TCS_EPI, kTcsWarps = 1 + kTcsProd + kTcsEpi;
+constexpr int kTcsEpiG = kTcsEpi / 2, kTcsSpan = kTcsNP * 4 / kTcsEpiG;  // warps per accumulator, columns per warp
+static_assert(kTcsNQ == 1 || kTcsEpi == 8, "column-split epilogue for whole-row-half accumulators only");
 constexpr int kTcsPT = kTcsProd * 32, kTcsPR = (256 + kTcsPT - 1) / kTcsPT;  // producer threads, points per thread
 constexpr int kTcsSmem = 2 * kTcsOp + kTcsStages * kTcsOp + 1024;
 constexpr long long kTcsParts = kTcsEpi;           // float64 partials per claim
-// instruction descriptor: D f32, A/B bf16 (f16 kind) or tf32, both K-major, N = kTcsNP, M = 128
-constexpr uint32_t kTcsIdesc = (1u << 4) | ((PC_TCS_BF16 ? 1u : 2u) << 7) | ((PC_TCS_BF16 ? 1u : 2u) << 10) |
-                               ((uint32_t)(kTcsNP >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+// instruction descriptor (kind::f16): D f32, A/B bf16, both K-major, N = kTcsNP, M = 128
+constexpr uint32_t kTcsIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTcsNP >> 3) << 17) |
+                               ((uint32_t)(128 >> 4) << 24);
 
-// exact three-way splits x = h + m + l: tf32 (round to nearest, ties away) or bf16 (nearest even)
+// exact three-way bf16 split x = h + m + l (round to nearest even; 8 + 8 + 8 significant bits)
 __device__ __forceinline__ float bf16r(float x) {  // round to nearest even on the integer pipe (finite x)
     const unsigned u = __float_as_uint(x);
     return __uint_as_float((u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u);
 }
 __device__ __forceinline__ void split3(float x, float& h, float& m, float& l) {
-    h = PC_TCS_BF16 ? bf16r(x) : tf32_rna(x);
+    h = bf16r(x);
     const float r = __fsub_rn(x, h);
-    m = PC_TCS_BF16 ? bf16r(r) : tf32_rna(r);
-    l = PC_TCS_BF16 ? bf16r(__fsub_rn(r, m)) : __fsub_rn(r, m);  // exact either way (<= 8 / 2 significant bits)
+    m = bf16r(r);
+    l = bf16r(__fsub_rn(r, m));  // exact: <= 8 significant bits left
 }
 __device__ __forceinline__ unsigned bf2(float lo, float hi) {  // two exact bf16 values, lo at the lower address
     return (__float_as_uint(hi) & 0xffff0000u) | (__float_as_uint(lo) >> 16);
@@ -104,53 +101,65 @@ __device__ __forceinline__ uint64_t tcs_desc(unsigned saddr) {
     return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)(128u >> 4) << 16) | ((uint64_t)((unsigned)kTcsGroup >> 4) << 32) |
            (1ull << 46);
 }
-// Row p of the A operand: a = q - o and A = 1 + |a|^2, split.  K order (bf16, 32):
-//   a_h a_h a_h a_m a_m a_m a_l a_l | A_h A_m A_l | 1 1 1 | 0 0     (each a_* three coordinates)
-// against the B order  b_h b_m b_l b_h b_m b_l b_h b_m | 1 1 1 | B_h B_m B_l | 0 0:
-// a_h.b_{h,m,l} + a_m.b_{h,m,l} + a_l.b_{h,m} + A + B (only a_l.b_l, <= 2^-32 |a||b|, dropped).
-// tf32 (24): a_h a_h a_m a_h a_m a_l | A_h A_m A_l | 1 1 1 against b_h b_m b_h b_l b_m b_h | 1 1 1 | B_h B_m B_l.
-__device__ __forceinline__ void tcs_write_row(unsigned char* d, int p, float ax, float ay, float az, float A) {
-    float xh, xm, xl, yh, ym, yl, zh, zm, zl, Ah, Am, Al;
-    split3(ax, xh, xm, xl);
-    split3(ay, yh, ym, yl);
-    split3(az, zh, zm, zl);
-    split3(A, Ah, Am, Al);
-#if PC_TCS_BF16
-    const float one = 1.f;
-    *reinterpret_cast<uint4*>(d + tcs_off(p, 0)) = make_uint4(bf2(xh, yh), bf2(zh, xh), bf2(yh, zh), bf2(xh, yh));
-    *reinterpret_cast<uint4*>(d + tcs_off(p, 1)) = make_uint4(bf2(zh, xm), bf2(ym, zm), bf2(xm, ym), bf2(zm, xm));
-    *reinterpret_cast<uint4*>(d + tcs_off(p, 2)) = make_uint4(bf2(ym, zm), bf2(xl, yl), bf2(zl, xl), bf2(yl, zl));
-    *reinterpret_cast<uint4*>(d + tcs_off(p, 3)) = make_uint4(bf2(Ah, Am), bf2(Al, one), bf2(one, one), 0u);
-#else
-    *reinterpret_cast<float4*>(d + tcs_off(p, 0)) = make_float4(xh, yh, zh, xh);
-    *reinterpret_cast<float4*>(d + tcs_off(p, 1)) = make_float4(yh, zh, xm, ym);
-    *reinterpret_cast<float4*>(d + tcs_off(p, 2)) = make_float4(zm, xh, yh, zh);
-    *reinterpret_cast<float4*>(d + tcs_off(p, 3)) = make_float4(xm, ym, zm, xl);
-    *reinterpret_cast<float4*>(d + tcs_off(p, 4)) = make_float4(yl, zl, Ah, Am);
-    *reinterpret_cast<float4*>(d + tcs_off(p, 5)) = make_float4(Al, 1.f, 1.f, 1.f);
-#endif
+// Two values split three ways at once, as packed bf16x2 words (x in the low half = the lower K
+// index): cvt.rn.bf16x2.f32 rounds both to nearest even, the residuals are exact in fp32.
+__device__ __forceinline__ unsigned pk2(float lo, float hi) {
+    unsigned r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
 }
-// Column p of the B operand from -2b and B = |b|^2
-__device__ __forceinline__ void tcs_write_col(unsigned char* d, int p, float bx, float by, float bz, float B) {
-    float xh, xm, xl, yh, ym, yl, zh, zm, zl, Bh, Bm, Bl;
-    split3(bx, xh, xm, xl);
-    split3(by, yh, ym, yl);
-    split3(bz, zh, zm, zl);
-    split3(B, Bh, Bm, Bl);
-#if PC_TCS_BF16
-    const float one = 1.f;
-    *reinterpret_cast<uint4*>(d + tcs_off(p, 0)) = make_uint4(bf2(xh, yh), bf2(zh, xm), bf2(ym, zm), bf2(xl, yl));
-    *reinterpret_cast<uint4*>(d + tcs_off(p, 1)) = make_uint4(bf2(zl, xh), bf2(yh, zh), bf2(xm, ym), bf2(zm, xl));
-    *reinterpret_cast<uint4*>(d + tcs_off(p, 2)) = make_uint4(bf2(yl, zl), bf2(xh, yh), bf2(zh, xm), bf2(ym, zm));
-    *reinterpret_cast<uint4*>(d + tcs_off(p, 3)) = make_uint4(bf2(one, one), bf2(one, Bh), bf2(Bm, Bl), 0u);
+__device__ __forceinline__ float lo_f(unsigned w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float hi_f(unsigned w) { return __uint_as_float(w & 0xffff0000u); }
+__device__ __forceinline__ void split3x2(float x, float y, unsigned& h, unsigned& m, unsigned& l) {
+    h = pk2(x, y);
+    const float rx = __fsub_rn(x, lo_f(h)), ry = __fsub_rn(y, hi_f(h));
+    m = pk2(rx, ry);
+    l = pk2(__fsub_rn(rx, lo_f(m)), __fsub_rn(ry, hi_f(m)));  // exact: <= 8 significant bits left
+}
+// halves of two words: (lo a, lo b), (lo a, hi b), (hi a, lo b), (hi a, hi b)
+__device__ __forceinline__ unsigned ll(unsigned a, unsigned b) { return __byte_perm(a, b, 0x5410); }
+__device__ __forceinline__ unsigned lh(unsigned a, unsigned b) { return __byte_perm(a, b, 0x7610); }
+__device__ __forceinline__ unsigned hl(unsigned a, unsigned b) { return __byte_perm(a, b, 0x5432); }
+__device__ __forceinline__ unsigned hh(unsigned a, unsigned b) { return __byte_perm(a, b, 0x7632); }
+constexpr unsigned kBf16One2 = 0x3F803F80u;  // (1, 1)
+
+// Row p of the A operand: a = q - o and A = 1 + |a|^2 (float64, carried as fp32 hi + lo), split.
+// K order (bf16, 32):  a_h a_h a_h a_m a_m a_m a_l a_l | A_h A_m A_l A_lo | 1 1 1 1
+// against the B order  b_h b_m b_l b_h b_m b_l b_h b_m | 1 1 1 1 | B_h B_m B_l B_lo   (each a_*, b_* three
+// coordinates): a_h.b_{h,m,l} + a_m.b_{h,m,l} + a_l.b_{h,m} + A + B -- every product exact in fp32, only
+// a_l.b_l (<= 2^-32 |a||b|) dropped, and A, B within 2^-32 relative of |a|^2 + 1, |b|^2 of the fp32 a, b.
+__device__ __forceinline__ void tcs_write_row(unsigned char* d, int p, float ax, float ay, float az) {
+#ifdef PC_TCS_DBG_F32NORM  // debug (timing only): fp32 norms
+    const float A = 1.f + ax * ax + ay * ay + az * az, Alo = 0.f;
 #else
-    *reinterpret_cast<float4*>(d + tcs_off(p, 0)) = make_float4(xh, yh, zh, xm);
-    *reinterpret_cast<float4*>(d + tcs_off(p, 1)) = make_float4(ym, zm, xh, yh);
-    *reinterpret_cast<float4*>(d + tcs_off(p, 2)) = make_float4(zh, xl, yl, zl);
-    *reinterpret_cast<float4*>(d + tcs_off(p, 3)) = make_float4(xm, ym, zm, xh);
-    *reinterpret_cast<float4*>(d + tcs_off(p, 4)) = make_float4(yh, zh, 1.f, 1.f);
-    *reinterpret_cast<float4*>(d + tcs_off(p, 5)) = make_float4(1.f, Bh, Bm, Bl);
+    const double Ad = 1.0 + (double)ax * ax + (double)ay * ay + (double)az * az;  // products exact in float64
+    const float A = (float)Ad, Alo = (float)(Ad - (double)A);
 #endif
+    unsigned XYh, XYm, XYl, ZAh, ZAm, ZAl;
+    split3x2(ax, ay, XYh, XYm, XYl);
+    split3x2(az, A, ZAh, ZAm, ZAl);
+    const unsigned lo2 = pk2(Alo, Alo);
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 0)) = make_uint4(XYh, ll(ZAh, XYh), hl(XYh, ZAh), XYh);
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 1)) = make_uint4(ll(ZAh, XYm), hl(XYm, ZAm), XYm, ll(ZAm, XYm));
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 2)) = make_uint4(hl(XYm, ZAm), XYl, ll(ZAl, XYl), hl(XYl, ZAl));
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 3)) = make_uint4(hh(ZAh, ZAm), hl(ZAl, lo2), kBf16One2, kBf16One2);
+}
+// Column p of the B operand from b = q - o: the products carry -2b (exact), B = |b|^2 (float64 hi + lo)
+__device__ __forceinline__ void tcs_write_col(unsigned char* d, int p, float bx, float by, float bz) {
+#ifdef PC_TCS_DBG_F32NORM
+    const float B = bx * bx + by * by + bz * bz, Blo = 0.f;
+#else
+    const double Bd = (double)bx * bx + (double)by * by + (double)bz * bz;
+    const float B = (float)Bd, Blo = (float)(Bd - (double)B);
+#endif
+    unsigned XYh, XYm, XYl, ZBh, ZBm, ZBl;
+    split3x2(-2.f * bx, -2.f * by, XYh, XYm, XYl);
+    split3x2(-2.f * bz, B, ZBh, ZBm, ZBl);
+    const unsigned lo2 = pk2(Blo, Blo);
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 0)) = make_uint4(XYh, ll(ZBh, XYm), hl(XYm, ZBm), XYl);
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 1)) = make_uint4(ll(ZBl, XYh), hl(XYh, ZBh), XYm, ll(ZBm, XYl));
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 2)) = make_uint4(hl(XYl, ZBl), XYh, ll(ZBh, XYm), hl(XYm, ZBm));
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 3)) = make_uint4(kBf16One2, kBf16One2, hh(ZBh, ZBm), hh(ZBl, lo2));
 }
 
 struct TcsArgs {
@@ -206,7 +215,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
         }
         for (int k = 0; k < kTcsNAcc; ++k) {
             mbar_init(acc_full + 8 * k, 2);  // the MMA thread's hand-off + the MMAs' commit
-            mbar_init(acc_empty + 8 * k, 4);
+            mbar_init(acc_empty + 8 * k, kTcsEpiG);
         }
         mbar_init_fence();
         s_items = 0;
@@ -271,7 +280,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                     for (int ks = 0; ks < PC_TCS_KSTEPS; ++ks) {
                         asm volatile(
                             "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                            " tcgen05.mma.cta_group::1.kind::" PC_TCS_KIND " [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (unsigned)(k * kTcsNP)),
+                            " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (unsigned)(k * kTcsNP)),
                             "l"(da + (uint64_t)(16 * ks)), "l"(db + (uint64_t)(16 * ks)), "r"(kTcsIdesc), "r"(ks));
                     }
                     tc_commit(acc_full + 8 * k);
@@ -402,8 +411,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                             if (p >= 256) break;
                             const float* q = a.xyz + 3ll * (i0 + p);
                             const float ax = __fsub_rn(q[0], o[0]), ay = __fsub_rn(q[1], o[1]), az = __fsub_rn(q[2], o[2]);
-                            const float A = __fadd_rn(1.f, fmaf(az, az, fmaf(ay, ay, __fmul_rn(ax, ax))));
-                            tcs_write_row(dA, p, ax, ay, az, A);
+                            tcs_write_row(dA, p, ax, ay, az);
                         }
                         fence_proxy_async_shared();
                         __syncwarp();
@@ -424,8 +432,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                         if (p >= 256) break;
                         const float bx = __fsub_rn(cur[3 * h], o[0]), by = __fsub_rn(cur[3 * h + 1], o[1]),
                                     bz = __fsub_rn(cur[3 * h + 2], o[2]);
-                        const float B = fmaf(bz, bz, fmaf(by, by, __fmul_rn(bx, bx)));
-                        tcs_write_col(dB, p, -2.f * bx, -2.f * by, -2.f * bz, B);
+                        tcs_write_col(dB, p, bx, by, bz);
                     }
                     fence_proxy_async_shared();
                     __syncwarp();
@@ -448,7 +455,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
         if (lane == 0) mbar_arrive_plain(b_full + 8 * sg);
     } else {
         // ---------------- epilogue: group h drains accumulators (h, 0) and (h, 1), lane quadrant warp % 4
-        const int ew = warp - 1 - kTcsProd, h = ew >> 2, quad = warp & 3;
+        const int ew = warp - 1 - kTcsProd, h = ew / kTcsEpiG, quad = warp & 3, cpart = (ew % kTcsEpiG) >> 2;
         long long cur = -1;
         for (long long it = 0;; ++it) {
             bool done = false;
@@ -471,15 +478,15 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                     cur = claim;
                 }
                 // the accumulator in rounds of kTcsRound columns; released after the last round's loads
-                const unsigned tbase = tmem + ((unsigned)(quad * 32) << 16) + (unsigned)(k * kTcsNP);
+                const unsigned tbase = tmem + ((unsigned)(quad * 32) << 16) + (unsigned)(k * kTcsNP + cpart * kTcsSpan);
                 float2 acc = make_float2(0.f, 0.f), acc2 = make_float2(0.f, 0.f);  // two chains
 #pragma unroll 1
-                for (int rd = 0; rd < kTcsNP / kTcsRound; ++rd) {
+                for (int rd = 0; rd < kTcsSpan / kTcsRound; ++rd) {
                     unsigned v[kTcsRound / 32][32];
 #pragma unroll
                     for (int w = 0; w < kTcsRound / 32; ++w) PC_TC_LD32(v[w], tbase + (unsigned)(kTcsRound * rd) + 32u * w);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (rd == kTcsNP / kTcsRound - 1) {
+                    if (rd == kTcsSpan / kTcsRound - 1) {
                         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                         __syncwarp();
                         if (lane == 0) mbar_arrive_plain(acc_empty + 8 * k);

@@ -43,7 +43,8 @@ for name in work:
         call()
     e1.record()
     torch.cuda.synchronize()
-    kms, cnt = _lib.kernel_timing_read()
+    (fms, fcnt), (tms, tcnt) = _lib.kernel_timing_read_split()
+    kms, cnt = fms + tms, fcnt + tcnt
     _lib.kernel_timing(False)
     step = e0.elapsed_time(e1) / reps
     r = _lib.PairsResult.from_buffer_copy(res.cpu().numpy().tobytes())
@@ -51,6 +52,6 @@ for name in work:
     g = gold[name]
     rel = abs(r.sum - g["inv_sum"]) / g["inv_sum"]
     print(json.dumps({"workload": name, "tcsum": os.environ.get("PAIRCOUNT_TCSUM", "1"), "step_ms": round(step, 3),
-                      "timed_kernels_ms": round(kms / reps, 3), "launches_per_step": cnt / reps,
+                      "timed_kernels_ms": round(kms / reps, 3), "ffma_ms": round(fms / reps, 3), "tc_ms": round(tms / reps, 3), "launches_per_step": cnt / reps,
                       "count": r.count, "count_ok": r.count == g["count"], "sum": r.sum, "sum_rel_err": rel,
                       "pairs": r.pairs, "error": r.error, "profile": prof}), flush=True)
