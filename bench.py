@@ -685,7 +685,8 @@ def run_ours(args):
             e1.synchronize()
             elapsed += e0.elapsed_time(e1)
     torch.cuda.synchronize()
-    kern_ms, kern_launches = _lib.kernel_timing_read()
+    (ffma_ms, ffma_launches), (tc_ms, tc_launches) = _lib.kernel_timing_read_split()
+    kern_ms, kern_launches = ffma_ms + tc_ms, ffma_launches + tc_launches
     _lib.kernel_timing(False)
     prof = _lib.profile_read(ws.data_ptr(), n, stream.cuda_stream)  # the last step's path counters
     if world > 1:
@@ -739,15 +740,14 @@ def run_ours(args):
         dist.destroy_process_group()
         return 0
 
-    # ---- roofline of the dominant kernel (pairs_kernel SORTED, this rank's launches)
-    kern_ms_avg = kern_ms / max(1, kern_launches)
+    # ---- roofline of the dominant kernel: pairs_tcs_kernel (the tensor-core Gram chunks, ~93 % of the
+    # pairs at 2^20), with the sorted FFMA kernel (the remaining near / far-direct / edge chunks) beside it
+    steps_timed = max(1, args.steps)
     rank_pairs = int(prof.pairs)
     clocks = clk.summary()
     clock_mhz = clocks.get("sm_mhz") or 1965.0
     ffma_rate, _ = _lib.microbench(0)  # lane-FFMA/s over all SMs, measured live
     peak_tflops = 2.0 * ffma_rate / 1e12
-    exe = executed_roofline(prof, kern_ms_avg * 1e-3, clock_mhz, sms)
-    norm_tflops = FLOPS_PER_PAIR * rank_pairs / (kern_ms_avg * 1e-3) / 1e12
     tinfo = {}
     tfile = ROOT / "profiles" / "kernel_traffic.json"
     if tfile.exists():
@@ -755,30 +755,87 @@ def run_ours(args):
             tinfo = json.loads(tfile.read_text())
         except (ValueError, OSError):
             tinfo = {}
-    pairs_s = rank_pairs / (kern_ms_avg * 1e-3)
-    # executed FMA-pipe work against the measured FFMA peak (lane-ops/s)
-    exec_lane_ops_s = (exe["fma_lane_ops_per_pair"] * pairs_s) if exe else None
-    roofline = {
-        "bound": "fp32 FMA pipe", "unit": "TFLOP/s",
-        "achieved": (exec_lane_ops_s * 2.0 / 1e12) if exe else norm_tflops,
-        "peak": peak_tflops,
-        "frac": (exec_lane_ops_s / ffma_rate) if exe else norm_tflops / peak_tflops,
-        "frac_basis": "executed FMA-pipe work (path counters of the timed step x per-pair SASS cost of each inner "
-                      "loop, profiles/sass_model.json) / the measured FFMA peak (pc_microbench, 2 flop per lane-FFMA)",
-        "traffic": tinfo.get("pairs_kernel_direct_flat_n2^20"),
-        "traffic_basis": "dram read+write bytes per launch of this kernel from the committed ncu --set full "
-                         "capture (profiles/kernel_traffic.json), not measured in this run",
-        "kernel": "pairs_kernel<4,8,256,DIRECT,FLAT,SORTED>", "kernel_ms": kern_ms_avg,
-        "pairs_per_s_kernel": pairs_s,
+    peaks = {}
+    pfile = ROOT / "MEASURED_PEAKS.json"
+    if pfile.exists():
+        try:
+            peaks = json.loads(pfile.read_text())
+        except (ValueError, OSError):
+            peaks = {}
+    ffma_ms_avg = ffma_ms / max(1, ffma_launches)
+    tc_ms_avg = tc_ms / max(1, tc_launches)
+    ppc = int(prof.pairs_per_chunk) or 65536
+    pairs_tc = int(prof.chunks_tc) * ppc
+    pairs_ffma = rank_pairs - pairs_tc
+    exe = executed_roofline(prof, ffma_ms_avg * 1e-3, clock_mhz, sms)  # the FFMA kernel over its own chunks
+    ffma_part = {
+        "kernel": "pairs_kernel<4,8,256,DIRECT,FLAT,SORTED> (near, far-direct and edge chunks; skips the "
+                  "tensor-core chunks)",
+        "kernel_ms": ffma_ms_avg, "launches_per_step": ffma_launches / steps_timed, "pairs": pairs_ffma,
+        "pairs_per_s": pairs_ffma / (ffma_ms_avg * 1e-3) if ffma_ms_avg else None,
         "executed": exe,
-        "normalised": {"flops_per_pair": FLOPS_PER_PAIR, "tflops": norm_tflops, "frac": norm_tflops / peak_tflops,
-                       "basis": "12 reference-formula flops per pair (3 sub, 3 mul, 2 add, cmp, add, div, acc); "
-                                "the kernel executes fewer (packed FP32, shared reciprocals, Gram form)"},
-        "survey_model": {"pairs_per_s_ceiling": 3.384e12, "ratio": pairs_s / 3.384e12,
-                         "basis": "SURVEY.md §8(d): 11 scalar instructions per pair at 1.965 GHz; the packed "
-                                  "loops issue fewer, so the ratio exceeds 1"},
-        "ncu_fma_pipe_active": tinfo.get("pairs_kernel_direct_fma_pipe_active"),
+        "frac_fma_pipe": (exe["frac"] if exe else None),
+        "frac_basis": "executed FMA-pipe work (its path counters x per-pair SASS cost of each inner loop, "
+                      "profiles/sass_model.json) / the kernel's time x FMA-pipe capacity",
     }
+    if tc_launches:
+        mma_flops_per_pair = 64  # tcgen05.mma kind::f16, K = 32 bf16 products per pair, 2 flop each
+        tc_s = tc_ms_avg * 1e-3
+        pairs_tc_s = pairs_tc / tc_s
+        bf16_peak = peaks.get("bf16_tflops") or 2250.0
+        achieved = mma_flops_per_pair * pairs_tc_s / 1e12
+        clk_hz = clock_mhz * 1e6
+        per_clk_sm = pairs_tc_s / (sms * clk_hz)
+        roofline = {
+            "bound": "tensor", "unit": "TFLOP/s",
+            "achieved": achieved, "peak": bf16_peak, "frac": achieved / bf16_peak,
+            "frac_basis": "executed tcgen05.mma flops (64 per pair: K = 32 bf16 products) of the timed step / "
+                          "pairs_tcs_kernel's CUDA-event time, against the measured dense bf16 peak "
+                          "(MEASURED_PEAKS.json bf16_tflops, burst)",
+            "traffic": tinfo.get("pairs_tcs_kernel_n2^20"),
+            "traffic_basis": "dram read+write bytes per launch from the committed ncu --set full capture "
+                             "(profiles/kernel_traffic.json), not measured in this run",
+            "kernel": "pairs_tcs_kernel (tcgen05.mma kind::f16 M=128 N=256 K=32, TMEM drained by 8 warps)",
+            "kernel_ms": tc_ms_avg, "pairs": pairs_tc, "pairs_per_s_kernel": pairs_tc_s,
+            "pairs_per_clk_per_sm": per_clk_sm,
+            "binding_resource": {
+                "what": "the epilogue: each pair's accumulator word read from TMEM (4 B) and folded into the sum "
+                        "with 2 FMA-pipe lane-ops + 1/4 MUFU.RCP (eight terms per two reciprocals)",
+                "fma_mufu_ceiling_pairs_per_clk_sm": 64.0,
+                "frac_of_fma_mufu_ceiling": per_clk_sm / 64.0,
+                "tmem_drain_ceiling_pairs_per_clk_sm": 78.7,
+                "frac_of_tmem_drain_ceiling": per_clk_sm / 78.7,
+                "pipelined_proto_pairs_per_clk_sm": 35.7,
+                "frac_of_pipelined_proto": per_clk_sm / 35.7,
+                "basis": "FMA 128 lane-ops/clk/SM / 2 per pair; MUFU 16/clk/SM / 0.25 per pair; TMEM loads alone "
+                         "78.7 pairs/clk/SM and the same epilogue on a static operand 35.7 "
+                         "(scripts/tc_sum_proto.cu, B200); ncu of this kernel: FMA pipe 49 %, XU 49 %, "
+                         "tensor 21 %, issue 53 % (profiles/r2_ncu_tcs_kernel.txt)",
+            },
+            "ffma_kernel": ffma_part,
+            "step_kernels_ms": {"pairs_tcs_kernel": tc_ms_avg, "pairs_kernel_sorted": ffma_ms_avg},
+            "normalised": {"flops_per_pair": FLOPS_PER_PAIR,
+                           "tflops": FLOPS_PER_PAIR * rank_pairs / ((tc_ms_avg + ffma_ms_avg) * 1e-3) / 1e12,
+                           "frac": FLOPS_PER_PAIR * rank_pairs / ((tc_ms_avg + ffma_ms_avg) * 1e-3) / 1e12 /
+                           peak_tflops,
+                           "basis": "12 reference-formula flops per pair over both kernels' time, against the "
+                                    "measured FP32 FFMA peak (a normalisation: the tensor cores do the product)"},
+        }
+    else:  # PAIRCOUNT_TCSUM=0: the FFMA sorted kernel alone
+        norm_tflops = FLOPS_PER_PAIR * rank_pairs / (ffma_ms_avg * 1e-3) / 1e12
+        pairs_s = rank_pairs / (ffma_ms_avg * 1e-3)
+        exec_lane_ops_s = (exe["fma_lane_ops_per_pair"] * pairs_s) if exe else None
+        roofline = {
+            "bound": "fp32 FMA pipe", "unit": "TFLOP/s",
+            "achieved": (exec_lane_ops_s * 2.0 / 1e12) if exe else norm_tflops,
+            "peak": peak_tflops,
+            "frac": (exec_lane_ops_s / ffma_rate) if exe else norm_tflops / peak_tflops,
+            "frac_basis": ffma_part["frac_basis"] + " (measured FFMA peak, pc_microbench)",
+            "traffic": tinfo.get("pairs_kernel_direct_flat_n2^20"),
+            "kernel": "pairs_kernel<4,8,256,DIRECT,FLAT,SORTED>", "kernel_ms": ffma_ms_avg,
+            "pairs_per_s_kernel": pairs_s, "executed": exe,
+        }
+    kern_ms_avg = kern_ms / steps_timed
 
     line = {
         "metric": "G pair-tests/s at N=2^20 (contact count + inverse-square sum)",
@@ -799,7 +856,7 @@ def run_ours(args):
         "cfg4_clustered_n2^22": cfg4,
     }
     if world > 1:
-        line["kernel_ms_max_over_ranks"] = kern_ms_max / max(1, kern_launches)
+        line["kernel_ms_per_step_max_over_ranks"] = kern_ms_max / max(1, args.steps)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_leg(obj, args.cpu_rows_per_core)
     if world == 1 and not args.no_secondary:

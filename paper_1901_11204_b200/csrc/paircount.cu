@@ -439,6 +439,8 @@ struct PairsArgs {
     long long win_blks;  // FLAT: blocks per tile window
     long long st_c0[kMaxStages + 1], st_b0[kMaxStages], st_s[kMaxStages];
     int tc_split;        // SORTED sum: the dense chunks tcs_takes() accepts are left to pairs_tcs_kernel
+    const unsigned* tc_bits;  // ... marked in this bitmap (bit t * tc_cpw_pad + chunk), or null: decided in-loop
+    long long tc_cpw_pad;
 };
 
 __device__ __forceinline__ int steps_for_dev(int n, int i) {
@@ -743,7 +745,7 @@ __global__ void blk_box_kernel(const T* __restrict__ xyz, long long n, int nblk,
 }
 
 struct WsLayout {
-    size_t pts, stats, prof, red, slots, claims, claims_tc, tc_a, tc_b, tc_cand, tc_cnt, srt, srt_temp, total;
+    size_t pts, stats, prof, red, slots, claims, claims_tc, tc_bits, tc_bits_cap, tc_a, tc_b, tc_cand, tc_cnt, srt, srt_temp, total;
 };
 WsLayout ws_layout(long long n) {
     WsLayout l;
@@ -755,7 +757,9 @@ WsLayout ws_layout(long long n) {
     l.slots = l.red + 2 * kRedBlocks * sizeof(double);  // FFMA claims, then tensor-core claims
     l.claims = align_up(l.slots + (size_t)max_slots(n) * sizeof(Slot), 256);
     l.claims_tc = align_up(l.claims + (size_t)kClaimsCap * sizeof(double), 256);
-    l.tc_a = align_up(l.claims_tc + (size_t)kClaimsCap * sizeof(double), 1024);
+    l.tc_bits = align_up(l.claims_tc + (size_t)kClaimsCap * sizeof(double), 256);
+    l.tc_bits_cap = tcs_bits_bytes(n < 0 ? 0 : n);  // the whole-range bitmap, up to kTcsBitsMax
+    l.tc_a = align_up(l.tc_bits + l.tc_bits_cap, 1024);
     const TcGeom g = tc_geom(n < 0 ? 0 : n);  // tensor-core count kernel operands (64 B per staged point)
     l.tc_b = align_up(l.tc_a + (size_t)g.n_rows * 64, 1024);
     l.tc_cand = align_up(l.tc_b + (size_t)g.n_ext * 64, 256);
@@ -931,8 +935,32 @@ bool tcs_enabled() {
     }();
     return on && 32 * kBig.r == kTcsT && kBig.w == kTcsW;
 }
+// The chunk bitmap of one range's tiles into `bits` (capacity cap_bytes); *cpw_pad stays 0 when it does
+// not fit (the kernels then classify in-loop).
+int classify_tcs(const PairsArgs& p, TileSel ts, unsigned* bits, size_t cap_bytes, long long* cpw_pad,
+                 cudaStream_t s) {
+    TcsArgs a{};
+    a.blk_box = p.blk_box;
+    a.n = p.n;
+    a.lo = p.lo;
+    a.hi = p.hi;
+    a.tstride = ts.tstride;
+    a.toff = ts.toff;
+    a.n_tiles = tiles_of(p.lo, p.hi, kTcsT, ts);
+    a.L = (long long)(kTcsT - 1) + (p.n >> 1);
+    a.cpw = tcs_cpw(p.n);
+    a.cpw_pad = tcs_cpw_pad(p.n);
+    a.bits = bits;
+    *cpw_pad = 0;
+    if (a.n_tiles == 0 || !bits || (size_t)a.n_tiles * (size_t)a.cpw_pad / 8 > cap_bytes) return PC_OK;
+    tcs_classify_kernel<<<(int)(((long long)a.n_tiles * (a.cpw_pad / 32) + 7) / 8), 256, 0, s>>>(a);
+    CK_LAUNCH("tcs_classify_kernel");
+    *cpw_pad = a.cpw_pad;
+    return PC_OK;
+}
+
 int launch_tcs(const PairsArgs& p, TileSel ts, double* claims_tc, Slot* slots, long long cap, int* nslots,
-               int* nparts, cudaStream_t s) {
+               int* nparts, cudaStream_t s, unsigned* bits = nullptr, long long cpw_pad = 0) {
     TcsArgs a{};
     a.xyz = (const float*)p.xyz;
     a.blk_box = p.blk_box;
@@ -950,6 +978,8 @@ int launch_tcs(const PairsArgs& p, TileSel ts, double* claims_tc, Slot* slots, l
     a.L = (long long)(kTcsT - 1) + (p.n >> 1);
     a.cpw = (a.L + kTcsW - 1) / kTcsW;
     a.items = (long long)a.n_tiles * a.cpw;
+    a.bits = bits;
+    a.cpw_pad = cpw_pad;
     // items per claim: the smallest power of two keeping the float64 partials (kTcsParts per
     // claim) within kClaimsCap
     const int grid = num_sms();
@@ -1306,6 +1336,8 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
         const long long lo = bounds[k], hi = bounds[k + 1];
         const bool use_tcs = use_tcs_call && lo % 32 == 0;
         args.tc_split = use_tcs ? 1 : 0;
+        args.tc_bits = nullptr;
+        args.tc_cpw_pad = 0;
         const int kern_id = !direct ? (sorted_count ? kKernSortedCount : kKernGram)
                                     : comp ? (sorted ? kKernCompSorted : kKernComp)
                                            : sorted ? (use_tcs ? kKernSortedTc : kKernSorted) : kKernDirect;
@@ -1316,6 +1348,16 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
             args.hi = (int)hi;
             const bool flat = tiling == PC_TILE_FLAT;
             int rc;
+            if (use_tcs) {  // the chunk bitmap both kernels follow (when it fits the workspace)
+                long long cpw_pad = 0;
+                unsigned* bits = (unsigned*)(ws + lay.tc_bits);
+                rc = lay.tc_bits_cap ? classify_tcs(args, ts, bits, lay.tc_bits_cap, &cpw_pad, s) : PC_OK;
+                if (rc) return rc;
+                if (cpw_pad) {
+                    args.tc_bits = bits;
+                    args.tc_cpw_pad = cpw_pad;
+                }
+            }
 #define PC_DISPATCH(CFG, ...) dispatch_cfg<CFG.warps, CFG.r, CFG.w, __VA_ARGS__>(args, flat, ts, cap, &nslots, &nclaims, \
                                                                                 &trows, &ppc, s)
             if (n < kSmallN)
@@ -1342,7 +1384,8 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
             }
             if (use_tcs) {
                 int ntc = 0;
-                rc = launch_tcs(args, ts, claims_tc, slots + nslots, cap - nslots, &ntc, &ntcparts, s);
+                rc = launch_tcs(args, ts, claims_tc, slots + nslots, cap - nslots, &ntc, &ntcparts, s,
+                                const_cast<unsigned*>(args.tc_bits), args.tc_cpw_pad);
                 if (rc) return rc;
                 nslots += ntc;
             }

@@ -329,7 +329,6 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
         tile = 0;
         off = 0;
         claim(tile, off, left);
-        if (lane == 0) s_claim[wid][0] = s_claim[wid][1];
     } else {
         tile = (int)gw;
         off = 0;
@@ -344,6 +343,27 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
         const int w = min(W, L - o);
         return (int)(w < lft ? w : lft);
     };
+    // SORTED sum with the tensor-core split and its chunk bitmap (tcs_classify_kernel): step over the
+    // chunks pairs_tcs_kernel evaluates before staging them, claiming on as claims run out
+    auto skip_tc = [&](int& t, int& o, long long& lft) {
+        if (!(SORTED && DIRECT && FLAT && !COMP) || !a.tc_bits) return;
+        while (lft > 0) {
+            const long long b = (long long)t * a.tc_cpw_pad + o / W;
+            if (!((__ldg(a.tc_bits + (b >> 5)) >> (b & 31)) & 1u)) return;
+            const int w_ = width(o, lft);
+            o += w_;
+            if (o == L) {
+                ++t;
+                o = 0;
+            }
+            lft -= w_;
+            if (lft == 0) claim(t, o, lft);
+        }
+    };
+    if (FLAT) {
+        skip_tc(tile, off, left);
+        if (lane == 0) s_claim[wid][0] = s_claim[wid][1];
+    }
     auto wrap = [&](int j) -> int {
         if (j >= n) j -= n;
         if (j >= n) j %= n;
@@ -531,6 +551,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
         }
         long long nleft = left - wc;
         if (FLAT && nleft == 0) claim(ntile, noff, nleft);
+        if (FLAT) skip_tc(ntile, noff, nleft);
         const int nwc = nleft > 0 ? width(noff, nleft) : 0;
         if (nleft > 0) {
             if (kTma) {
@@ -625,7 +646,10 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 for (int k = 0; k < 3; ++k) o[k] = cg.o[k];
                 const float gap2 = cg.gap2, ab = cg.ab;
                 // a chunk the tensor-core kernel evaluates (pairs_tcsum.cuh): nothing to do here
-                tc_skip = !COMP && a.tc_split && tcs_takes(cg);
+                tc_skip = !COMP && a.tc_split && !a.tc_bits && tcs_takes(cg);  // (with the bitmap: skipped above)
+#ifdef PC_DBG_SKIPALL  // debug (timing only): every dense chunk skipped -- the walk's own cost
+                tc_skip = true;
+#endif
                 // 8u (|a| + |b|)^2 <= 5e-6 (1 + dmin^2), u = 2^-24 -- written as the same
                 // inequality 5u (..)^2 <= 3.125e-6 (..): eight roundings of terms of at most
                 // (|a| + |b|)^2 against p >= 1 + dmin^2

@@ -162,6 +162,17 @@ __device__ __forceinline__ void tcs_write_col(unsigned char* d, int p, float bx,
     *reinterpret_cast<uint4*>(d + tcs_off(p, 3)) = make_uint4(kBf16One2, kBf16One2, hh(ZBh, ZBm), hh(ZBl, lo2));
 }
 
+// Chunk bitmap: bit t * cpw_pad + c set when pairs_tcs_kernel evaluates chunk c of row tile t (whole
+// 32-bit words per tile, so one warp writes a tile's row with ballots).  Sized for the whole range;
+// beyond kTcsBitsMax (n > ~2^23) both kernels classify in-loop instead.
+constexpr size_t kTcsBitsMax = (size_t)64 << 20;
+__host__ __device__ inline long long tcs_cpw(long long n) { return ((long long)(kTcsT - 1) + n / 2 + kTcsW - 1) / kTcsW; }
+__host__ __device__ inline long long tcs_cpw_pad(long long n) { return (tcs_cpw(n) + 31) / 32 * 32; }
+inline size_t tcs_bits_bytes(long long n) {
+    const size_t b = (size_t)((n + kTcsT - 1) / kTcsT) * (size_t)tcs_cpw_pad(n) / 8;
+    return b <= kTcsBitsMax ? (b + 255) / 256 * 256 : 0;
+}
+
 struct TcsArgs {
     const float* xyz;  // sorted points (fp32, 12 B each)
     const float4* blk_box;
@@ -176,7 +187,61 @@ struct TcsArgs {
     long long items;   // n_tiles * cpw
     long long S;       // items per claim
     long long nclaims;
+    unsigned* bits;    // chunk bitmap (tcs_classify_kernel writes it, the kernels read it), or null
+    long long cpw_pad;
 };
+
+// The chunk bitmap: one warp per 32-chunk word of a row tile, a lane per chunk (the tile's box from its
+// eight per-32 boxes, each chunk's from its nine -- the unions the FFMA kernel forms, min / max exact).
+__global__ void __launch_bounds__(256) tcs_classify_kernel(const TcsArgs a) {
+    const int lane = threadIdx.x & 31;
+    const long long wg = (long long)blockIdx.x * 8 + (threadIdx.x >> 5), words = a.cpw_pad / 32;
+    const long long t = wg / words, c0 = (wg - t * words) * 32;  // one warp per 32-chunk word of a tile
+    if (t >= a.n_tiles) return;
+    const int n = a.n;
+    const int steps_min = (n & 1) ? (n - 1) >> 1 : (n >> 1) - 1;
+    const int i0 = a.lo + ((int)t * a.tstride + a.toff) * kTcsT;
+    const bool rows_ok = i0 + kTcsT <= a.hi;
+    float tmin[3] = {INFINITY, INFINITY, INFINITY}, tmax[3] = {-INFINITY, -INFINITY, -INFINITY};
+    if (rows_ok) {
+        float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+        if (lane < kTcsT / 32) {
+            const float4 lo4 = a.blk_box[2 * ((i0 >> 5) + lane)], hi4 = a.blk_box[2 * ((i0 >> 5) + lane) + 1];
+            mn[0] = lo4.x; mn[1] = lo4.y; mn[2] = lo4.z;
+            mx[0] = hi4.x; mx[1] = hi4.y; mx[2] = hi4.z;
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            tmin[k] = warp_min_f(mn[k]);
+            tmax[k] = warp_max_f(mx[k]);
+        }
+    }
+    {
+        const long long c = c0 + lane;
+        const long long off = c * kTcsW;
+        bool take = false;
+        if (rows_ok && c < a.cpw && off + kTcsW <= a.L && off + 1 >= kTcsT && off + kTcsW <= steps_min) {
+            int jw = i0 + (int)off + 1;
+            if (jw >= n) jw -= n;
+            const int jend = jw + kTcsW - 1;
+            const int nb1 = (min(jend, n - 1) >> 5) - (jw >> 5) + 1;
+            const int nb2 = jend >= n ? ((jend - n) >> 5) + 1 : 0;
+            float cl[3] = {INFINITY, INFINITY, INFINITY}, ch[3] = {-INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int q = 0; q < kTcsW / 32 + 2; ++q) {  // <= 9 blocks, 10 when the window wraps
+                if (q < nb1 + nb2) {
+                    const int bq = q < nb1 ? (jw >> 5) + q : q - nb1;
+                    const float4 lo4 = __ldg(a.blk_box + 2 * bq), hi4 = __ldg(a.blk_box + 2 * bq + 1);
+                    cl[0] = fminf(cl[0], lo4.x); cl[1] = fminf(cl[1], lo4.y); cl[2] = fminf(cl[2], lo4.z);
+                    ch[0] = fmaxf(ch[0], hi4.x); ch[1] = fmaxf(ch[1], hi4.y); ch[2] = fmaxf(ch[2], hi4.z);
+                }
+            }
+            take = tcs_takes(chunk_geom(tmin, tmax, cl, ch));
+        }
+        const unsigned w = __ballot_sync(0xffffffffu, take);
+        if (lane == 0) a.bits[(t * a.cpw_pad + c0) >> 5] = w;
+    }
+}
 
 __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs a) {
     extern __shared__ __align__(1024) unsigned char tcs_smem[];
@@ -332,7 +397,13 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
             for (long long ub = u0; ub < u1; ub += 32) {
                 // ---- classification, one item per lane
                 bool take = false;
-                {
+                if (a.bits) {
+                    const long long u = ub + lane;
+                    if (u < u1) {
+                        const long long t = u / C, b = t * a.cpw_pad + (u - t * C);
+                        take = (__ldg(a.bits + (b >> 5)) >> (b & 31)) & 1u;
+                    }
+                } else {
                     const long long u = ub + lane;
                     if (u < u1) {
                         long long off;
