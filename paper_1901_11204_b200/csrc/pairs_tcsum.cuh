@@ -66,7 +66,7 @@ constexpr int kTcsStages = PC_TCS_STAGES;
 #define PC_TCS_KSTEPS 2
 #endif
 #ifndef PC_TCS_PROD
-#define PC_TCS_PROD 4  // producer warps (13 warps: 16 warp slots of 128 registers; 3 and 7 measured slower)
+#define PC_TCS_PROD 3  // producer warps: 12 warps in all, 168 registers each (13 warps take 16 slots of 128: spills)
 #endif
 #ifndef PC_TCS_EPI
 #define PC_TCS_EPI 8  // epilogue warps: 4 per accumulator (each all its columns) or 8 (half the columns each)
@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(256) tcs_classify_kernel(const TcsArgs a) {
             take = tcs_takes(chunk_geom(tmin, tmax, cl, ch));
         }
         const unsigned w = __ballot_sync(0xffffffffu, take);
+        PC_CHECK(t * a.cpw_pad + c0 + 32 <= (long long)a.n_tiles * a.cpw_pad);
         if (lane == 0) a.bits[(t * a.cpw_pad + c0) >> 5] = w;
     }
 }
@@ -382,6 +383,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
             for (int h = 0; h < kTcsPR; ++h) {
                 int j = jw + min(tid + kTcsPT * h, 255);
                 if (j >= n) j -= n;
+                PC_CHECK(j >= 0 && j < n);
                 const float* src = a.xyz + 3ll * j;
                 q[3 * h] = __ldg(src);
                 q[3 * h + 1] = __ldg(src + 1);
@@ -480,6 +482,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                         for (int h = 0; h < kTcsPR; ++h) {
                             const int p = tid + kTcsPT * h;
                             if (p >= 256) break;
+                            PC_CHECK(i0 + p >= a.lo && i0 + p < a.hi);
                             const float* q = a.xyz + 3ll * (i0 + p);
                             const float ax = __fsub_rn(q[0], o[0]), ay = __fsub_rn(q[1], o[1]), az = __fsub_rn(q[2], o[2]);
                             tcs_write_row(dA, p, ax, ay, az);
@@ -543,6 +546,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                 if (claim != cur) {
                     if (cur >= 0) {
                         const double cs = warp_sum(sum);
+                        PC_CHECK(cur < a.nclaims);
                         if (lane == 0) a.claim_sums[cur * kTcsParts + ew] = cs;
                         sum = 0.0;
                     }
@@ -591,6 +595,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
         }
         if (cur >= 0) {
             const double cs = warp_sum(sum);
+            PC_CHECK(cur < a.nclaims);
             if (lane == 0) a.claim_sums[cur * kTcsParts + ew] = cs;
         }
         sum = 0.0;
