@@ -71,7 +71,12 @@ constexpr int kTcsStages = PC_TCS_STAGES;
 #ifndef PC_TCS_EPI
 #define PC_TCS_EPI 8  // epilogue warps: 4 per accumulator (each all its columns) or 8 (half the columns each)
 #endif
-constexpr int kTcsProd = PC_TCS_PROD, kTcsEpi = PC_TCS_EPI, kTcsWarps = 1 + kTcsProd + kTcsEpi;
+#ifndef PC_TCS_MMA
+#define PC_TCS_MMA 1  // MMA-issuing warps: one for both row halves, or one per row half
+#endif
+constexpr int kTcsMma = PC_TCS_MMA, kTcsProd = PC_TCS_PROD, kTcsEpi = PC_TCS_EPI,
+              kTcsWarps = kTcsMma + kTcsProd + kTcsEpi;
+static_assert(kTcsMma == 1 || PC_TCS_NQ == 1, "one MMA warp per row half: whole-row-half accumulators");
 constexpr int kTcsEpiG = kTcsEpi / 2, kTcsSpan = kTcsNP * 4 / kTcsEpiG;  // warps per accumulator, columns per warp
 static_assert(kTcsNQ == 1 || kTcsEpi == 8, "column-split epilogue for whole-row-half accumulators only");
 constexpr int kTcsPT = kTcsProd * 32, kTcsPR = (256 + kTcsPT - 1) / kTcsPT;  // producer threads, points per thread
@@ -273,11 +278,11 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
     if (threadIdx.x == 0) {
         for (int k = 0; k < kTcsStages; ++k) {
             mbar_init(b_full + 8 * k, kTcsProd);
-            mbar_init(b_empty + 8 * k, 1);
+            mbar_init(b_empty + 8 * k, kTcsMma);
         }
         for (int k = 0; k < 2; ++k) {
             mbar_init(a_full + 8 * k, kTcsProd);
-            mbar_init(a_empty + 8 * k, 1);
+            mbar_init(a_empty + 8 * k, kTcsMma);
         }
         for (int k = 0; k < kTcsNAcc; ++k) {
             mbar_init(acc_full + 8 * k, 2);  // the MMA thread's hand-off + the MMAs' commit
@@ -299,8 +304,8 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
     const int steps_min = (n & 1) ? (n - 1) >> 1 : (n >> 1) - 1;
     double sum = 0.0;
 
-    if (warp == 0) {
-        // ---------------- MMA issuer
+    if (warp < kTcsMma) {
+        // ---------------- MMA issuer(s): warp m issues row half m's MMAs when there are two
         if (lane == 0) {
             long long it = 0;
             long long aloads[2] = {0, 0};
@@ -314,6 +319,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                 const long long tag = s_item[sg];
                 if (tag < 0) {
                     for (int k = 0; k < kTcsNAcc; ++k) {
+                        if (kTcsMma > 1 && k != warp) continue;
                         if (it >= 1) mbar_wait(acc_empty + 8 * k, (unsigned)((it - 1) & 1));
                         s_meta[k] = -1;
                         mbar_arrive_plain(acc_full + 8 * k);
@@ -336,6 +342,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                     // accumulator k = (row half h, column piece q) = h NQ + q, in the order the two
                     // epilogue groups release them: (0,0), (1,0), (0,1), (1,1), ...
                     const int h = kk & 1, q = kk >> 1, k = h * kTcsNQ + q;
+                    if (kTcsMma > 1 && h != warp) continue;
                     if (it >= 1) mbar_wait(acc_empty + 8 * k, (unsigned)((it - 1) & 1));
                     s_meta[k] = tag >> 2;
                     mbar_arrive_plain(acc_full + 8 * k);  // release: the epilogue reads s_meta after its wait
@@ -353,15 +360,15 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                 }
                 tc_commit(b_empty + 8 * sg);
             }
-            s_items = items;
+            if (warp == 0) s_items = items;
         }
-    } else if (warp <= kTcsProd) {
+    } else if (warp < kTcsMma + kTcsProd) {
         // ---------------- producers: claims, classification, operands
         // Per claim: the items are classified 32 at a time (lane l takes item ub + l: its tile's
         // and chunk's per-32 boxes -- the same union of boxes the FFMA kernel reduces across its
         // lanes, min/max being exact -- then chunk_geom / tcs_takes), and the eligible ones are
         // built in order with the next one's column coordinates already in flight.
-        const int pw = warp - 1, tid = pw * 32 + lane;
+        const int pw = warp - kTcsMma, tid = pw * 32 + lane;
         long long it = 0, nclaim = 0;
         int sg = 0, abuf = 1;
         long long aloads[2] = {0, 0};
@@ -529,7 +536,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
         if (lane == 0) mbar_arrive_plain(b_full + 8 * sg);
     } else {
         // ---------------- epilogue: group h drains accumulators (h, 0) and (h, 1), lane quadrant warp % 4
-        const int ew = warp - 1 - kTcsProd, h = ew / kTcsEpiG, quad = warp & 3, cpart = (ew % kTcsEpiG) >> 2;
+        const int ew = warp - kTcsMma - kTcsProd, h = ew / kTcsEpiG, quad = warp & 3, cpart = (ew % kTcsEpiG) >> 2;
         long long cur = -1;
         for (long long it = 0;; ++it) {
             bool done = false;
