@@ -117,7 +117,8 @@ typedef struct {
     int64_t pairs_per_chunk; /* T x W of the kernel (0: tensor-core or no kernel)      */
     int32_t kernel;          /* 1 Gram count, 2 direct sum, 3 sorted sum, 4 compensated sum, 5 tensor-core
                                 count, 6 INT32 key count, 7 thread-per-row (paper), 8 pruned sorted count,
-                                9 sorted sum of float64 points, 10 sorted sum with tensor-core Gram chunks */
+                                9 sorted sum of float64 points, 10 sorted sum with tensor-core Gram chunks,
+                                11 sorted sum of float64 points with tensor-core Gram chunks */
     int32_t f64_taken;       /* 1: the float64 kernel evaluated the sum (non-finite / huge / wide input) */
     int64_t chunks_tc;       /* sorted sum: T x W chunks evaluated on the tensor cores (pairs_tcs_kernel) */
 } pc_pairs_profile;

@@ -395,7 +395,7 @@ struct Slot {
 static_assert(sizeof(Slot) == 64, "Slot is one 64-byte record");
 // kernel ids recorded in pc_pairs_profile.kernel
 constexpr int kKernGram = 1, kKernDirect = 2, kKernSorted = 3, kKernComp = 4, kKernTc = 5, kKernKey = 6,
-              kKernRow = 7, kKernSortedCount = 8, kKernCompSorted = 9, kKernSortedTc = 10;
+              kKernRow = 7, kKernSortedCount = 8, kKernCompSorted = 9, kKernSortedTc = 10, kKernCompSortedTc = 11;
 
 // FLAT work claims (guided self-scheduling): claim c of stage k covers columns
 // [b0[k] + (c - c0[k]) * s[k], + s[k]) of the flat (row tile, window column) space.  Stage k
@@ -632,6 +632,7 @@ constexpr KernelCfg kBigComp{4, 4, PC_COMP_W};          // compensated sum kerne
 #define PC_COMP_SORTED_W 192
 #endif
 constexpr KernelCfg kBigCompSorted{4, PC_COMP_SORTED_R, PC_COMP_SORTED_W};  // float64 points, sorted
+constexpr KernelCfg kBigCompSortedTc{4, 8, 256};  // ... beside the tensor-core kernel (its tile and chunk)
 constexpr KernelCfg kSmall{4, 2, 64};  // warp tile 64 rows, for n < kSmallN
 constexpr int kSmallN = 16384;
 
@@ -962,7 +963,7 @@ int classify_tcs(const PairsArgs& p, TileSel ts, unsigned* bits, size_t cap_byte
 int launch_tcs(const PairsArgs& p, TileSel ts, double* claims_tc, Slot* slots, long long cap, int* nslots,
                int* nparts, cudaStream_t s, unsigned* bits = nullptr, long long cpw_pad = 0) {
     TcsArgs a{};
-    a.xyz = (const float*)p.xyz;
+    a.xyz = p.xyz;
     a.blk_box = p.blk_box;
     a.st = p.st;
     a.slots = slots;
@@ -995,7 +996,8 @@ int launch_tcs(const PairsArgs& p, TileSel ts, double* claims_tc, Slot* slots, l
     int dev = 0;
     CK(cudaGetDevice(&dev));
     if (!attr_set[dev & 63]) {
-        CK(cudaFuncSetAttribute(pairs_tcs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcsSmem));
+        CK(cudaFuncSetAttribute(pairs_tcs_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcsSmem));
+        CK(cudaFuncSetAttribute(pairs_tcs_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcsSmem));
         attr_set[dev & 63] = true;
     }
     CK(cudaMemsetAsync(a.work_ctr, 0, sizeof(unsigned long long), s));
@@ -1011,7 +1013,8 @@ int launch_tcs(const PairsArgs& p, TileSel ts, double* claims_tc, Slot* slots, l
         ev->kind = 1;
         CK(cudaEventRecord(ev->a, s));
     }
-    pairs_tcs_kernel<<<grid, kTcsWarps * 32, kTcsSmem, s>>>(a);
+    if (p.dtype == PC_F64) pairs_tcs_kernel<double><<<grid, kTcsWarps * 32, kTcsSmem, s>>>(a);
+    else pairs_tcs_kernel<float><<<grid, kTcsWarps * 32, kTcsSmem, s>>>(a);
     CK_LAUNCH("pairs_tcs_kernel");
     if (ev) CK(cudaEventRecord(ev->b, s));
     *nslots = grid;
@@ -1330,7 +1333,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
     }
     // sorted fp32 sums: the Gram chunks the tensor cores can take go to pairs_tcs_kernel (ranges
     // starting on a 32-point block, so both kernels see the same per-32 boxes of every tile)
-    const bool use_tcs_call = sorted && !comp && n >= kSmallN && tcs_enabled();
+    const bool use_tcs_call = sorted && (!comp || dtype == PC_F64) && n >= kSmallN && tcs_enabled();
     double* claims_tc = (double*)(ws + lay.claims_tc);
     for (int k = 0; k < nranges; ++k) {
         const long long lo = bounds[k], hi = bounds[k + 1];
@@ -1339,7 +1342,7 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
         args.tc_bits = nullptr;
         args.tc_cpw_pad = 0;
         const int kern_id = !direct ? (sorted_count ? kKernSortedCount : kKernGram)
-                                    : comp ? (sorted ? kKernCompSorted : kKernComp)
+                                    : comp ? (sorted ? (use_tcs ? kKernCompSortedTc : kKernCompSorted) : kKernComp)
                                            : sorted ? (use_tcs ? kKernSortedTc : kKernSorted) : kKernDirect;
         int nslots = 0, nclaims = 0, trows = 1, ntcparts = 0;
         long long ppc = 0;
@@ -1365,7 +1368,9 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
                      : direct ? PC_DISPATCH(kSmall, true)
                               : PC_DISPATCH(kSmall, false);
             else
-                rc = comp     ? (sorted ? PC_DISPATCH(kBigCompSorted, true, true, true) : PC_DISPATCH(kBigComp, true, true))
+                rc = comp     ? (sorted ? (use_tcs ? PC_DISPATCH(kBigCompSortedTc, true, true, true)
+                                          : PC_DISPATCH(kBigCompSorted, true, true, true))
+                                : PC_DISPATCH(kBigComp, true, true))
                      : sorted ? PC_DISPATCH(kBig, true, false, true)
                      : direct ? PC_DISPATCH(kBig, true)
                      : sorted_count ? PC_DISPATCH(kBigGram, false, false, true)

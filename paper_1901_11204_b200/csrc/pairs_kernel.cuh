@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
     // SORTED sum with the tensor-core split and its chunk bitmap (tcs_classify_kernel): step over the
     // chunks pairs_tcs_kernel evaluates before staging them, claiming on as claims run out
     auto skip_tc = [&](int& t, int& o, long long& lft) {
-        if (!(SORTED && DIRECT && FLAT && !COMP) || !a.tc_bits) return;
+        if (!(SORTED && DIRECT && FLAT) || !a.tc_bits) return;
         while (lft > 0) {
             const long long b = (long long)t * a.tc_cpw_pad + o / W;
             if (!((__ldg(a.tc_bits + (b >> 5)) >> (b & 31)) & 1u)) return;
@@ -646,7 +646,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 for (int k = 0; k < 3; ++k) o[k] = cg.o[k];
                 const float gap2 = cg.gap2, ab = cg.ab;
                 // a chunk the tensor-core kernel evaluates (pairs_tcsum.cuh): nothing to do here
-                tc_skip = !COMP && a.tc_split && !a.tc_bits && tcs_takes(cg);  // (with the bitmap: skipped above)
+                tc_skip = a.tc_split && !a.tc_bits && tcs_takes(cg);  // (with the bitmap: skipped above)
 #ifdef PC_DBG_SKIPALL  // debug (timing only): every dense chunk skipped -- the walk's own cost
                 tc_skip = true;
 #endif

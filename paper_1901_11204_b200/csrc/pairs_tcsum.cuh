@@ -179,7 +179,7 @@ inline size_t tcs_bits_bytes(long long n) {
 }
 
 struct TcsArgs {
-    const float* xyz;  // sorted points (fp32, 12 B each)
+    const void* xyz;   // sorted points (fp32, or float64 for the compensated path)
     const float4* blk_box;
     const PrepStats* st;
     Slot* slots;
@@ -249,7 +249,12 @@ __global__ void __launch_bounds__(256) tcs_classify_kernel(const TcsArgs a) {
     }
 }
 
+// T = float: fp32 points, a = fl32(q - o); T = double: float64 points (the sorted compensated path),
+// a = fl32((q - c) - o) with c the bounding-box centre the FFMA kernel's centred boxes use -- one
+// rounding either way, so the same error bound holds.
+template <typename T>
 __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs a) {
+    constexpr bool kF64 = sizeof(T) == 8;
     extern __shared__ __align__(1024) unsigned char tcs_smem[];
     unsigned char* base = (unsigned char*)(((uintptr_t)tcs_smem + 1023) & ~(uintptr_t)1023);
     unsigned char* sA = base;              // [2][kTcsOp]
@@ -264,7 +269,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
     __shared__ unsigned s_items;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool skip = f64_takes(*a.st, a.dtype, false);  // the float64 kernel takes this call
+    const bool skip = f64_takes(*a.st, a.dtype, kF64);  // the float64 kernel takes this call
     if (skip || a.n_tiles == 0) {
         if (threadIdx.x == 0) a.slots[blockIdx.x] = Slot{};
         return;
@@ -385,17 +390,27 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
             const int j0 = row0t(tt) + (int)off + 1;
             return j0 >= n ? j0 - n : j0;
         };
-        auto load_cols = [&](int jw, float (&q)[3 * kTcsPR]) {
+        const T* xyz = (const T*)a.xyz;
+        double cc[3] = {0.0, 0.0, 0.0};  // float64 points: the bounding-box centre of the centred boxes
+        if (kF64) {
+            long long ci[3];
+            bbox_centre(*a.st, PC_F64, cc, ci);
+        }
+        auto load_cols = [&](int jw, T (&q)[3 * kTcsPR]) {
 #pragma unroll
             for (int h = 0; h < kTcsPR; ++h) {
                 int j = jw + min(tid + kTcsPT * h, 255);
                 if (j >= n) j -= n;
                 PC_CHECK(j >= 0 && j < n);
-                const float* src = a.xyz + 3ll * j;
+                const T* src = xyz + 3ll * j;
                 q[3 * h] = __ldg(src);
                 q[3 * h + 1] = __ldg(src + 1);
                 q[3 * h + 2] = __ldg(src + 2);
             }
+        };
+        auto rel = [&](T q, int k) -> float {  // the coordinate relative to the tile centre o, one rounding
+            if constexpr (kF64) return (float)(((double)q - cc[k]) - (double)o[k]);
+            else return __fsub_rn((float)q, o[k]);
         };
         for (;; ++nclaim) {
             if (tid == 0) s_pclaim[nclaim & 1] = (long long)atomicAdd(a.work_ctr, 1ull);
@@ -444,7 +459,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                 unsigned mask = __ballot_sync(0xffffffffu, take);
                 if (!mask) continue;
                 // ---- the eligible items, in order, one ahead in flight
-                float cur[3 * kTcsPR], nxt[3 * kTcsPR];
+                T cur[3 * kTcsPR], nxt[3 * kTcsPR];
                 int e = __ffs(mask) - 1;
                 mask &= mask - 1;
                 long long eoff;
@@ -490,8 +505,8 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                             const int p = tid + kTcsPT * h;
                             if (p >= 256) break;
                             PC_CHECK(i0 + p >= a.lo && i0 + p < a.hi);
-                            const float* q = a.xyz + 3ll * (i0 + p);
-                            const float ax = __fsub_rn(q[0], o[0]), ay = __fsub_rn(q[1], o[1]), az = __fsub_rn(q[2], o[2]);
+                            const T* q = xyz + 3ll * (i0 + p);
+                            const float ax = rel(q[0], 0), ay = rel(q[1], 1), az = rel(q[2], 2);
                             tcs_write_row(dA, p, ax, ay, az);
                         }
                         fence_proxy_async_shared();
@@ -511,8 +526,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                     for (int h = 0; h < kTcsPR; ++h) {
                         const int p = tid + kTcsPT * h;
                         if (p >= 256) break;
-                        const float bx = __fsub_rn(cur[3 * h], o[0]), by = __fsub_rn(cur[3 * h + 1], o[1]),
-                                    bz = __fsub_rn(cur[3 * h + 2], o[2]);
+                        const float bx = rel(cur[3 * h], 0), by = rel(cur[3 * h + 1], 1), bz = rel(cur[3 * h + 2], 2);
                         tcs_write_col(dB, p, bx, by, bz);
                     }
                     fence_proxy_async_shared();

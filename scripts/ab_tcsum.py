@@ -24,13 +24,15 @@ work = ["cfg3"] + (["cfg4u", "cfg4c"] if os.environ.get("AB_CFG4") else [])
 st = torch.cuda.current_stream()
 for name in work:
     x = config_input(cfgs, name)
+    if os.environ.get("AB_F64"):  # the float64 points the reference's generators return
+        x = x.astype(np.float64)
     n = len(x)
     d = torch.from_numpy(x).cuda()
     ws = torch.empty(_lib.workspace_bytes(n), dtype=torch.uint8, device="cuda")
     res = torch.zeros(6, dtype=torch.int64, device="cuda")
 
     def call():
-        _lib.pairs_async(d.data_ptr(), _lib.PC_F32, n, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, np.array([0, n]),
+        _lib.pairs_async(d.data_ptr(), _lib.PC_F64 if x.dtype == np.float64 else _lib.PC_F32, n, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, np.array([0, n]),
                          ws.data_ptr(), ws.numel(), res.data_ptr(), st.cuda_stream, _lib.PC_TILE_AUTO)
 
     for _ in range(2):
@@ -51,7 +53,7 @@ for name in work:
     prof = _lib.profile_read(ws.data_ptr(), n, st.cuda_stream).as_dict()
     g = gold[name]
     rel = abs(r.sum - g["inv_sum"]) / g["inv_sum"]
-    print(json.dumps({"workload": name, "tcsum": os.environ.get("PAIRCOUNT_TCSUM", "1"), "step_ms": round(step, 3),
+    print(json.dumps({"workload": name + (" f64" if x.dtype == np.float64 else ""), "tcsum": os.environ.get("PAIRCOUNT_TCSUM", "1"), "step_ms": round(step, 3),
                       "timed_kernels_ms": round(kms / reps, 3), "ffma_ms": round(fms / reps, 3), "tc_ms": round(tms / reps, 3), "launches_per_step": cnt / reps,
                       "count": r.count, "count_ok": r.count == g["count"], "sum": r.sum, "sum_rel_err": rel,
                       "pairs": r.pairs, "error": r.error, "profile": prof}), flush=True)

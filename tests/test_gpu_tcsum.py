@@ -66,6 +66,24 @@ def test_tcsum_matches_oracle(n):
         assert _chunks(prof) == tiles * -(-(255 + n // 2) // 256), name
 
 
+@pytest.mark.parametrize("n", [32768, 65537])
+def test_tcsum_float64_points_match_oracle(n):
+    # float64 points (what the reference's generators return): the compensated sorted kernel beside
+    # the tensor-core kernel, which forms a = fl32((q - c) - o) in float64 (kernel 11)
+    for name, pts in _inputs(n, n + 11).items():
+        pts = np.ascontiguousarray(pts, dtype=np.float64)
+        want_c, want_s, pairs = c_oracle.rows(pts, 0, n, "balanced")
+        (r,) = _lib.pairs_host(pts, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, n])
+        prof = _lib.last_profile()
+        assert (r.count, r.pairs, r.error) == (want_c, pairs, 0), name
+        assert abs(r.sum - want_s) <= 1e-6 * want_s, (name, r.sum, want_s)
+        if TCS:
+            assert prof.kernel == 11, (name, prof.kernel)
+        if not prof.f64_taken:  # (a span beyond the compensated staging goes to the float64 kernel)
+            tiles = -(-n // 256)
+            assert _chunks(prof) == tiles * -(-(255 + n // 2) // 256), name
+
+
 def test_tcsum_takes_most_chunks_of_the_headline_shape():
     if not TCS:
         pytest.skip("PAIRCOUNT_TCSUM=0")
