@@ -981,11 +981,13 @@ int launch_tcs(const PairsArgs& p, TileSel ts, double* claims_tc, Slot* slots, l
     a.items = (long long)a.n_tiles * a.cpw;
     a.bits = bits;
     a.cpw_pad = cpw_pad;
-    // items per claim: the smallest power of two keeping the float64 partials (kTcsParts per
-    // claim) within kClaimsCap
+    // items per claim: a power of two keeping the float64 partials (kTcsParts per claim) within
+    // kClaimsCap, and as large as ~128 claims per CTA allows (up to 128 items): a claim's items are
+    // consecutive chunks of one tile, so small claims rebuild the row operand often (tile parts)
     const int grid = num_sms();
     long long S = 1;
     while (S * (kClaimsCap / kTcsParts) < a.items) S *= 2;
+    while (S < 128 && S * 2 * (long long)grid * 128 <= a.items) S *= 2;
     a.S = S;
     a.nclaims = (a.items + S - 1) / S;
     *nslots = 0;
