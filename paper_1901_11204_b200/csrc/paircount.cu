@@ -19,6 +19,12 @@
 //   pairs_tc.cuh      the count filter on the tensor cores: tcgen05.mma tf32
 //                     (3xTF32) into TMEM, warp-specialised loader / MMA /
 //                     drain warps, candidate queues + exact pass
+//   pairs_tcsum.cuh   the sorted sum's Gram chunks on the tensor cores:
+//                     chunk bitmap, tcgen05.mma kind::f16 on three-way bf16
+//                     splits (operands built in shared memory per item), TMEM
+//                     drained with eight terms per two reciprocals
+//   pairs_key.cuh     exact coincidences by 30-bit keys on the INT32 pipe
+//   pairs_row.cuh     the paper's thread-per-row schemes (a baseline)
 //   lattice.cuh       counting-array kernels (sparse regime) and the driver
 //   lattice_slab.cuh  dense regime: key partition + shared-memory slabs + TMA
 //                     bulk stores

@@ -1,47 +1,44 @@
 // Tensor-core Gram chunks of the sorted inverse-square sum (included by paircount.cu
-// inside its anonymous namespace, after pairs_tc.cuh).
+// inside its anonymous namespace, after pairs_tc.cuh).  DESIGN.md §3 "pairs_tcs_kernel".
 //
 // The sorted sum kernel (pairs_kernel.cuh, SORTED + DIRECT) evaluates most of its
 // chunks in tile-local Gram form, p = A_i + B_j - 2 a_i.b_j with a = q_i - o,
 // b = q_j - o about the row tile's centre o: a matrix product plus a per-pair
 // epilogue.  Here that product runs on the 5th-generation tensor cores and the
-// FFMA pipe is left with the epilogue alone:
-//   * tcgen05.mma kind::tf32, M = 128 rows, N = 128 columns, K = 24: every operand
-//     split three ways into exact tf32 pieces x = h + m + l (h, m the
-//     round-to-nearest tf32 of x and of x - h, l = x - h - m), products
-//       a_h b_h + a_h b_m + a_m b_h + a_h b_l + a_m b_m + a_l b_h   (the b side carries -2)
-//       + (A_h + A_m + A_l) + (B_h + B_m + B_l)
-//     all exact in fp32 (dropped terms <= 2^-33 |a||b|); what remains is the tensor
-//     core's fp32 accumulation, measured at <= 3.2u (1 + (|a| + |b|)^2) on 300k pairs of
-//     nine geometries (scripts/tc_prec_proto.cu: 2.1-3.2u; the FFMA2 Gram form measures
-//     2.2-4.0u there).  Bound used for a chunk (DESIGN.md §3 "Error budget"): A_i and
-//     B_j roundings 4u|a|^2 + 3u|b|^2, the subtractions a = q - o, b = q - o 2u(|a|+|b|)^2,
-//     the accumulation taken as 6u (1 + (|a|+|b|)^2): <= 6u + 12u (|a|max + |b|max)^2.
-//   * epilogue: the accumulator's p values, eight terms per two reciprocals, packed:
-//     1/a + 1/c + 1/e + 1/g = ((a+c) eg + (e+g) ac) / (ac eg) in the x lanes (even
-//     columns) and the y lanes (odd columns) -- 8 FFMA2/FMUL2/FADD2 + 2 MUFU per eight
-//     pairs, against 11 + 2 for the FFMA2 Gram loop without the product.
-// Which chunks: the dense chunks (every cell owned) of whole 256-row tiles whose boxes
-// satisfy tcs_takes() -- 12u (|a|+|b|)^2 <= 3.125e-6 (1 + dmin^2), dmin^2 > 4.5 (no
-// contact in the chunk, so no contact test here), |a|+|b| <= 3e4 (the four-term products
-// stay finite).  The FFMA sorted kernel runs first over the same (tile, chunk) space and
-// skips exactly these chunks: both evaluate chunk_geom() on the same boxes with explicit
-// round-to-nearest operations, so every chunk has one owner.
+// FP32 pipes are left with the epilogue:
+//   * tcgen05.mma.cta_group::1.kind::f16, M = 128 rows (a row half of the 256-row
+//     tile), N = 256 columns (the chunk), K = 32 as two K = 16 steps: every coordinate
+//     split three ways into exact bf16 pieces x = h + m + l, products
+//       a_h.b_{h,m,l} + a_m.b_{h,m,l} + a_l.b_{h,m}    (the b side carries -2)
+//       + (A_h + A_m + A_l + A_lo) + (B_h + B_m + B_l + B_lo)
+//     with A = 1 + |a|^2, B = |b|^2 computed in float64 and carried as fp32 hi + lo: every
+//     product exact in fp32, a_l.b_l (<= 2^-32 |a||b|) dropped.  What remains is the
+//     rounding of a = q - o, b = q - o (2u (|a|+|b|)^2) and the tensor core's fp32
+//     accumulation, measured at <= 3.2u (1 + (|a|+|b|)^2) over nine geometries
+//     (scripts/tc_prec_proto.cu) and allowed 6u: the FFMA Gram form's 8u (|a|+|b|)^2 test.
+//   * epilogue: eight terms per two reciprocals, packed: 1/a + 1/c + 1/e + 1/g =
+//     ((a+c) eg + (e+g) ac) / (ac eg) in the x lanes (even columns) and the y lanes (odd
+//     columns) -- 8 FFMA2/FMUL2/FADD2 + 2 MUFU per eight pairs.
+// Which chunks: tcs_classify_kernel's bitmap (or, beyond its size cap, the same test
+// in-loop): dense chunks of whole 256-row tiles whose boxes pass tcs_takes() -- the
+// Gram test, dmin^2 > 4.5 (no contact in the chunk, so no contact test here), and
+// |a|+|b| <= 3e4 (the four-term products stay finite).  The FFMA sorted kernel skips
+// exactly these chunks: both form the boxes as unions of the per-32 boxes and evaluate
+// chunk_geom() with explicit round-to-nearest operations, so every chunk has one owner.
 //
 // Work: items (row tile, chunk) of the FFMA kernel's 256 x 256 geometry in tile-major
-// order, claimed S at a time from one counter.  Each item is four accumulators of
-// 128 x 128: (row half h, column half q).  CTA = 13 warps, one per SM:
+// order, claimed S at a time from one counter.  An item is two accumulators of 128 x 256
+// (the row halves), all 512 TMEM columns.  CTA = 12 warps, one per SM:
 //   warp 0       MMA issuer (one elected thread)
-//   warps 1-4    producers: claim items, classify them (chunk_geom on the per-32 boxes),
-//                build the row operand A (256 rows, on a tile change) and the column
-//                operand B (256 columns, every item) in shared memory from the sorted
-//                points -- K-major no-swizzle layout, 768 B per 8 points
-//   warps 5-12   epilogue: group h = (w - 5) / 4 drains the row-half-h accumulators
-//                (TMEM lanes 32 (w % 4) ..), one column half at a time: 128 values into
-//                registers, the accumulator released, then the arithmetic -- so the
-//                next MMA, the other column half's drain and this arithmetic overlap.
-// Sums: each epilogue warp keeps a float64 partial per claim (its rows and columns of
-// the claim's items, in item order) and writes it to claim_sums[claim * 8 + warp]: the
+//   warps 1-3    producers: claim items, read the bitmap, build the row operand A (256
+//                rows, on a tile change) and the column operand B (256 columns, every
+//                item, the next item's coordinates already in flight) in shared memory --
+//                K-major no-swizzle layout, 512 B per 8 points
+//   warps 4-11   drain: group h (4 warps, one per TMEM lane quadrant) reads accumulator h
+//                in two rounds of 128 columns, releases it after the second round's loads,
+//                and folds the values -- so the next MMA overlaps the last round's arithmetic.
+// Sums: each drain warp keeps a float64 partial per claim (its rows and columns of the
+// claim's items, in item order) and writes it to claim_sums[claim * 8 + warp]: the
 // claim's composition is fixed by its index, so the float64 total is bit-reproducible.
 
 constexpr int kTcsT = 256, kTcsW = 256;           // the FFMA sorted kernel's tile and chunk
