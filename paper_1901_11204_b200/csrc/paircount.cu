@@ -935,6 +935,15 @@ int dispatch_cfg(PairsArgs args, bool flat, TileSel ts, long long cap, int* nslo
 #ifndef PC_TCSUM
 #define PC_TCSUM 1
 #endif
+// PAIRCOUNT_TCS_BITMAP=0: classify chunks in-loop in both kernels (the path beyond the bitmap's size
+// cap), for tests at sizes where the bitmap would fit
+bool tcs_bitmap_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("PAIRCOUNT_TCS_BITMAP");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 bool tcs_enabled() {
     static const bool on = [] {
         const char* e = getenv("PAIRCOUNT_TCSUM");
@@ -1362,7 +1371,8 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
             if (use_tcs) {  // the chunk bitmap both kernels follow (when it fits the workspace)
                 long long cpw_pad = 0;
                 unsigned* bits = (unsigned*)(ws + lay.tc_bits);
-                rc = lay.tc_bits_cap ? classify_tcs(args, ts, bits, lay.tc_bits_cap, &cpw_pad, s) : PC_OK;
+                rc = lay.tc_bits_cap && tcs_bitmap_enabled() ? classify_tcs(args, ts, bits, lay.tc_bits_cap, &cpw_pad, s)
+                                                              : PC_OK;
                 if (rc) return rc;
                 if (cpw_pad) {
                     args.tc_bits = bits;

@@ -71,6 +71,9 @@ constexpr int kTcsStages = PC_TCS_STAGES;
 #ifndef PC_TCS_MMA
 #define PC_TCS_MMA 1  // MMA-issuing warps: one for both row halves, or one per row half
 #endif
+#ifndef PC_TCS_OOO
+#define PC_TCS_OOO 0  // one MMA thread, the two row halves advanced independently
+#endif
 constexpr int kTcsMma = PC_TCS_MMA, kTcsProd = PC_TCS_PROD, kTcsEpi = PC_TCS_EPI,
               kTcsWarps = kTcsMma + kTcsProd + kTcsEpi;
 static_assert(kTcsMma == 1 || PC_TCS_NQ == 1, "one MMA warp per row half: whole-row-half accumulators");
@@ -82,6 +85,14 @@ constexpr long long kTcsParts = kTcsEpi;           // float64 partials per claim
 // instruction descriptor (kind::f16): D f32, A/B bf16, both K-major, N = kTcsNP, M = 128
 constexpr uint32_t kTcsIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTcsNP >> 3) << 17) |
                                ((uint32_t)(128 >> 4) << 24);
+
+__device__ __forceinline__ bool mbar_test_wait(unsigned bar, unsigned parity) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+    return ok != 0;
+}
 
 // exact three-way bf16 split x = h + m + l (round to nearest even; 8 + 8 + 8 significant bits)
 __device__ __forceinline__ float bf16r(float x) {  // round to nearest even on the integer pipe (finite x)
@@ -306,7 +317,77 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
     const int steps_min = (n & 1) ? (n - 1) >> 1 : (n >> 1) - 1;
     double sum = 0.0;
 
+#if PC_TCS_OOO
+    if (warp == 0) {
+        // ---------------- MMA issuer, the two row halves decoupled: each half advances through the
+        // items as soon as its own accumulator is free, so one drain group never waits for the other
+        if (lane == 0) {
+            const uint64_t dA0 = tcs_desc((unsigned)__cvta_generic_to_shared(sA));
+            const uint64_t dB0 = tcs_desc((unsigned)__cvta_generic_to_shared(sB));
+            long long nit[2] = {0, 0};    // next item of each half
+            int cur_ab[2] = {-1, -1};     // A buffer each half last used
+            long long aw[2][2] = {{0, 0}, {0, 0}};  // a_full waits per half and buffer
+            int issued[kTcsStages];       // halves issued on each stage's current item
+            for (int k = 0; k < kTcsStages; ++k) issued[k] = 0;
+            bool done[2] = {false, false};
+            unsigned items = 0, idle = 0;
+            while (!(done[0] && done[1])) {
+                bool moved = false;
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {
+                    if (done[h]) continue;
+                    const long long i = nit[h];
+                    const int sg = (int)(i % kTcsStages);
+                    if (!mbar_test_wait(b_full + 8 * sg, (unsigned)((i / kTcsStages) & 1))) continue;
+                    if (i >= 1 && !mbar_test_wait(acc_empty + 8 * h, (unsigned)((i - 1) & 1))) continue;
+                    const long long tag = s_item[sg];
+                    if (tag < 0) {  // the sentinel: this half's drain group stops
+                        s_meta[h] = -1;
+                        mbar_arrive_plain(acc_full + 8 * h);
+                        mbar_arrive_plain(acc_full + 8 * h);
+                        done[h] = true;
+                        moved = true;
+                        continue;
+                    }
+                    const int ab = (int)((tag >> 1) & 1);
+                    if (ab != cur_ab[h]) {  // this half's first item on a new row operand
+                        const int old = cur_ab[h];
+                        // (not a blocking wait: the other half may have to move off this buffer first)
+                        if (!mbar_test_wait(a_full + 8 * ab, (unsigned)(aw[h][ab] & 1))) continue;
+                        ++aw[h][ab];
+                        cur_ab[h] = ab;
+                        // the old buffer is free once neither half uses it (after the MMAs so far)
+                        if (old >= 0 && cur_ab[h ^ 1] != old) tc_commit(a_empty + 8 * old);
+                    }
+                    s_meta[h] = tag >> 2;
+                    mbar_arrive_plain(acc_full + 8 * h);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint64_t da = dA0 + (uint64_t)((ab * kTcsOp + h * kTcsHalf) >> 4),
+                                   db = dB0 + (uint64_t)((sg * kTcsOp) >> 4);
+#pragma unroll
+                    for (int ks = 0; ks < PC_TCS_KSTEPS; ++ks) {
+                        asm volatile(
+                            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                            " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (unsigned)(h * kTcsNP)),
+                            "l"(da + (uint64_t)(16 * ks)), "l"(db + (uint64_t)(16 * ks)), "r"(kTcsIdesc), "r"(ks));
+                    }
+                    tc_commit(acc_full + 8 * h);
+                    if (++issued[sg] == 2) {  // both halves of this stage's item issued
+                        issued[sg] = 0;
+                        tc_commit(b_empty + 8 * sg);
+                        ++items;
+                    }
+                    nit[h] = i + 1;
+                    moved = true;
+                }
+                if (!moved && ++idle == (1u << 30)) __trap();  // a lost arrival must fail loudly
+            }
+            s_items = items;
+        }
+    } else if (false) {
+#else
     if (warp < kTcsMma) {
+#endif
         // ---------------- MMA issuer(s): warp m issues row half m's MMAs when there are two
         if (lane == 0) {
             long long it = 0;

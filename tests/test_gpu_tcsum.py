@@ -134,6 +134,29 @@ def test_tcsum_agrees_with_the_ffma_only_path(tmp_path):
         assert abs(s - s0) <= 1e-6 * s0, (name, s, s0)
 
 
+def test_tcsum_in_loop_classification_matches_the_bitmap(tmp_path):
+    # beyond the bitmap's size cap (n > ~2^23) both kernels classify every chunk in-loop;
+    # PAIRCOUNT_TCS_BITMAP=0 forces that path here: the same chunks, the same total, bit for bit
+    if not TCS:
+        pytest.skip("PAIRCOUNT_TCSUM=0")
+    n = 2**17 + 5
+    files, got = [], []
+    for name, pts in list(_inputs(n, 21).items())[:4]:
+        for dt in (np.float32, np.float64):
+            x = np.ascontiguousarray(pts, dtype=dt)
+            f = tmp_path / f"{len(files)}.npy"
+            np.save(f, x)
+            files.append(str(f))
+            (r,) = _lib.pairs_host(x, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, n])
+            got.append((name, r.count, r.sum, _lib.last_profile().chunks_tc))
+    env = dict(os.environ, PAIRCOUNT_TCS_BITMAP="0")
+    res = subprocess.run([sys.executable, "-c", _FFMA_ONLY.format(root=str(ROOT)), *files], env=env,
+                         capture_output=True, text=True, timeout=600, check=True)
+    ref = json.loads(res.stdout.strip().splitlines()[-1])
+    for (name, c, s_, tc), (c0, s0, kern0, tc0) in zip(got, ref):
+        assert (c, s_, tc) == (c0, s0, tc0), (name, c, s_, tc, c0, s0, tc0)
+
+
 def test_tcsum_unaligned_ranges_stay_on_the_ffma_kernel():
     # a range starting off a 32-point block boundary: its tiles' boxes differ from the per-32 boxes,
     # so the whole range stays on the FFMA kernel; aligned ranges split as usual
