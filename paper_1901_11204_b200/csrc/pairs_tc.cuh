@@ -33,7 +33,12 @@
 // tcgen05.mma per item into one of two 256-column accumulators); warps 2..9
 // drain the accumulators (warp w reads TMEM lanes 32*(w%4).., columns
 // 128*((w-2)/4)..).
-constexpr int kTcM = 128, kTcN = 256, kTcStages = 7, kTcWarps = 10;
+#ifndef PC_TC_DRAIN
+#define PC_TC_DRAIN 8  // drain warps: 8 (a 32 x 128 slice each) or 16 (32 x 64)
+#endif
+constexpr int kTcM = 128, kTcN = 256, kTcStages = 7;
+constexpr int kTcDrain = PC_TC_DRAIN, kTcDrainCols = kTcN * 4 / kTcDrain, kTcDrainBlk = kTcDrainCols / 32;
+constexpr int kTcWarps = 2 + kTcDrain;
 constexpr int kTcABytes = kTcM * 64, kTcBBytes = kTcN * 64;
 constexpr int kTcSmem = 2 * kTcABytes + kTcStages * kTcBBytes + 1024;  // > half the SM: one CTA per SM
 // PC_TILE_AUTO's range for it: below, the FFMA kernel's small-tile config wins; from
@@ -192,7 +197,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) pairs_tc_kernel(const TcArgs
             mbar_init(a_full + 8 * k, 1);
             mbar_init(a_empty + 8 * k, 1);
             mbar_init(acc_full + 8 * k, 2);  // the MMA thread's item hand-off + the MMAs' commit
-            mbar_init(acc_empty + 8 * k, 8);
+            mbar_init(acc_empty + 8 * k, kTcDrain);
         }
         mbar_init_fence();
         s_ncand = 0;
@@ -300,7 +305,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) pairs_tc_kernel(const TcArgs
         }
     } else {
         // ---------------- epilogue: 8 warps, lane quadrant warp%4, column half (warp-2)/4
-        const int quad = warp & 3, half = (warp - 2) >> 2;
+        const int quad = warp & 3, half = (warp - 2) >> 2;  // half: this warp's column slice
         const double M = dec_f64_or0(a.st->mnorm);
         const bool force = !(M < 1e30);
         const float half_tb = (float)(0.5 * ((double)a.thr + 1.52587890625e-05 * (M + 4.0)));  // b = 2^-16 (M + 4)
@@ -329,41 +334,39 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1) pairs_tc_kernel(const TcArgs
                     lim = 0;
                 }
             }
-            const unsigned taddr = tmem + ((unsigned)(quad * 32) << 16) + (unsigned)(acc * kTcN + half * 128);
+            const unsigned taddr = tmem + ((unsigned)(quad * 32) << 16) + (unsigned)(acc * kTcN + half * kTcDrainCols);
             // the whole 32 x 128 slice into registers, then the accumulator goes straight back to
             // the MMA warp: the reduction and any candidate handling overlap the next MMAs
-            unsigned v0[32], v1[32], v2[32], v3[32];
-            PC_TC_LD32(v0, taddr);
-            PC_TC_LD32(v1, taddr + 32u);
-            PC_TC_LD32(v2, taddr + 64u);
-            PC_TC_LD32(v3, taddr + 96u);
+            unsigned v[kTcDrainBlk][32];
+#pragma unroll
+            for (int q = 0; q < kTcDrainBlk; ++q) PC_TC_LD32(v[q], taddr + 32u * q);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive_plain(acc_empty + 8 * acc);
-            float bm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            float bm[kTcDrainBlk], bmax = -INFINITY;
 #pragma unroll
-            for (int e = 0; e < 32; e += 2) {
-                bm[0] = max3f(bm[0], __uint_as_float(v0[e]), __uint_as_float(v0[e + 1]));
-                bm[1] = max3f(bm[1], __uint_as_float(v1[e]), __uint_as_float(v1[e + 1]));
-                bm[2] = max3f(bm[2], __uint_as_float(v2[e]), __uint_as_float(v2[e + 1]));
-                bm[3] = max3f(bm[3], __uint_as_float(v3[e]), __uint_as_float(v3[e + 1]));
+            for (int q = 0; q < kTcDrainBlk; ++q) {
+                bm[q] = -INFINITY;
+#pragma unroll
+                for (int e = 0; e < 32; e += 2) bm[q] = max3f(bm[q], __uint_as_float(v[q][e]), __uint_as_float(v[q][e + 1]));
+                bmax = fmaxf(bmax, bm[q]);
             }
             // s of this lane's first column; rows own 1 <= s - rl <= lim
-            const long long s0 = c * kTcN + half * 128;
-            const bool any_owned = valid && s0 + 127 - rl >= 1 && s0 - rl <= lim;
-            const bool flag = any_owned && (force || max3f(bm[0], bm[1], fmaxf(bm[2], bm[3])) > rc);
+            const long long s0 = c * kTcN + half * kTcDrainCols;
+            const bool any_owned = valid && s0 + (kTcDrainCols - 1) - rl >= 1 && s0 - rl <= lim;
+            const bool flag = any_owned && (force || bmax > rc);
             if (flag) {
                 // queue this row's owned candidates for the exact pass
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < kTcDrainBlk; ++q) {
                     if (!(force || bm[q] > rc)) continue;
-                    const unsigned* v = q == 0 ? v0 : q == 1 ? v1 : q == 2 ? v2 : v3;
+                    const unsigned* vq = v[q];
                     unsigned m = 0xffffffffu;
                     if (!force) {
                         m = 0;
 #pragma unroll
-                        for (int e = 0; e < 32; ++e) m |= (__uint_as_float(v[e]) > rc ? 1u : 0u) << e;
+                        for (int e = 0; e < 32; ++e) m |= (__uint_as_float(vq[e]) > rc ? 1u : 0u) << e;
                     }
                     while (m) {
                         const int e = __ffs(m) - 1;
