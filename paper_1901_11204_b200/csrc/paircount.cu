@@ -752,7 +752,7 @@ __global__ void blk_box_kernel(const T* __restrict__ xyz, long long n, int nblk,
 }
 
 struct WsLayout {
-    size_t pts, stats, prof, red, slots, claims, claims_tc, tc_bits, tc_bits_cap, tc_a, tc_b, tc_cand, tc_cnt, srt, srt_temp, total;
+    size_t pts, stats, prof, red, slots, claims, claims_tc, tc_bits, tc_bits_cap, tc_cbox, tc_a, tc_b, tc_cand, tc_cnt, srt, srt_temp, total;
 };
 WsLayout ws_layout(long long n) {
     WsLayout l;
@@ -766,7 +766,8 @@ WsLayout ws_layout(long long n) {
     l.claims_tc = align_up(l.claims + (size_t)kClaimsCap * sizeof(double), 256);
     l.tc_bits = align_up(l.claims_tc + (size_t)kClaimsCap * sizeof(double), 256);
     l.tc_bits_cap = tcs_bits_bytes(n < 0 ? 0 : n);  // the whole-range bitmap, up to kTcsBitsMax
-    l.tc_a = align_up(l.tc_bits + l.tc_bits_cap, 1024);
+    l.tc_cbox = align_up(l.tc_bits + l.tc_bits_cap, 256);  // per-256 chunk boxes, 32 B each
+    l.tc_a = align_up(l.tc_cbox + (size_t)((n < 0 ? 0 : n) / 256 + 1) * 32, 1024);
     const TcGeom g = tc_geom(n < 0 ? 0 : n);  // tensor-core count kernel operands (64 B per staged point)
     l.tc_b = align_up(l.tc_a + (size_t)g.n_rows * 64, 1024);
     l.tc_cand = align_up(l.tc_b + (size_t)g.n_ext * 64, 256);
@@ -954,7 +955,7 @@ bool tcs_enabled() {
 // The chunk bitmap of one range's tiles into `bits` (capacity cap_bytes); *cpw_pad stays 0 when it does
 // not fit (the kernels then classify in-loop).
 int classify_tcs(const PairsArgs& p, TileSel ts, unsigned* bits, size_t cap_bytes, long long* cpw_pad,
-                 cudaStream_t s) {
+                 cudaStream_t s, float4* cbox_area = nullptr) {
     TcsArgs a{};
     a.blk_box = p.blk_box;
     a.n = p.n;
@@ -969,6 +970,12 @@ int classify_tcs(const PairsArgs& p, TileSel ts, unsigned* bits, size_t cap_byte
     a.bits = bits;
     *cpw_pad = 0;
     if (a.n_tiles == 0 || !bits || (size_t)a.n_tiles * (size_t)a.cpw_pad / 8 > cap_bytes) return PC_OK;
+    if (cbox_area && p.n % 256 == 0 && p.lo % 256 == 0) {  // every chunk starts at 256 m + 1
+        const int nchunk = p.n / 256;
+        tcs_chunk_box_kernel<<<(nchunk + 255) / 256, 256, 0, s>>>(p.blk_box, p.n / 32, nchunk, cbox_area);
+        CK_LAUNCH("tcs_chunk_box_kernel");
+        a.cbox = cbox_area;
+    }
     tcs_classify_kernel<<<(int)(((long long)a.n_tiles * (a.cpw_pad / 32) + 7) / 8), 256, 0, s>>>(a);
     CK_LAUNCH("tcs_classify_kernel");
     *cpw_pad = a.cpw_pad;
@@ -1371,8 +1378,9 @@ int run_pairs(const void* xyz, int dtype, long long n, int interaction, int sche
             if (use_tcs) {  // the chunk bitmap both kernels follow (when it fits the workspace)
                 long long cpw_pad = 0;
                 unsigned* bits = (unsigned*)(ws + lay.tc_bits);
-                rc = lay.tc_bits_cap && tcs_bitmap_enabled() ? classify_tcs(args, ts, bits, lay.tc_bits_cap, &cpw_pad, s)
-                                                              : PC_OK;
+                rc = lay.tc_bits_cap && tcs_bitmap_enabled()
+                         ? classify_tcs(args, ts, bits, lay.tc_bits_cap, &cpw_pad, s, (float4*)(ws + lay.tc_cbox))
+                         : PC_OK;
                 if (rc) return rc;
                 if (cpw_pad) {
                     args.tc_bits = bits;

@@ -202,7 +202,27 @@ struct TcsArgs {
     long long nclaims;
     unsigned* bits;    // chunk bitmap (tcs_classify_kernel writes it, the kernels read it), or null
     long long cpw_pad;
+    const float4* cbox;  // classify: the box of the chunk starting at 256 m + 1 (n, lo multiples of 256), or null
 };
+
+// Per-chunk boxes when every chunk starts at 256 m + 1 (n and lo multiples of 256): chunk m covers the
+// per-32 blocks 8m .. 8m+8 (mod n / 32), the blocks the FFMA kernel unions for it.
+__global__ void __launch_bounds__(256) tcs_chunk_box_kernel(const float4* __restrict__ box, int nblk, int nchunk,
+                                                            float4* __restrict__ cbox) {
+    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < nchunk; m += gridDim.x * blockDim.x) {
+        float4 lo = make_float4(INFINITY, INFINITY, INFINITY, 0.f), hi = make_float4(-INFINITY, -INFINITY, -INFINITY, 0.f);
+#pragma unroll
+        for (int q = 0; q <= kTcsW / 32; ++q) {
+            int b = 8 * m + q;
+            if (b >= nblk) b -= nblk;
+            const float4 l = box[2 * b], h = box[2 * b + 1];
+            lo = make_float4(fminf(lo.x, l.x), fminf(lo.y, l.y), fminf(lo.z, l.z), 0.f);
+            hi = make_float4(fmaxf(hi.x, h.x), fmaxf(hi.y, h.y), fmaxf(hi.z, h.z), 0.f);
+        }
+        cbox[2 * m] = lo;
+        cbox[2 * m + 1] = hi;
+    }
+}
 
 // The chunk bitmap: one warp per 32-chunk word of a row tile, a lane per chunk (the tile's box from its
 // eight per-32 boxes, each chunk's from its nine -- the unions the FFMA kernel forms, min / max exact).
@@ -240,6 +260,12 @@ __global__ void __launch_bounds__(256) tcs_classify_kernel(const TcsArgs a) {
             const int nb1 = (min(jend, n - 1) >> 5) - (jw >> 5) + 1;
             const int nb2 = jend >= n ? ((jend - n) >> 5) + 1 : 0;
             float cl[3] = {INFINITY, INFINITY, INFINITY}, ch[3] = {-INFINITY, -INFINITY, -INFINITY};
+            if (a.cbox) {  // the same union, precomputed (aligned chunk starts)
+                PC_CHECK(((jw - 1) & 255) == 0);
+                const float4 lo4 = __ldg(a.cbox + 2 * ((jw - 1) >> 8)), hi4 = __ldg(a.cbox + 2 * ((jw - 1) >> 8) + 1);
+                cl[0] = lo4.x; cl[1] = lo4.y; cl[2] = lo4.z;
+                ch[0] = hi4.x; ch[1] = hi4.y; ch[2] = hi4.z;
+            } else
 #pragma unroll
             for (int q = 0; q < kTcsW / 32 + 2; ++q) {  // <= 9 blocks, 10 when the window wraps
                 if (q < nb1 + nb2) {
