@@ -139,9 +139,9 @@ def test_tcsum_in_loop_classification_matches_the_bitmap(tmp_path):
     # PAIRCOUNT_TCS_BITMAP=0 forces that path here: the same chunks, the same total, bit for bit
     if not TCS:
         pytest.skip("PAIRCOUNT_TCSUM=0")
-    n = 2**17 + 5
     files, got = [], []
-    for name, pts in list(_inputs(n, 21).items())[:4]:
+    # n = 2^17 + 5: the general chunk boxes; n = 2^17: the precomputed per-256 ones (tcs_chunk_box_kernel)
+    for n, name, pts in [(m, nm, p) for m in (2**17 + 5, 2**17) for nm, p in list(_inputs(m, 21).items())[:4]]:
         for dt in (np.float32, np.float64):
             x = np.ascontiguousarray(pts, dtype=dt)
             f = tmp_path / f"{len(files)}.npy"
