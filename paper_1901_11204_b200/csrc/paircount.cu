@@ -458,6 +458,7 @@ __device__ __forceinline__ int steps_for_dev(int n, int i) {
 #include "pairs_kernel.cuh"
 #include "pairs_tc.cuh"
 #include "pairs_tcsum.cuh"
+#include "pairs_tcs2.cuh"
 #include "pairs_key.cuh"
 #include "pairs_row.cuh"
 
@@ -945,6 +946,15 @@ bool tcs_bitmap_enabled() {
     }();
     return on;
 }
+// PAIRCOUNT_TCS2=1: the SM-pair kernel (pairs_tcs2.cuh) for fp32 points -- correct, but measured
+// 110.6 ms against 66.2 for pairs_tcs_kernel at 2^20, so off by default
+bool tcs2_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("PAIRCOUNT_TCS2");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
 bool tcs_enabled() {
     static const bool on = [] {
         const char* e = getenv("PAIRCOUNT_TCSUM");
@@ -1006,9 +1016,12 @@ int launch_tcs(const PairsArgs& p, TileSel ts, double* claims_tc, Slot* slots, l
     // items per claim: a power of two keeping the float64 partials (kTcsParts per claim) within
     // kClaimsCap, and as large as ~128 claims per CTA allows (up to 128 items): a claim's items are
     // consecutive chunks of one tile, so small claims rebuild the row operand often (tile parts)
-    const int grid = num_sms();
+    // fp32 points with the bitmap and PAIRCOUNT_TCS2=1: the SM-pair kernel (pairs_tcs2.cuh)
+    const bool pair = tcs2_enabled() && p.dtype == PC_F32 && bits != nullptr && num_sms() >= 2;
+    const long long parts = pair ? kTc2Parts : kTcsParts;
+    const int grid = pair ? num_sms() & ~1 : num_sms();
     long long S = 1;
-    while (S * (kClaimsCap / kTcsParts) < a.items) S *= 2;
+    while (S * (kClaimsCap / parts) < a.items) S *= 2;
     while (S < 128 && S * 2 * (long long)grid * 128 <= a.items) S *= 2;
     a.S = S;
     a.nclaims = (a.items + S - 1) / S;
@@ -1022,10 +1035,11 @@ int launch_tcs(const PairsArgs& p, TileSel ts, double* claims_tc, Slot* slots, l
     if (!attr_set[dev & 63]) {
         CK(cudaFuncSetAttribute(pairs_tcs_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcsSmem));
         CK(cudaFuncSetAttribute(pairs_tcs_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcsSmem));
+        CK(cudaFuncSetAttribute(pairs_tcs2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTc2Smem));
         attr_set[dev & 63] = true;
     }
     CK(cudaMemsetAsync(a.work_ctr, 0, sizeof(unsigned long long), s));
-    CK(cudaMemsetAsync(claims_tc, 0, (size_t)a.nclaims * kTcsParts * sizeof(double), s));
+    CK(cudaMemsetAsync(claims_tc, 0, (size_t)a.nclaims * parts * sizeof(double), s));
     EvPair* ev = nullptr;
     if (g_timing && g_ev_used < 4096) {
         if (g_ev_used == g_ev_made) {
@@ -1037,12 +1051,13 @@ int launch_tcs(const PairsArgs& p, TileSel ts, double* claims_tc, Slot* slots, l
         ev->kind = 1;
         CK(cudaEventRecord(ev->a, s));
     }
-    if (p.dtype == PC_F64) pairs_tcs_kernel<double><<<grid, kTcsWarps * 32, kTcsSmem, s>>>(a);
+    if (pair) pairs_tcs2_kernel<<<grid, kTc2Warps * 32, kTc2Smem, s>>>(a);
+    else if (p.dtype == PC_F64) pairs_tcs_kernel<double><<<grid, kTcsWarps * 32, kTcsSmem, s>>>(a);
     else pairs_tcs_kernel<float><<<grid, kTcsWarps * 32, kTcsSmem, s>>>(a);
     CK_LAUNCH("pairs_tcs_kernel");
     if (ev) CK(cudaEventRecord(ev->b, s));
     *nslots = grid;
-    *nparts = (int)(a.nclaims * kTcsParts);
+    *nparts = (int)(a.nclaims * parts);
     return PC_OK;
 }
 
