@@ -26,7 +26,15 @@
 // acc_full to both CTAs (multicast); the drain warps walk the same item sequence
 // themselves, so no per-item message crosses the pair.
 
-constexpr int kTc2Prod = 2, kTc2Epi = 8, kTc2Warps = 1 + kTc2Prod + kTc2Epi;  // 11 warps: 12 slots of 168 registers
+#ifndef PC_TC2_PROD
+#define PC_TC2_PROD 2  // producer warps per CTA (2: 11 warps, 168 registers; 4: 13 warps, 128 registers)
+#endif
+constexpr int kTc2Prod = PC_TC2_PROD, kTc2Epi = 8, kTc2Warps = 1 + kTc2Prod + kTc2Epi;
+constexpr int kTc2PT = kTc2Prod * 32, kTc2PR = 128 / kTc2PT;  // producer threads, points per thread
+#ifndef PC_TC2_ROUND
+#define PC_TC2_ROUND 128  // drain columns per round (64 when the register budget is 128)
+#endif
+constexpr int kTc2Round = PC_TC2_ROUND;
 constexpr int kTc2Half = kTcsHalf;  // bytes of a 128-point operand half (8 KB)
 #ifndef PC_TC2_STAGES
 #define PC_TC2_STAGES 6
@@ -217,7 +225,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTc2Warps * 32, 1) p
         }
     } else if (warp <= kTc2Prod) {
         // ---------------- producers (both CTAs): this CTA's half of every operand
-        const int tid = (warp - 1) * 32 + lane;  // 64 threads: points tid, tid + 64 of the half
+        const int tid = (warp - 1) * 32 + lane;  // points tid, tid + kTc2PT, ... of the half
         long long it = 0;
         int sg = 0, abuf = 1;
         long long aloads[2] = {0, 0};
@@ -234,10 +242,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTc2Warps * 32, 1) p
             while (jw >= n) jw -= n;
             return jw;
         };
-        auto load2 = [&](int j0, float (&q)[6]) {
+        auto load2 = [&](int j0, float (&q)[3 * kTc2PR]) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                int j = j0 + tid + 64 * h;
+            for (int h = 0; h < kTc2PR; ++h) {
+                int j = j0 + tid + kTc2PT * h;
                 if (j >= n) j -= n;
                 PC_CHECK(j >= 0 && j < n);
                 const float* src = xyz + 3ll * j;
@@ -247,7 +255,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTc2Warps * 32, 1) p
             }
         };
         long long c = 0, u = 0, c2 = 0, u2 = 0;
-        float cur[6], nxt[6];
+        float cur[3 * kTc2PR], nxt[3 * kTc2PR];
         bool have = advance(c, u);
         if (have) load2(col0(u), cur);
         while (have) {
@@ -279,8 +287,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTc2Warps * 32, 1) p
                 if (aloads[abuf] > 0) mbar_wait(a_empty + 8 * abuf, (unsigned)((aloads[abuf] - 1) & 1));
                 unsigned char* dA = sA + abuf * kTc2Half;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int p = tid + 64 * h;
+                for (int h = 0; h < kTc2PR; ++h) {
+                    const int p = tid + kTc2PT * h;
                     const int i = i0 + 128 * (int)rank + p;
                     PC_CHECK(i >= a.lo && i < a.hi);
                     const float* q = xyz + 3ll * i;
@@ -301,8 +309,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTc2Warps * 32, 1) p
             if (it >= kTc2Stages) mbar_wait(b_empty + 8 * sg, (unsigned)(((it / kTc2Stages) - 1) & 1));
             unsigned char* dB = sB + sg * kTc2Half;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int p = tid + 64 * h;
+            for (int h = 0; h < kTc2PR; ++h) {
+                const int p = tid + kTc2PT * h;
                 tcs_write_col(dB, p, __fsub_rn(cur[3 * h], o[0]), __fsub_rn(cur[3 * h + 1], o[1]),
                               __fsub_rn(cur[3 * h + 2], o[2]));
             }
@@ -319,7 +327,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTc2Warps * 32, 1) p
             c = c2;
             u = u2;
 #pragma unroll
-            for (int k = 0; k < 6; ++k) cur[k] = nxt[k];
+            for (int k = 0; k < 3 * kTc2PR; ++k) cur[k] = nxt[k];
         }
         if (it >= kTc2Stages) mbar_wait(b_empty + 8 * sg, (unsigned)(((it / kTc2Stages) - 1) & 1));
         if (leader && tid == 0) s_item[sg] = -1;
@@ -349,19 +357,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTc2Warps * 32, 1) p
                 const int acc = (int)(it & 1);
                 mbar_wait(acc_full + 8 * acc, (unsigned)((it >> 1) & 1));
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                unsigned v[4][32];
                 const unsigned taddr = tmem + ((unsigned)(quad * 32) << 16) + (unsigned)(acc * 256 + chalf * 128);
-#pragma unroll
-                for (int w = 0; w < 4; ++w) PC_TC_LD32(v[w], taddr + 32u * w);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                __syncwarp();
-                // the loads have completed (wait::ld): a relaxed arrival suffices to free the accumulator
-                if (lane == 0) mbar_arrive_cluster_relaxed(L_accempty + 8 * acc);
-                ++it;
                 float2 facc = make_float2(0.f, 0.f), facc2 = make_float2(0.f, 0.f);
+#pragma unroll 1
+                for (int rd = 0; rd < 128 / kTc2Round; ++rd) {
+                unsigned v[kTc2Round / 32][32];
 #pragma unroll
-                for (int w = 0; w < 4; ++w) {
+                for (int w = 0; w < kTc2Round / 32; ++w) PC_TC_LD32(v[w], taddr + (unsigned)(kTc2Round * rd) + 32u * w);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (rd == 128 / kTc2Round - 1) {
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    // the loads have completed (wait::ld): a relaxed arrival suffices to free the accumulator
+                    if (lane == 0) mbar_arrive_cluster_relaxed(L_accempty + 8 * acc);
+                }
+#pragma unroll
+                for (int w = 0; w < kTc2Round / 32; ++w) {
 #pragma unroll
                     for (int e = 0; e < 32; e += 8) {
                         const float2 p1 = make_float2(__uint_as_float(v[w][e]), __uint_as_float(v[w][e + 1]));
@@ -376,6 +387,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTc2Warps * 32, 1) p
                         else facc = __ffma2_rn(Nn, make_float2(rcp_approx(P.x), rcp_approx(P.y)), facc);
                     }
                 }
+                }
+                ++it;
                 facc = __fadd2_rn(facc, facc2);
                 sum += (double)(facc.x + facc.y);
             }
