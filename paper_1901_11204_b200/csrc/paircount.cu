@@ -1010,14 +1010,18 @@ int launch_tcs(const PairsArgs& p, TileSel ts, double* claims_tc, Slot* slots, l
     a.n_tiles = tiles_of(p.lo, p.hi, kTcsT, ts);
     a.L = (long long)(kTcsT - 1) + (p.n >> 1);
     a.cpw = (a.L + kTcsW - 1) / kTcsW;
-    a.items = (long long)a.n_tiles * a.cpw;
     a.bits = bits;
     a.cpw_pad = cpw_pad;
-    // items per claim: a power of two keeping the float64 partials (kTcsParts per claim) within
-    // kClaimsCap, and as large as ~128 claims per CTA allows (up to 128 items): a claim's items are
-    // consecutive chunks of one tile, so small claims rebuild the row operand often (tile parts)
     // fp32 points with the bitmap and PAIRCOUNT_TCS2=1: the SM-pair kernel (pairs_tcs2.cuh)
     const bool pair = tcs2_enabled() && p.dtype == PC_F32 && bits != nullptr && num_sms() >= 2;
+    // work units: the diagonals of groups of G consecutive tiles (one column operand for up to G
+    // items) when the call's tiles are whole origin groups; else one item per unit
+    a.G = !pair && ts.tstride == 1 && ts.toff % kTcsOrgG == 0 ? kTcsOrgG : 1;
+    a.upg = a.cpw + a.G - 1;
+    a.items = (long long)((a.n_tiles + a.G - 1) / a.G) * a.upg;
+    // units per claim: a power of two keeping the float64 partials (kTcsParts per claim) within
+    // kClaimsCap, and as large as ~128 claims per CTA allows (up to 128 units): a claim's units are
+    // consecutive diagonals of one group, so small claims rebuild the row operands often (tile parts)
     const long long parts = pair ? kTc2Parts : kTcsParts;
     const int grid = pair ? num_sms() & ~1 : num_sms();
     long long S = 1;

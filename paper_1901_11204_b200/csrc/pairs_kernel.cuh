@@ -78,6 +78,51 @@ __device__ __forceinline__ ChunkGeom chunk_geom(const float tmin[3], const float
     g.ab = __fadd_rn(__fsqrt_rn(rt2), __fsqrt_rn(bm2));
     return g;
 }
+// The tensor-core sum (pairs_tcsum.cuh) centres a and b on the box of an origin GROUP of kTcsOrgG
+// consecutive 256-row tiles (absolute tile index / kTcsOrgG), so one column operand serves the items
+// (t + k, c - k) of the group's tiles along its diagonal.  Its chunk test: the tile's box (for |a|)
+// and the chunk's box (for |b|, the gap) about the group's centre o.
+#ifndef PC_TCS_G
+#define PC_TCS_G 3  // (2 / 3 / 4 tiles: 70.3 / 69.0 / 70.9 ms at 2^20, each at its best ring depth)
+#endif
+constexpr int kTcsOrgG = PC_TCS_G;
+static_assert(kTcsOrgG >= 1 && kTcsOrgG <= 4, "an origin group's per-32 boxes: one per lane");
+// the origin group's box: the union of the per-32 boxes of its full tiles (rows lo + 256 t ..
+// + 255 < hi), lo a multiple of 32; warp-collective, min / max exact (every caller gets the same box)
+__device__ __forceinline__ void tcs_group_box(const float4* __restrict__ blk_box, int lo, int hi, int tabs, int lane,
+                                              float gmin[3], float gmax[3]) {
+    const int tq = tabs / kTcsOrgG * kTcsOrgG + (lane >> 3);
+    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    if ((lane >> 3) < kTcsOrgG && (long long)lo + 256ll * (tq + 1) <= hi) {
+        const int b = (lo >> 5) + 8 * tq + (lane & 7);
+        const float4 lo4 = __ldg(blk_box + 2 * b), hi4 = __ldg(blk_box + 2 * b + 1);
+        mn[0] = lo4.x; mn[1] = lo4.y; mn[2] = lo4.z;
+        mx[0] = hi4.x; mx[1] = hi4.y; mx[2] = hi4.z;
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        gmin[k] = warp_min_f(mn[k]);
+        gmax[k] = warp_max_f(mx[k]);
+    }
+}
+__device__ __forceinline__ ChunkGeom chunk_geom_g(const float tmin[3], const float tmax[3], const float gmin[3],
+                                                  const float gmax[3], const float cl[3], const float ch[3]) {
+    ChunkGeom g;
+    float gap2 = 0.f, ra2 = 0.f, bm2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        g.o[k] = __fmul_rn(0.5f, __fadd_rn(gmin[k], gmax[k]));
+        const float d = fmaxf(0.f, fmaxf(__fsub_rn(cl[k], tmax[k]), __fsub_rn(tmin[k], ch[k])));
+        gap2 = __fadd_rn(gap2, __fmul_rn(d, d));
+        const float aa = fmaxf(fabsf(__fsub_rn(tmin[k], g.o[k])), fabsf(__fsub_rn(tmax[k], g.o[k])));
+        ra2 = __fadd_rn(ra2, __fmul_rn(aa, aa));
+        const float bb = fmaxf(fabsf(__fsub_rn(cl[k], g.o[k])), fabsf(__fsub_rn(ch[k], g.o[k])));
+        bm2 = __fadd_rn(bm2, __fmul_rn(bb, bb));
+    }
+    g.gap2 = gap2;
+    g.ab = __fadd_rn(__fsqrt_rn(ra2), __fsqrt_rn(bm2));
+    return g;
+}
 // a dense chunk the tensor-core sum kernel takes (pairs_tcsum.cuh): the Gram test below, 8u (|a|+|b|)^2
 // <= 5e-6 (1 + dmin^2) written as 5u (..)^2 <= 3.125e-6 (..), dmin^2 > 4.5, and |a|+|b| <= 3e4 (the
 // epilogue's four-term products stay finite)
@@ -646,7 +691,13 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 for (int k = 0; k < 3; ++k) o[k] = cg.o[k];
                 const float gap2 = cg.gap2, ab = cg.ab;
                 // a chunk the tensor-core kernel evaluates (pairs_tcsum.cuh): nothing to do here
-                tc_skip = a.tc_split && !a.tc_bits && tcs_takes(cg);  // (with the bitmap: skipped above)
+                // (with the bitmap: skipped above; in-loop, the same test about the origin group's centre)
+                if (a.tc_split && !a.tc_bits) {
+                    PC_CHECK(T == 256 && W == 256);
+                    float gmn[3], gmx[3];
+                    tcs_group_box(a.blk_box, a.lo, a.hi, tile * a.tstride + a.toff, lane, gmn, gmx);
+                    tc_skip = tcs_takes(chunk_geom_g(tmin, tmax, gmn, gmx, cl, ch));
+                }
 #ifdef PC_DBG_SKIPALL  // debug (timing only): every dense chunk skipped -- the walk's own cost
                 tc_skip = true;
 #endif

@@ -263,23 +263,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTc2Warps * 32, 1) p
             if (have2) load2(col0(u2), nxt);
             const long long t = u / C;
             const int tt = (int)t, i0 = row0t(tt);
-            if (tt != o_tile) {  // the tile's centre: its box from its eight per-32 boxes
+            if (tt != o_tile) {  // the origin: the centre of the tile's origin group's box (chunk_geom_g's o)
                 o_tile = tt;
-                float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-                if (lane < kTcsT / 32) {
-                    const float4 lo4 = a.blk_box[2 * ((i0 >> 5) + lane)], hi4 = a.blk_box[2 * ((i0 >> 5) + lane) + 1];
-                    mn[0] = lo4.x; mn[1] = lo4.y; mn[2] = lo4.z;
-                    mx[0] = hi4.x; mx[1] = hi4.y; mx[2] = hi4.z;
-                }
-                float tmin[3], tmax[3];
+                float gmn[3], gmx[3];
+                tcs_group_box(a.blk_box, a.lo, a.hi, tt * a.tstride + a.toff, lane, gmn, gmx);
 #pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    tmin[k] = warp_min_f(mn[k]);
-                    tmax[k] = warp_max_f(mx[k]);
-                }
-                const ChunkGeom g = chunk_geom(tmin, tmax, tmin, tmax);
-#pragma unroll
-                for (int k = 0; k < 3; ++k) o[k] = g.o[k];
+                for (int k = 0; k < 3; ++k) o[k] = __fmul_rn(0.5f, __fadd_rn(gmn[k], gmx[k]));
             }
             long long flag = 0;
             if (tt != a_tile) {  // this CTA's 128 rows of the new tile

@@ -56,31 +56,25 @@ constexpr int kTcsNQ = PC_TCS_NQ, kTcsNP = 256 / kTcsNQ, kTcsNAcc = 2 * kTcsNQ;
 constexpr int kTcsRound = PC_TCS_ROUND;
 static_assert(kTcsNAcc * kTcsNP == 512 && kTcsNP % kTcsRound == 0 && kTcsRound % 32 == 0, "TMEM: 512 columns");
 #ifndef PC_TCS_STAGES
-#define PC_TCS_STAGES 5
+#define PC_TCS_STAGES 4  // column stages: with G = 3 the dynamic shared memory (161 KB) fits the 164 KB carveout
 #endif
 constexpr int kTcsStages = PC_TCS_STAGES;
 #ifndef PC_TCS_KSTEPS  // K = 16 steps per accumulator; a debug knob for A/B of the MMA cost
 #define PC_TCS_KSTEPS 2
 #endif
 #ifndef PC_TCS_PROD
-#define PC_TCS_PROD 3  // producer warps: 12 warps in all, 168 registers each (13 warps take 16 slots of 128: spills)
+#define PC_TCS_PROD 2  // producer warps: 11 warps in all (12 slots), 168 registers each; a column operand serves
+                       // up to G items, so two warps keep the MMA fed (3: +0.5 ms, 1: +2.6 ms; 13 warps take 16 slots: spills)
 #endif
 #ifndef PC_TCS_EPI
 #define PC_TCS_EPI 8  // epilogue warps: 4 per accumulator (each all its columns) or 8 (half the columns each)
 #endif
-#ifndef PC_TCS_MMA
-#define PC_TCS_MMA 1  // MMA-issuing warps: one for both row halves, or one per row half
-#endif
-#ifndef PC_TCS_OOO
-#define PC_TCS_OOO 0  // one MMA thread, the two row halves advanced independently
-#endif
-constexpr int kTcsMma = PC_TCS_MMA, kTcsProd = PC_TCS_PROD, kTcsEpi = PC_TCS_EPI,
-              kTcsWarps = kTcsMma + kTcsProd + kTcsEpi;
-static_assert(kTcsMma == 1 || PC_TCS_NQ == 1, "one MMA warp per row half: whole-row-half accumulators");
+constexpr int kTcsMma = 1, kTcsProd = PC_TCS_PROD, kTcsEpi = PC_TCS_EPI,
+              kTcsWarps = kTcsMma + kTcsProd + kTcsEpi;  // one MMA warp, producers, drain warps
 constexpr int kTcsEpiG = kTcsEpi / 2, kTcsSpan = kTcsNP * 4 / kTcsEpiG;  // warps per accumulator, columns per warp
 static_assert(kTcsNQ == 1 || kTcsEpi == 8, "column-split epilogue for whole-row-half accumulators only");
 constexpr int kTcsPT = kTcsProd * 32, kTcsPR = (256 + kTcsPT - 1) / kTcsPT;  // producer threads, points per thread
-constexpr int kTcsSmem = 2 * kTcsOp + kTcsStages * kTcsOp + 1024;
+constexpr int kTcsSmem = (2 * kTcsOrgG + kTcsStages) * kTcsOp + 1024;  // rows [2][G], columns [stages]
 constexpr long long kTcsParts = kTcsEpi;           // float64 partials per claim
 // instruction descriptor (kind::f16): D f32, A/B bf16, both K-major, N = kTcsNP, M = 128
 constexpr uint32_t kTcsIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kTcsNP >> 3) << 17) |
@@ -197,13 +191,47 @@ struct TcsArgs {
     int tstride, toff, n_tiles;
     long long L;       // window length (T - 1 + n/2)
     long long cpw;     // chunks per window
-    long long items;   // n_tiles * cpw
-    long long S;       // items per claim
+    int G;             // tiles per work unit: kTcsOrgG (tstride 1, toff a multiple of it), else 1
+    long long upg;     // units per group of G tiles: cpw + G - 1 diagonals
+    long long items;   // work units: ceil(n_tiles / G) * upg (pairs_tcs2_kernel: G = 1, n_tiles * cpw)
+    long long S;       // units per claim
     long long nclaims;
     unsigned* bits;    // chunk bitmap (tcs_classify_kernel writes it, the kernels read it), or null
     long long cpw_pad;
     const float4* cbox;  // classify: the box of the chunk starting at 256 m + 1 (n, lo multiples of 256), or null
 };
+
+// In-loop classification of item (call tile i, chunk c) by one thread (no bitmap: n > ~2^23): the same
+// boxes tcs_classify_kernel unions across its lanes, so the same decision.
+__device__ __noinline__ bool tcs_item_takes(const float4* __restrict__ blk_box, int n, int lo, int hi, int tabs,
+                                            long long L, long long c) {
+    const int steps_min = (n & 1) ? (n - 1) >> 1 : (n >> 1) - 1;
+    const int i0 = lo + tabs * kTcsT;
+    const long long off = c * kTcsW;
+    if (!(off + kTcsW <= L && i0 + kTcsT <= hi && off + 1 >= kTcsT && off + kTcsW <= steps_min)) return false;
+    auto add = [&](int b, float (&mn)[3], float (&mx)[3]) {
+        const float4 lo4 = __ldg(blk_box + 2 * b), hi4 = __ldg(blk_box + 2 * b + 1);
+        mn[0] = fminf(mn[0], lo4.x); mn[1] = fminf(mn[1], lo4.y); mn[2] = fminf(mn[2], lo4.z);
+        mx[0] = fmaxf(mx[0], hi4.x); mx[1] = fmaxf(mx[1], hi4.y); mx[2] = fmaxf(mx[2], hi4.z);
+    };
+    float tmin[3] = {INFINITY, INFINITY, INFINITY}, tmax[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int q = 0; q < kTcsT / 32; ++q) add((i0 >> 5) + q, tmin, tmax);
+    float gmin[3] = {INFINITY, INFINITY, INFINITY}, gmax[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int k = 0; k < kTcsOrgG; ++k) {  // tcs_group_box, one thread
+        const int tq = tabs / kTcsOrgG * kTcsOrgG + k;
+        if ((long long)lo + 256ll * (tq + 1) > hi) continue;
+        for (int q = 0; q < 8; ++q) add((lo >> 5) + 8 * tq + q, gmin, gmax);
+    }
+    // the chunk's box: one or two runs of per-32 boxes (the FFMA kernel's blocks)
+    int jw = i0 + (int)off + 1;
+    if (jw >= n) jw -= n;
+    const int jend = jw + kTcsW - 1;
+    const int nb1 = (min(jend, n - 1) >> 5) - (jw >> 5) + 1;
+    const int nb2 = jend >= n ? ((jend - n) >> 5) + 1 : 0;
+    float cl[3] = {INFINITY, INFINITY, INFINITY}, ch[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int q = 0; q < nb1 + nb2; ++q) add(q < nb1 ? (jw >> 5) + q : q - nb1, cl, ch);
+    return tcs_takes(chunk_geom_g(tmin, tmax, gmin, gmax, cl, ch));
+}
 
 // Per-chunk boxes when every chunk starts at 256 m + 1 (n and lo multiples of 256): chunk m covers the
 // per-32 blocks 8m .. 8m+8 (mod n / 32), the blocks the FFMA kernel unions for it.
@@ -249,6 +277,8 @@ __global__ void __launch_bounds__(256) tcs_classify_kernel(const TcsArgs a) {
             tmax[k] = warp_max_f(mx[k]);
         }
     }
+    float gmin[3] = {0.f, 0.f, 0.f}, gmax[3] = {0.f, 0.f, 0.f};  // the origin group's box
+    if (rows_ok) tcs_group_box(a.blk_box, a.lo, a.hi, (int)t * a.tstride + a.toff, lane, gmin, gmax);
     {
         const long long c = c0 + lane;
         const long long off = c * kTcsW;
@@ -275,7 +305,7 @@ __global__ void __launch_bounds__(256) tcs_classify_kernel(const TcsArgs a) {
                     ch[0] = fmaxf(ch[0], hi4.x); ch[1] = fmaxf(ch[1], hi4.y); ch[2] = fmaxf(ch[2], hi4.z);
                 }
             }
-            take = tcs_takes(chunk_geom(tmin, tmax, cl, ch));
+            take = tcs_takes(chunk_geom_g(tmin, tmax, gmin, gmax, cl, ch));
         }
         const unsigned w = __ballot_sync(0xffffffffu, take);
         PC_CHECK(t * a.cpw_pad + c0 + 32 <= (long long)a.n_tiles * a.cpw_pad);
@@ -291,12 +321,12 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
     constexpr bool kF64 = sizeof(T) == 8;
     extern __shared__ __align__(1024) unsigned char tcs_smem[];
     unsigned char* base = (unsigned char*)(((uintptr_t)tcs_smem + 1023) & ~(uintptr_t)1023);
-    unsigned char* sA = base;              // [2][kTcsOp]
-    unsigned char* sB = base + 2 * kTcsOp; // [kTcsStages][kTcsOp]
+    unsigned char* sA = base;                         // [2][kTcsOrgG][kTcsOp]: a group's row operands
+    unsigned char* sB = base + 2 * kTcsOrgG * kTcsOp; // [kTcsStages][kTcsOp]: column operands
     __shared__ __align__(8) unsigned long long bar_bfull[kTcsStages], bar_bempty[kTcsStages];
     __shared__ __align__(8) unsigned long long bar_afull[2], bar_aempty[2];
     __shared__ __align__(8) unsigned long long bar_accfull[kTcsNAcc], bar_accempty[kTcsNAcc];  // index h NQ + q
-    __shared__ long long s_item[kTcsStages];  // claim << 2 | abuf << 1 | new tile; -1 = done
+    __shared__ long long s_item[kTcsStages];  // claim << 8 | item mask << 2 | abuf << 1 | new group; -1 = done
     __shared__ long long s_meta[kTcsNAcc];    // MMA -> epilogue: the accumulator's claim (-1 = done)
     __shared__ long long s_pclaim[2];
     __shared__ unsigned s_tmem;
@@ -343,83 +373,13 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
     const int steps_min = (n & 1) ? (n - 1) >> 1 : (n >> 1) - 1;
     double sum = 0.0;
 
-#if PC_TCS_OOO
     if (warp == 0) {
-        // ---------------- MMA issuer, the two row halves decoupled: each half advances through the
-        // items as soon as its own accumulator is free, so one drain group never waits for the other
+        // ---------------- MMA issuer (one elected thread): per stage, the unit's items -- tile k of
+        // the group against the stage's column operand, for each bit k of the unit's item mask
         if (lane == 0) {
-            const uint64_t dA0 = tcs_desc((unsigned)__cvta_generic_to_shared(sA));
-            const uint64_t dB0 = tcs_desc((unsigned)__cvta_generic_to_shared(sB));
-            long long nit[2] = {0, 0};    // next item of each half
-            int cur_ab[2] = {-1, -1};     // A buffer each half last used
-            long long aw[2][2] = {{0, 0}, {0, 0}};  // a_full waits per half and buffer
-            int issued[kTcsStages];       // halves issued on each stage's current item
-            for (int k = 0; k < kTcsStages; ++k) issued[k] = 0;
-            bool done[2] = {false, false};
-            unsigned items = 0, idle = 0;
-            while (!(done[0] && done[1])) {
-                bool moved = false;
-#pragma unroll 1
-                for (int h = 0; h < 2; ++h) {
-                    if (done[h]) continue;
-                    const long long i = nit[h];
-                    const int sg = (int)(i % kTcsStages);
-                    if (!mbar_test_wait(b_full + 8 * sg, (unsigned)((i / kTcsStages) & 1))) continue;
-                    if (i >= 1 && !mbar_test_wait(acc_empty + 8 * h, (unsigned)((i - 1) & 1))) continue;
-                    const long long tag = s_item[sg];
-                    if (tag < 0) {  // the sentinel: this half's drain group stops
-                        s_meta[h] = -1;
-                        mbar_arrive_plain(acc_full + 8 * h);
-                        mbar_arrive_plain(acc_full + 8 * h);
-                        done[h] = true;
-                        moved = true;
-                        continue;
-                    }
-                    const int ab = (int)((tag >> 1) & 1);
-                    if (ab != cur_ab[h]) {  // this half's first item on a new row operand
-                        const int old = cur_ab[h];
-                        // (not a blocking wait: the other half may have to move off this buffer first)
-                        if (!mbar_test_wait(a_full + 8 * ab, (unsigned)(aw[h][ab] & 1))) continue;
-                        ++aw[h][ab];
-                        cur_ab[h] = ab;
-                        // the old buffer is free once neither half uses it (after the MMAs so far)
-                        if (old >= 0 && cur_ab[h ^ 1] != old) tc_commit(a_empty + 8 * old);
-                    }
-                    s_meta[h] = tag >> 2;
-                    mbar_arrive_plain(acc_full + 8 * h);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint64_t da = dA0 + (uint64_t)((ab * kTcsOp + h * kTcsHalf) >> 4),
-                                   db = dB0 + (uint64_t)((sg * kTcsOp) >> 4);
-#pragma unroll
-                    for (int ks = 0; ks < PC_TCS_KSTEPS; ++ks) {
-                        asm volatile(
-                            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                            " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (unsigned)(h * kTcsNP)),
-                            "l"(da + (uint64_t)(16 * ks)), "l"(db + (uint64_t)(16 * ks)), "r"(kTcsIdesc), "r"(ks));
-                    }
-                    tc_commit(acc_full + 8 * h);
-                    if (++issued[sg] == 2) {  // both halves of this stage's item issued
-                        issued[sg] = 0;
-                        tc_commit(b_empty + 8 * sg);
-                        ++items;
-                    }
-                    nit[h] = i + 1;
-                    moved = true;
-                }
-                if (!moved && ++idle == (1u << 30)) __trap();  // a lost arrival must fail loudly
-            }
-            s_items = items;
-        }
-    } else if (false) {
-#else
-    if (warp < kTcsMma) {
-#endif
-        // ---------------- MMA issuer(s): warp m issues row half m's MMAs when there are two
-        if (lane == 0) {
-            long long it = 0;
+            long long it = 0, fills = 0;  // stages consumed, items issued (each fills both accumulators)
             long long aloads[2] = {0, 0};
             int cur_abuf = -1, sg = 0;
-            unsigned items = 0;
             // (the operands stay inside the 256 KB window of the 14-bit address field: offsets add)
             const uint64_t dA0 = tcs_desc((unsigned)__cvta_generic_to_shared(sA));
             const uint64_t dB0 = tcs_desc((unsigned)__cvta_generic_to_shared(sB));
@@ -428,71 +388,88 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                 const long long tag = s_item[sg];
                 if (tag < 0) {
                     for (int k = 0; k < kTcsNAcc; ++k) {
-                        if (kTcsMma > 1 && k != warp) continue;
-                        if (it >= 1) mbar_wait(acc_empty + 8 * k, (unsigned)((it - 1) & 1));
+                        if (fills >= 1) mbar_wait(acc_empty + 8 * k, (unsigned)((fills - 1) & 1));
                         s_meta[k] = -1;
                         mbar_arrive_plain(acc_full + 8 * k);
                         mbar_arrive_plain(acc_full + 8 * k);
                     }
                     break;
                 }
-                ++items;
                 const int ab = (int)((tag >> 1) & 1);
-                if (tag & 1) {  // first item of a tile: its A landed; the previous A is free after the MMAs so far
+                if (tag & 1) {  // first unit of a group: its rows landed; the previous rows are free after the MMAs so far
                     if (cur_abuf >= 0) tc_commit(a_empty + 8 * cur_abuf);
                     mbar_wait(a_full + 8 * ab, (unsigned)(aloads[ab] & 1));
                     ++aloads[ab];
                     cur_abuf = ab;
                 }
-                // descriptors: the base descriptor plus the 16-byte-unit offset (start address field)
-                const uint64_t da0 = dA0 + (uint64_t)((ab * kTcsOp) >> 4), db0 = dB0 + (uint64_t)((sg * kTcsOp) >> 4);
+                const uint64_t db0 = dB0 + (uint64_t)((sg * kTcsOp) >> 4);
+                for (unsigned km = (unsigned)((tag >> 2) & 0xF); km; km &= km - 1) {
+                    const int g = __ffs(km) - 1;
+                    // descriptors: the base descriptor plus the 16-byte-unit offset (start address field)
+                    const uint64_t da0 = dA0 + (uint64_t)(((ab * kTcsOrgG + g) * kTcsOp) >> 4);
 #pragma unroll
-                for (int kk = 0; kk < kTcsNAcc; ++kk) {
-                    // accumulator k = (row half h, column piece q) = h NQ + q, in the order the two
-                    // epilogue groups release them: (0,0), (1,0), (0,1), (1,1), ...
-                    const int h = kk & 1, q = kk >> 1, k = h * kTcsNQ + q;
-                    if (kTcsMma > 1 && h != warp) continue;
-                    if (it >= 1) mbar_wait(acc_empty + 8 * k, (unsigned)((it - 1) & 1));
-                    s_meta[k] = tag >> 2;
-                    mbar_arrive_plain(acc_full + 8 * k);  // release: the epilogue reads s_meta after its wait
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint64_t da = da0 + (uint64_t)((h * kTcsHalf) >> 4),
-                                   db = db0 + (uint64_t)((q * (kTcsNP / 8) * kTcsGroup) >> 4);
+                    for (int kk = 0; kk < kTcsNAcc; ++kk) {
+                        // accumulator k = (row half h, column piece q) = h NQ + q, in the order the two
+                        // epilogue groups release them: (0,0), (1,0), (0,1), (1,1), ...
+                        const int h = kk & 1, q = kk >> 1, k = h * kTcsNQ + q;
+                        if (fills >= 1) mbar_wait(acc_empty + 8 * k, (unsigned)((fills - 1) & 1));
+                        s_meta[k] = tag >> 8;
+                        mbar_arrive_plain(acc_full + 8 * k);  // release: the epilogue reads s_meta after its wait
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        const uint64_t da = da0 + (uint64_t)((h * kTcsHalf) >> 4),
+                                       db = db0 + (uint64_t)((q * (kTcsNP / 8) * kTcsGroup) >> 4);
 #pragma unroll
-                    for (int ks = 0; ks < PC_TCS_KSTEPS; ++ks) {
-                        asm volatile(
-                            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                            " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (unsigned)(k * kTcsNP)),
-                            "l"(da + (uint64_t)(16 * ks)), "l"(db + (uint64_t)(16 * ks)), "r"(kTcsIdesc), "r"(ks));
+                        for (int ks = 0; ks < PC_TCS_KSTEPS; ++ks) {
+                            asm volatile(
+                                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                                " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem + (unsigned)(k * kTcsNP)),
+                                "l"(da + (uint64_t)(16 * ks)), "l"(db + (uint64_t)(16 * ks)), "r"(kTcsIdesc), "r"(ks));
+                        }
+                        tc_commit(acc_full + 8 * k);
                     }
-                    tc_commit(acc_full + 8 * k);
+                    ++fills;
                 }
                 tc_commit(b_empty + 8 * sg);
             }
-            if (warp == 0) s_items = items;
+            s_items = (unsigned)fills;
         }
-    } else if (warp < kTcsMma + kTcsProd) {
-        // ---------------- producers: claims, classification, operands
-        // Per claim: the items are classified 32 at a time (lane l takes item ub + l: its tile's
-        // and chunk's per-32 boxes -- the same union of boxes the FFMA kernel reduces across its
-        // lanes, min/max being exact -- then chunk_geom / tcs_takes), and the eligible ones are
-        // built in order with the next one's column coordinates already in flight.
-        const int pw = warp - kTcsMma, tid = pw * 32 + lane;
+    } else if (warp < 1 + kTcsProd) {
+        // ---------------- producers: claims, item masks, operands
+        // Work units: (call group gc, diagonal d) -> the items (tile gc G + k, chunk d - k), k < G, which
+        // all cover the columns from row0(gc G) + 256 d + 1.  Per claim the units are examined 32 at a
+        // time (lane l: unit ub + l, its items' bitmap bits or in-loop tests), and the units with items
+        // are built in order -- the group's G row operands on a group change, then ONE column operand
+        // for the unit's items -- with the next unit's column coordinates already in flight.
+        const int pw = warp - 1, tid = pw * 32 + lane;
         long long it = 0, nclaim = 0;
-        int sg = 0, abuf = 1;
+        int sg = 0, abuf = 1, o_grp = -1;
         long long aloads[2] = {0, 0};
-        int a_tile = -1, o_tile = -1;
+        long long a_grp = -1;
         float o[3] = {0.f, 0.f, 0.f};
-        const long long C = a.cpw;
-        auto item_tile = [&](long long u, long long& off) -> int {
-            const long long t = u / C;
-            off = (u - t * C) * kTcsW;
-            return (int)t;
-        };
+        const long long C = a.cpw, UPG = a.upg;
+        const int G = a.G;
         auto row0t = [&](int tt) -> int { return a.lo + (tt * a.tstride + a.toff) * kTcsT; };
-        auto first_col = [&](int tt, long long off) -> int {  // first column of the chunk, wrapped
-            const int j0 = row0t(tt) + (int)off + 1;
+        auto unit_col = [&](long long u, long long& gc) -> int {  // the unit's group and first column, wrapped
+            gc = u / UPG;
+            const int j0 = row0t((int)(gc * G)) + (int)(u - gc * UPG) * kTcsW + 1;
             return j0 >= n ? j0 - n : j0;
+        };
+        auto unit_mask = [&](long long u) -> unsigned {  // bit k: item (gc G + k, d - k) is a tensor-core chunk
+            const long long gc = u / UPG, d = u - gc * UPG;
+            unsigned km = 0;
+            for (int k = 0; k < G; ++k) {
+                const long long i = gc * G + k, ch = d - k;
+                if (i >= a.n_tiles || ch < 0 || ch >= C) continue;
+                bool take;
+                if (a.bits) {
+                    const long long b = i * a.cpw_pad + ch;
+                    take = (__ldg(a.bits + (b >> 5)) >> (b & 31)) & 1u;
+                } else {
+                    take = tcs_item_takes(a.blk_box, n, a.lo, a.hi, (int)i * a.tstride + a.toff, a.L, ch);
+                }
+                km |= (take ? 1u : 0u) << k;
+            }
+            return km;
         };
         const T* xyz = (const T*)a.xyz;
         double cc[3] = {0.0, 0.0, 0.0};  // float64 points: the bounding-box centre of the centred boxes
@@ -512,7 +489,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                 q[3 * h + 2] = __ldg(src + 2);
             }
         };
-        auto rel = [&](T q, int k) -> float {  // the coordinate relative to the tile centre o, one rounding
+        auto rel = [&](T q, int k) -> float {  // the coordinate relative to the group centre o, one rounding
             if constexpr (kF64) return (float)(((double)q - cc[k]) - (double)o[k]);
             else return __fsub_rn((float)q, o[k]);
         };
@@ -523,101 +500,55 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
             if (c >= a.nclaims) break;
             const long long u0 = c * a.S, u1 = min(u0 + a.S, a.items);
             for (long long ub = u0; ub < u1; ub += 32) {
-                // ---- classification, one item per lane
-                bool take = false;
-                if (a.bits) {
-                    const long long u = ub + lane;
-                    if (u < u1) {
-                        const long long t = u / C, b = t * a.cpw_pad + (u - t * C);
-                        take = (__ldg(a.bits + (b >> 5)) >> (b & 31)) & 1u;
-                    }
-                } else {
-                    const long long u = ub + lane;
-                    if (u < u1) {
-                        long long off;
-                        const int tt = item_tile(u, off);
-                        const int i0 = row0t(tt);
-                        if (off + kTcsW <= a.L && i0 + kTcsT <= a.hi && off + 1 >= kTcsT && off + kTcsW <= steps_min) {
-                            float tmin[3] = {INFINITY, INFINITY, INFINITY}, tmax[3] = {-INFINITY, -INFINITY, -INFINITY};
-                            for (int q = 0; q < kTcsT / 32; ++q) {
-                                const float4 lo4 = a.blk_box[2 * ((i0 >> 5) + q)], hi4 = a.blk_box[2 * ((i0 >> 5) + q) + 1];
-                                tmin[0] = fminf(tmin[0], lo4.x); tmin[1] = fminf(tmin[1], lo4.y); tmin[2] = fminf(tmin[2], lo4.z);
-                                tmax[0] = fmaxf(tmax[0], hi4.x); tmax[1] = fmaxf(tmax[1], hi4.y); tmax[2] = fmaxf(tmax[2], hi4.z);
-                            }
-                            // the chunk's box: one or two runs of per-32 boxes (the FFMA kernel's blocks)
-                            const int jw = first_col(tt, off);
-                            const int jend = jw + kTcsW - 1;
-                            const int nb1 = (min(jend, n - 1) >> 5) - (jw >> 5) + 1;
-                            const int nb2 = jend >= n ? ((jend - n) >> 5) + 1 : 0;
-                            float cl[3] = {INFINITY, INFINITY, INFINITY}, ch[3] = {-INFINITY, -INFINITY, -INFINITY};
-                            for (int q = 0; q < nb1 + nb2; ++q) {
-                                const int bq = q < nb1 ? (jw >> 5) + q : q - nb1;
-                                const float4 lo4 = a.blk_box[2 * bq], hi4 = a.blk_box[2 * bq + 1];
-                                cl[0] = fminf(cl[0], lo4.x); cl[1] = fminf(cl[1], lo4.y); cl[2] = fminf(cl[2], lo4.z);
-                                ch[0] = fmaxf(ch[0], hi4.x); ch[1] = fmaxf(ch[1], hi4.y); ch[2] = fmaxf(ch[2], hi4.z);
-                            }
-                            take = tcs_takes(chunk_geom(tmin, tmax, cl, ch));
-                        }
-                    }
-                }
-                unsigned mask = __ballot_sync(0xffffffffu, take);
+                const unsigned km = ub + lane < u1 ? unit_mask(ub + lane) : 0u;
+                unsigned mask = __ballot_sync(0xffffffffu, km != 0u);
                 if (!mask) continue;
-                // ---- the eligible items, in order, one ahead in flight
+                // ---- the units with items, in order, one ahead in flight
                 T cur[3 * kTcsPR], nxt[3 * kTcsPR];
                 int e = __ffs(mask) - 1;
                 mask &= mask - 1;
-                long long eoff;
-                int ett = item_tile(ub + e, eoff);
-                load_cols(first_col(ett, eoff), cur);
+                long long egc;
+                load_cols(unit_col(ub + e, egc), cur);
                 for (;;) {
                     const int e2 = mask ? __ffs(mask) - 1 : -1;
                     if (mask) mask &= mask - 1;
-                    long long noff = 0;
-                    int ntt = 0;
-                    if (e2 >= 0) {
-                        ntt = item_tile(ub + e2, noff);
-                        load_cols(first_col(ntt, noff), nxt);
-                    }
+                    long long ngc = 0;
+                    if (e2 >= 0) load_cols(unit_col(ub + e2, ngc), nxt);
+                    const unsigned ekm = __shfl_sync(0xffffffffu, km, e);
                     long long flag = 0;
-                    if (ett != o_tile) {  // the tile's centre (the FFMA kernel's o: its rows' box)
-                        o_tile = ett;
-                        const int i0 = row0t(ett);
-                        float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-                        if (lane < kTcsT / 32) {
-                            const float4 lo4 = a.blk_box[2 * ((i0 >> 5) + lane)], hi4 = a.blk_box[2 * ((i0 >> 5) + lane) + 1];
-                            mn[0] = lo4.x; mn[1] = lo4.y; mn[2] = lo4.z;
-                            mx[0] = hi4.x; mx[1] = hi4.y; mx[2] = hi4.z;
-                        }
-                        float tmin[3], tmax[3];
+                    if (egc != a_grp) {
+                        // the origin: the centre of the origin group's box (chunk_geom_g's o)
+                        const int tabs = (int)(egc * G) * a.tstride + a.toff;
+                        if (tabs / kTcsOrgG != o_grp) {
+                            o_grp = tabs / kTcsOrgG;
+                            float gmn[3], gmx[3];
+                            tcs_group_box(a.blk_box, a.lo, a.hi, tabs, lane, gmn, gmx);
 #pragma unroll
-                        for (int k = 0; k < 3; ++k) {
-                            tmin[k] = warp_min_f(mn[k]);
-                            tmax[k] = warp_max_f(mx[k]);
+                            for (int k = 0; k < 3; ++k) o[k] = __fmul_rn(0.5f, __fadd_rn(gmn[k], gmx[k]));
                         }
-                        const ChunkGeom g = chunk_geom(tmin, tmax, tmin, tmax);
-#pragma unroll
-                        for (int k = 0; k < 3; ++k) o[k] = g.o[k];
-                    }
-                    if (ett != a_tile) {
-                        // the row operand of the new tile: a = q - o, A = 1 + |a|^2, three-way splits
+                        // the row operands of the group's full tiles: a = q - o, A = 1 + |a|^2, three-way splits
                         abuf ^= 1;
                         if (aloads[abuf] > 0) mbar_wait(a_empty + 8 * abuf, (unsigned)((aloads[abuf] - 1) & 1));
-                        unsigned char* dA = sA + abuf * kTcsOp;
-                        const int i0 = row0t(ett);
+                        for (int k = 0; k < G; ++k) {
+                            const long long i = egc * G + k;
+                            const int i0 = row0t((int)i);
+                            if (i >= a.n_tiles || i0 + kTcsT > a.hi) continue;
+                            unsigned char* dA = sA + (abuf * kTcsOrgG + k) * kTcsOp;
 #pragma unroll
-                        for (int h = 0; h < kTcsPR; ++h) {
-                            const int p = tid + kTcsPT * h;
-                            if (p >= 256) break;
-                            PC_CHECK(i0 + p >= a.lo && i0 + p < a.hi);
-                            const T* q = xyz + 3ll * (i0 + p);
-                            const float ax = rel(q[0], 0), ay = rel(q[1], 1), az = rel(q[2], 2);
-                            tcs_write_row(dA, p, ax, ay, az);
+                            for (int h = 0; h < kTcsPR; ++h) {
+                                const int p = tid + kTcsPT * h;
+                                if (p >= 256) break;
+                                PC_CHECK(i0 + p >= a.lo && i0 + p < a.hi);
+                                const T* q = xyz + 3ll * (i0 + p);
+                                const float ax = rel(q[0], 0), ay = rel(q[1], 1), az = rel(q[2], 2);
+                                tcs_write_row(dA, p, ax, ay, az);
+                            }
                         }
                         fence_proxy_async_shared();
                         __syncwarp();
                         if (lane == 0) mbar_arrive_plain(a_full + 8 * abuf);
                         ++aloads[abuf];
-                        a_tile = ett;
+                        a_grp = egc;
                         flag = 1;
                     }
                     // the column operand: b = q - o (carrying -2), B = |b|^2
@@ -635,14 +566,13 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                     }
                     fence_proxy_async_shared();
                     __syncwarp();
-                    if (tid == 0) s_item[sg] = (c << 2) | ((long long)abuf << 1) | flag;
+                    if (tid == 0) s_item[sg] = (c << 8) | ((long long)ekm << 2) | ((long long)abuf << 1) | flag;
                     if (lane == 0) mbar_arrive_plain(b_full + 8 * sg);
                     ++it;
                     sg = sg + 1 == kTcsStages ? 0 : sg + 1;
                     if (e2 < 0) break;
                     e = e2;
-                    ett = ntt;
-                    eoff = noff;
+                    egc = ngc;
 #pragma unroll
                     for (int k = 0; k < 3 * kTcsPR; ++k) cur[k] = nxt[k];
                 }
