@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(256) pairs_f64_kernel(const PairsArgs a, int c
         const bool bal = a.sched == PC_BALANCED;
         for (long long i = a.lo + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.hi;
              i += (long long)gridDim.x * blockDim.x) {
-            if (a.tstride > 1 && ((i - a.lo) / a.tile_rows) % a.tstride != a.toff) continue;
+            if (a.tstride > 1 && ((i - a.lo) / a.tile_rows / kTcsOrgG) % a.tstride != a.toff) continue;
             const long long m = bal ? steps_for_dev(a.n, (int)i) : (long long)a.n - 1 - i;
             const double xi = coord_f64(a.xyz, a.dtype, i, 0), yi = coord_f64(a.xyz, a.dtype, i, 1),
                          zi = coord_f64(a.xyz, a.dtype, i, 2);
@@ -890,21 +890,29 @@ int launch_pairs(PairsArgs args, long long n_slots_cap, int* nslots_out, int* nc
     return PC_OK;
 }
 
-// Row tiles of one call: the tiles toff, toff + tstride, ... of [lo, hi) (all of them when
-// tstride = 1) -- pc_pairs_part_async deals a range's tiles round-robin over nparts calls.
+// Row tiles of one call: all tiles of [lo, hi) when tstride = 1, else the blocks of kTcsOrgG tiles
+// toff, toff + tstride, ... -- pc_pairs_part_async deals a range's tile blocks round-robin over nparts
+// calls; the call's i-th tile is absolute tile tile_abs(i) (pairs_kernel.cuh).
 struct TileSel {
     int tstride, toff;
 };
 inline int tiles_of(long long lo, long long hi, int T, TileSel ts) {
     const long long all = (hi - lo + T - 1) / T;
-    return all > ts.toff ? (int)((all - ts.toff + ts.tstride - 1) / ts.tstride) : 0;
+    if (ts.tstride == 1) return (int)all;
+    const long long blocks = (all + kTcsOrgG - 1) / kTcsOrgG;  // the last one may be partial
+    if (blocks <= ts.toff) return 0;
+    const long long nb = (blocks - ts.toff + ts.tstride - 1) / ts.tstride, last = ts.toff + (nb - 1) * ts.tstride;
+    return (int)((nb - 1) * kTcsOrgG + std::min<long long>(kTcsOrgG, all - last * kTcsOrgG));
 }
 // pairs owned by the selected tiles' rows
 long long tile_sel_pairs(long long n, long long lo, long long hi, int T, TileSel ts, int sched) {
     if (ts.tstride == 1) return row_pairs(n, lo, hi, sched);
     long long p = 0;
-    for (long long t = ts.toff; lo + t * T < hi; t += ts.tstride)
+    const int nt = tiles_of(lo, hi, T, ts);
+    for (int i = 0; i < nt; ++i) {
+        const long long t = tile_abs(i, ts.tstride, ts.toff);
         p += row_pairs(n, lo + t * T, std::min(hi, lo + (t + 1) * T), sched);
+    }
     return p;
 }
 
@@ -1015,8 +1023,8 @@ int launch_tcs(const PairsArgs& p, TileSel ts, double* claims_tc, Slot* slots, l
     // fp32 points with the bitmap and PAIRCOUNT_TCS2=1: the SM-pair kernel (pairs_tcs2.cuh)
     const bool pair = tcs2_enabled() && p.dtype == PC_F32 && bits != nullptr && num_sms() >= 2;
     // work units: the diagonals of groups of G consecutive tiles (one column operand for up to G
-    // items) when the call's tiles are whole origin groups; else one item per unit
-    a.G = !pair && ts.tstride == 1 && ts.toff % kTcsOrgG == 0 ? kTcsOrgG : 1;
+    // items; tile parts deal whole groups); the SM-pair kernel: one item per unit
+    a.G = pair ? 1 : kTcsOrgG;
     a.upg = a.cpw + a.G - 1;
     a.items = (long long)((a.n_tiles + a.G - 1) / a.G) * a.upg;
     // units per claim: a power of two keeping the float64 partials (kTcsParts per claim) within

@@ -87,6 +87,13 @@ __device__ __forceinline__ ChunkGeom chunk_geom(const float tmin[3], const float
 #endif
 constexpr int kTcsOrgG = PC_TCS_G;
 static_assert(kTcsOrgG >= 1 && kTcsOrgG <= 4, "an origin group's per-32 boxes: one per lane");
+// Tile parts (pc_pairs_part_async): blocks of kTcsOrgG consecutive row tiles dealt round-robin, part
+// toff of tstride holding blocks toff, toff + tstride, ...  The call's i-th tile is absolute tile
+// tile_abs(i) -- whole origin groups per part, so a part's tensor-core sum keeps the column reuse.
+__host__ __device__ __forceinline__ int tile_abs(int i, int tstride, int toff) {
+    if (tstride == 1) return i + toff;
+    return (i / kTcsOrgG) * (kTcsOrgG * tstride) + toff * kTcsOrgG + i % kTcsOrgG;
+}
 // the origin group's box: the union of the per-32 boxes of its full tiles (rows lo + 256 t ..
 // + 255 < hi), lo a multiple of 32; warp-collective, min / max exact (every caller gets the same box)
 __device__ __forceinline__ void tcs_group_box(const float4* __restrict__ blk_box, int lo, int hi, int tabs, int lane,
@@ -309,7 +316,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
         return g2 > cull_gap2;
     };
     auto tile_box = [&](int tt) {  // the rows of tile tt from the per-32 boxes
-        const int i0t = a.lo + (tt * a.tstride + a.toff) * T;
+        const int i0t = a.lo + tile_abs(tt, a.tstride, a.toff) * T;
         const int i1t = min(i0t + T, a.hi) - 1;
         const int b0 = i0t >> 5, nb = (i1t >> 5) - b0 + 1;
         float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
@@ -352,7 +359,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
             if (len <= 0) continue;  // past the end of the window
             if (SORTED && !DIRECT) {
                 tile_box(tt);
-                const long long jc = (long long)a.lo + ((long long)tt * a.tstride + a.toff) * T + oo + 1;
+                const long long jc = (long long)a.lo + (long long)tile_abs(tt, a.tstride, a.toff) * T + oo + 1;
                 if (union_far(jc, len, a.blk2_box, 10)) {
                     count_path(kPathFar, (unsigned)((len + W - 1) / W));
                     continue;  // every pair of the claim decided by its boxes
@@ -366,7 +373,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
         }
     };
     // first row of tile t of this call (tiles toff, toff + tstride, ... of [lo, hi))
-    auto row0 = [&](int t) -> int { return a.lo + (t * a.tstride + a.toff) * T; };
+    auto row0 = [&](int t) -> int { return a.lo + tile_abs(t, a.tstride, a.toff) * T; };
     if (lane < kNumPaths + 1) s_path[wid][lane] = 0u;
     __syncwarp();
     if (FLAT) {
@@ -695,7 +702,7 @@ __global__ void __launch_bounds__(WARPS * 32, PC_MINB) pairs_kernel(const PairsA
                 if (a.tc_split && !a.tc_bits) {
                     PC_CHECK(T == 256 && W == 256);
                     float gmn[3], gmx[3];
-                    tcs_group_box(a.blk_box, a.lo, a.hi, tile * a.tstride + a.toff, lane, gmn, gmx);
+                    tcs_group_box(a.blk_box, a.lo, a.hi, tile_abs(tile, a.tstride, a.toff), lane, gmn, gmx);
                     tc_skip = tcs_takes(chunk_geom_g(tmin, tmax, gmn, gmx, cl, ch));
                 }
 #ifdef PC_DBG_SKIPALL  // debug (timing only): every dense chunk skipped -- the walk's own cost

@@ -233,7 +233,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTc2Warps * 32, 1) p
         float o[3] = {0.f, 0.f, 0.f};
         const long long C = a.cpw;
         const float* xyz = (const float*)a.xyz;
-        auto row0t = [&](int tt) -> int { return a.lo + (tt * a.tstride + a.toff) * kTcsT; };
+        auto row0t = [&](int tt) -> int { return a.lo + tile_abs(tt, a.tstride, a.toff) * kTcsT; };
         Tc2Walker walk(&a, cid, nclusters);
         auto advance = [&](long long& c_out, long long& u_out) -> bool { return walk.next(c_out, u_out); };
         auto col0 = [&](long long u) -> int {  // this CTA's first column of item u's chunk
@@ -266,7 +266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTc2Warps * 32, 1) p
             if (tt != o_tile) {  // the origin: the centre of the tile's origin group's box (chunk_geom_g's o)
                 o_tile = tt;
                 float gmn[3], gmx[3];
-                tcs_group_box(a.blk_box, a.lo, a.hi, tt * a.tstride + a.toff, lane, gmn, gmx);
+                tcs_group_box(a.blk_box, a.lo, a.hi, tile_abs(tt, a.tstride, a.toff), lane, gmn, gmx);
 #pragma unroll
                 for (int k = 0; k < 3; ++k) o[k] = __fmul_rn(0.5f, __fadd_rn(gmn[k], gmx[k]));
             }

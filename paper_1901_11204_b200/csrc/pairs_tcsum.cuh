@@ -191,7 +191,7 @@ struct TcsArgs {
     int tstride, toff, n_tiles;
     long long L;       // window length (T - 1 + n/2)
     long long cpw;     // chunks per window
-    int G;             // tiles per work unit: kTcsOrgG (tstride 1, toff a multiple of it), else 1
+    int G;             // tiles per work unit: kTcsOrgG (pairs_tcs2_kernel: 1)
     long long upg;     // units per group of G tiles: cpw + G - 1 diagonals
     long long items;   // work units: ceil(n_tiles / G) * upg (pairs_tcs2_kernel: G = 1, n_tiles * cpw)
     long long S;       // units per claim
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(256) tcs_classify_kernel(const TcsArgs a) {
     if (t >= a.n_tiles) return;
     const int n = a.n;
     const int steps_min = (n & 1) ? (n - 1) >> 1 : (n >> 1) - 1;
-    const int i0 = a.lo + ((int)t * a.tstride + a.toff) * kTcsT;
+    const int i0 = a.lo + tile_abs((int)t, a.tstride, a.toff) * kTcsT;
     const bool rows_ok = i0 + kTcsT <= a.hi;
     float tmin[3] = {INFINITY, INFINITY, INFINITY}, tmax[3] = {-INFINITY, -INFINITY, -INFINITY};
     if (rows_ok) {
@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(256) tcs_classify_kernel(const TcsArgs a) {
         }
     }
     float gmin[3] = {0.f, 0.f, 0.f}, gmax[3] = {0.f, 0.f, 0.f};  // the origin group's box
-    if (rows_ok) tcs_group_box(a.blk_box, a.lo, a.hi, (int)t * a.tstride + a.toff, lane, gmin, gmax);
+    if (rows_ok) tcs_group_box(a.blk_box, a.lo, a.hi, tile_abs((int)t, a.tstride, a.toff), lane, gmin, gmax);
     {
         const long long c = c0 + lane;
         const long long off = c * kTcsW;
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
         float o[3] = {0.f, 0.f, 0.f};
         const long long C = a.cpw, UPG = a.upg;
         const int G = a.G;
-        auto row0t = [&](int tt) -> int { return a.lo + (tt * a.tstride + a.toff) * kTcsT; };
+        auto row0t = [&](int tt) -> int { return a.lo + tile_abs(tt, a.tstride, a.toff) * kTcsT; };
         auto unit_col = [&](long long u, long long& gc) -> int {  // the unit's group and first column, wrapped
             gc = u / UPG;
             const int j0 = row0t((int)(gc * G)) + (int)(u - gc * UPG) * kTcsW + 1;
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                     const long long b = i * a.cpw_pad + ch;
                     take = (__ldg(a.bits + (b >> 5)) >> (b & 31)) & 1u;
                 } else {
-                    take = tcs_item_takes(a.blk_box, n, a.lo, a.hi, (int)i * a.tstride + a.toff, a.L, ch);
+                    take = tcs_item_takes(a.blk_box, n, a.lo, a.hi, tile_abs((int)i, a.tstride, a.toff), a.L, ch);
                 }
                 km |= (take ? 1u : 0u) << k;
             }
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                     long long flag = 0;
                     if (egc != a_grp) {
                         // the origin: the centre of the origin group's box (chunk_geom_g's o)
-                        const int tabs = (int)(egc * G) * a.tstride + a.toff;
+                        const int tabs = tile_abs((int)(egc * G), a.tstride, a.toff);
                         if (tabs / kTcsOrgG != o_grp) {
                             o_grp = tabs / kTcsOrgG;
                             float gmn[3], gmx[3];
