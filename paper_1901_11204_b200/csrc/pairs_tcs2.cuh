@@ -379,7 +379,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kTc2Warps * 32, 1) p
                 }
                 ++it;
                 facc = __fadd2_rn(facc, facc2);
-                sum += (double)(facc.x + facc.y);
+                sum += (double)(facc.x + facc.y) * (double)kTcsS;  // (the column operand's scale)
             }
         }
     }

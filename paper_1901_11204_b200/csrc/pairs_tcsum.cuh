@@ -129,6 +129,16 @@ __device__ __forceinline__ unsigned lh(unsigned a, unsigned b) { return __byte_p
 __device__ __forceinline__ unsigned hl(unsigned a, unsigned b) { return __byte_perm(a, b, 0x5432); }
 __device__ __forceinline__ unsigned hh(unsigned a, unsigned b) { return __byte_perm(a, b, 0x7632); }
 constexpr unsigned kBf16One2 = 0x3F803F80u;  // (1, 1)
+// The drain folds PC_TCS_FOLD terms per two reciprocals.  Sixteen: the column operand scales every
+// p by S = 2^-16 (exact; its ones become S), so for the tensor-core chunks' p in [5.5, 9e8] (dmin^2 >
+// 4.5, |a| + |b| <= 3e4) every product of eight S p and its reciprocal stay normal fp32; the sums
+// take the factor back (exact).
+#ifndef PC_TCS_FOLD
+#define PC_TCS_FOLD 8  // (sixteen, scaled: 58.6 vs 57.5 ms at 2^20 -- the drain is latency-, not MUFU-bound)
+#endif
+static_assert(PC_TCS_FOLD == 8 || PC_TCS_FOLD == 16, "eight or sixteen terms per two reciprocals");
+constexpr float kTcsS = PC_TCS_FOLD == 16 ? 1.52587890625e-05f : 1.f;  // 2^-16 or 1
+constexpr unsigned kBf16S2 = PC_TCS_FOLD == 16 ? 0x37803780u : kBf16One2;  // (S, S) in bf16
 
 // Row p of the A operand: a = q - o and A = 1 + |a|^2 (float64, carried as fp32 hi + lo), split.
 // K order (bf16, 32):  a_h a_h a_h a_m a_m a_m a_l a_l | A_h A_m A_l A_lo | 1 1 1 1
@@ -160,13 +170,14 @@ __device__ __forceinline__ void tcs_write_col(unsigned char* d, int p, float bx,
     const float B = (float)Bd, Blo = (float)(Bd - (double)B);
 #endif
     unsigned XYh, XYm, XYl, ZBh, ZBm, ZBl;
-    split3x2(-2.f * bx, -2.f * by, XYh, XYm, XYl);
-    split3x2(-2.f * bz, B, ZBh, ZBm, ZBl);
-    const unsigned lo2 = pk2(Blo, Blo);
+    constexpr float m2 = -2.f * kTcsS;
+    split3x2(m2 * bx, m2 * by, XYh, XYm, XYl);
+    split3x2(m2 * bz, kTcsS * B, ZBh, ZBm, ZBl);
+    const unsigned lo2 = pk2(kTcsS * Blo, kTcsS * Blo);
     *reinterpret_cast<uint4*>(d + tcs_off(p, 0)) = make_uint4(XYh, ll(ZBh, XYm), hl(XYm, ZBm), XYl);
     *reinterpret_cast<uint4*>(d + tcs_off(p, 1)) = make_uint4(ll(ZBl, XYh), hl(XYh, ZBh), XYm, ll(ZBm, XYl));
     *reinterpret_cast<uint4*>(d + tcs_off(p, 2)) = make_uint4(hl(XYl, ZBl), XYh, ll(ZBh, XYm), hl(XYm, ZBm));
-    *reinterpret_cast<uint4*>(d + tcs_off(p, 3)) = make_uint4(kBf16One2, kBf16One2, hh(ZBh, ZBm), hh(ZBl, lo2));
+    *reinterpret_cast<uint4*>(d + tcs_off(p, 3)) = make_uint4(kBf16S2, kBf16S2, hh(ZBh, ZBm), hh(ZBl, lo2));
 }
 
 // Chunk bitmap: bit t * cpw_pad + c set when pairs_tcs_kernel evaluates chunk c of row tile t (whole
@@ -628,23 +639,35 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
 #pragma unroll
                     for (int w = 0; w < kTcsRound / 32; ++w) {
 #pragma unroll
-                        for (int e = 0; e < 32; e += 8) {
-                            const float2 p1 = make_float2(__uint_as_float(v[w][e]), __uint_as_float(v[w][e + 1]));
-                            const float2 p2 = make_float2(__uint_as_float(v[w][e + 2]), __uint_as_float(v[w][e + 3]));
-                            const float2 p3 = make_float2(__uint_as_float(v[w][e + 4]), __uint_as_float(v[w][e + 5]));
-                            const float2 p4 = make_float2(__uint_as_float(v[w][e + 6]), __uint_as_float(v[w][e + 7]));
-                            const float2 m12 = __fmul2_rn(p1, p2), s12 = __fadd2_rn(p1, p2);
-                            const float2 m34 = __fmul2_rn(p3, p4), s34 = __fadd2_rn(p3, p4);
-                            const float2 P = __fmul2_rn(m12, m34);
-                            const float2 Nn = __ffma2_rn(s34, m12, __fmul2_rn(s12, m34));
-                            if (e & 8) acc2 = __ffma2_rn(Nn, make_float2(rcp_approx(P.x), rcp_approx(P.y)), acc2);
+                        for (int e = 0; e < 32; e += PC_TCS_FOLD) {
+                            // four terms (x lanes: even columns, y lanes: odd) -> numerator and denominator
+                            auto quad = [&](int f, float2& Nq, float2& Pq) {
+                                const float2 p1 = make_float2(__uint_as_float(v[w][f]), __uint_as_float(v[w][f + 1]));
+                                const float2 p2 = make_float2(__uint_as_float(v[w][f + 2]), __uint_as_float(v[w][f + 3]));
+                                const float2 p3 = make_float2(__uint_as_float(v[w][f + 4]), __uint_as_float(v[w][f + 5]));
+                                const float2 p4 = make_float2(__uint_as_float(v[w][f + 6]), __uint_as_float(v[w][f + 7]));
+                                const float2 m12 = __fmul2_rn(p1, p2), s12 = __fadd2_rn(p1, p2);
+                                const float2 m34 = __fmul2_rn(p3, p4), s34 = __fadd2_rn(p3, p4);
+                                Pq = __fmul2_rn(m12, m34);
+                                Nq = __ffma2_rn(s34, m12, __fmul2_rn(s12, m34));
+                            };
+                            float2 Nn, P;
+                            quad(e, Nn, P);
+                            if (PC_TCS_FOLD == 16) {  // 1/a + ... + 1/h = (N1 P2 + N2 P1) / (P1 P2)
+                                float2 N2, P2;
+                                quad(e + 8, N2, P2);
+                                Nn = __ffma2_rn(Nn, P2, __fmul2_rn(N2, P));
+                                P = __fmul2_rn(P, P2);
+                            }
+                            if (PC_TCS_FOLD == 8 ? (e & 8) : (e & 16))  // two chains
+                                acc2 = __ffma2_rn(Nn, make_float2(rcp_approx(P.x), rcp_approx(P.y)), acc2);
                             else acc = __ffma2_rn(Nn, make_float2(rcp_approx(P.x), rcp_approx(P.y)), acc);
                         }
                     }
 #endif
                 }
                 acc = __fadd2_rn(acc, acc2);
-                sum += (double)(acc.x + acc.y);
+                sum += (double)(acc.x + acc.y) * (double)kTcsS;
             }
             if (done) break;
         }
