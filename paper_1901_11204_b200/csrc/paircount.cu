@@ -1034,7 +1034,10 @@ int launch_tcs(const PairsArgs& p, TileSel ts, double* claims_tc, Slot* slots, l
     const int grid = pair ? num_sms() & ~1 : num_sms();
     long long S = 1;
     while (S * (kClaimsCap / parts) < a.items) S *= 2;
-    while (S < 128 && S * 2 * (long long)grid * 128 <= a.items) S *= 2;
+#ifndef PC_TCS_SMAX
+#define PC_TCS_SMAX 128  // (2^20: 32 / 64 / 128 / 256 units -> 58.1 / 57.6 / 57.5 / 57.5 ms)
+#endif
+    while (S < PC_TCS_SMAX && S * 2 * (long long)grid * 128 <= a.items) S *= 2;
     a.S = S;
     a.nclaims = (a.items + S - 1) / S;
     *nslots = 0;
