@@ -180,3 +180,26 @@ def test_tcsum_tile_parts_and_reproducibility():
                                       tiling=_lib.PC_TILE_SORTED) for p in range(nparts)]
         assert sum(q.count for q in parts) == r.count and sum(q.pairs for q in parts) == r.pairs
         assert abs(sum(q.sum for q in parts) - r.sum) <= 1e-9 * r.sum, nparts
+
+
+@pytest.mark.parametrize("lo", [12_512, 4_096 + 32])
+def test_tcsum_origin_groups_on_offset_ranges_and_parts(lo):
+    # a range starting on a 32-point block but not on a 256-point tile: the origin groups are counted
+    # from lo; tile parts deal blocks of three tiles (the last block ragged).  PC_TILE_SORTED ranges
+    # index the sorted order (include/paircount.h), so [0, lo) + [lo, n) make the oracle's total
+    n = 70_001
+    x = gen.random_spheres(n, gen.contact_box_edge(n), 17).astype(np.float32)
+    want_c, want_s, pairs = c_oracle.rows(x, 0, n, "balanced")
+    r0, r = _lib.pairs_host(x, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [0, lo, n], tiling=_lib.PC_TILE_SORTED)
+    assert (r0.count + r.count, r0.pairs + r.pairs) == (want_c, pairs)
+    assert abs(r0.sum + r.sum - want_s) <= 1e-6 * want_s
+    (r1,) = _lib.pairs_host(x, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, [lo, n], tiling=_lib.PC_TILE_SORTED)
+    prof = _lib.last_profile()
+    assert (r1.count, r1.pairs) == (r.count, r.pairs) and abs(r1.sum - r.sum) <= 1e-9 * r.sum
+    if TCS:
+        assert prof.kernel == 10 and prof.chunks_tc > 0
+    for nparts in (2, 3, 7):
+        parts = [_lib.pairs_part_host(x, _lib.PC_COLLISION_INVSQ, _lib.PC_BALANCED, lo, n, p, nparts,
+                                      tiling=_lib.PC_TILE_SORTED) for p in range(nparts)]
+        assert sum(q.count for q in parts) == r.count and sum(q.pairs for q in parts) == r.pairs, nparts
+        assert abs(sum(q.sum for q in parts) - r.sum) <= 1e-9 * r.sum, nparts
