@@ -83,7 +83,7 @@ __device__ __forceinline__ ChunkGeom chunk_geom(const float tmin[3], const float
 // (t + k, c - k) of the group's tiles along its diagonal.  Its chunk test: the tile's box (for |a|)
 // and the chunk's box (for |b|, the gap) about the group's centre o.
 #ifndef PC_TCS_G
-#define PC_TCS_G 3  // (2 / 3 / 4 tiles: 70.3 / 69.0 / 70.9 ms at 2^20, each at its best ring depth)
+#define PC_TCS_G 4  // (pipelined drain, 2^20 step: 3 / 4 tiles 62.0 / 61.4 ms, each at its best ring depth)
 #endif
 constexpr int kTcsOrgG = PC_TCS_G;
 static_assert(kTcsOrgG >= 1 && kTcsOrgG <= 4, "an origin group's per-32 boxes: one per lane");

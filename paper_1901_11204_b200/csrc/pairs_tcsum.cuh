@@ -51,20 +51,20 @@ constexpr int kTcsHalf = kTcsOp / 2;               // 128 points
 #endif
 constexpr int kTcsNQ = PC_TCS_NQ, kTcsNP = 256 / kTcsNQ, kTcsNAcc = 2 * kTcsNQ;
 #ifndef PC_TCS_ROUND
-#define PC_TCS_ROUND 128  // accumulator columns per drain round (loaded before the accumulator is released)
+#define PC_TCS_ROUND 64  // accumulator columns per drain round (pipelined: 64 -> 50.3, 32 -> 50.7 ms)
 #endif
 constexpr int kTcsRound = PC_TCS_ROUND;
 static_assert(kTcsNAcc * kTcsNP == 512 && kTcsNP % kTcsRound == 0 && kTcsRound % 32 == 0, "TMEM: 512 columns");
 #ifndef PC_TCS_STAGES
-#define PC_TCS_STAGES 4  // column stages: with G = 3 the dynamic shared memory (161 KB) fits the 164 KB carveout
+#define PC_TCS_STAGES 3  // column stages (G = 4: 2 / 3 stages 61.5 / 61.4 ms; G = 3: 4 beat 3 and 5)
 #endif
 constexpr int kTcsStages = PC_TCS_STAGES;
 #ifndef PC_TCS_KSTEPS  // K = 16 steps per accumulator; a debug knob for A/B of the MMA cost
 #define PC_TCS_KSTEPS 2
 #endif
 #ifndef PC_TCS_PROD
-#define PC_TCS_PROD 2  // producer warps: 11 warps in all (12 slots), 168 registers each; a column operand serves
-                       // up to G items, so two warps keep the MMA fed (3: +0.5 ms, 1: +2.6 ms; 13 warps take 16 slots: spills)
+#define PC_TCS_PROD 3  // producer warps: 12 warps in all (142 registers with the pipelined drain); three beat
+                       // two by 0.5 ms (two beat three before the pipelined drain; 13 warps take 16 slots)
 #endif
 #ifndef PC_TCS_EPI
 #define PC_TCS_EPI 8  // epilogue warps: 4 per accumulator (each all its columns) or 8 (half the columns each)
@@ -133,6 +133,10 @@ constexpr unsigned kBf16One2 = 0x3F803F80u;  // (1, 1)
 // p by S = 2^-16 (exact; its ones become S), so for the tensor-core chunks' p in [5.5, 9e8] (dmin^2 >
 // 4.5, |a| + |b| <= 3e4) every product of eight S p and its reciprocal stay normal fp32; the sums
 // take the factor back (exact).
+#ifndef PC_TCS_PIPE
+#define PC_TCS_PIPE 1  // drain: the next round's TMEM loads in flight while a round folds (57.5 -> 50.3 ms)
+#endif
+static_assert(!PC_TCS_PIPE || PC_TCS_ROUND < 256, "a pipelined drain needs two rounds or more");
 #ifndef PC_TCS_FOLD
 #define PC_TCS_FOLD 8  // (sixteen, scaled: 58.6 vs 57.5 ms at 2^20 -- the drain is latency-, not MUFU-bound)
 #endif
@@ -621,21 +625,8 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                 // the accumulator in rounds of kTcsRound columns; released after the last round's loads
                 const unsigned tbase = tmem + ((unsigned)(quad * 32) << 16) + (unsigned)(k * kTcsNP + cpart * kTcsSpan);
                 float2 acc = make_float2(0.f, 0.f), acc2 = make_float2(0.f, 0.f);  // two chains
-#pragma unroll 1
-                for (int rd = 0; rd < kTcsSpan / kTcsRound; ++rd) {
-                    unsigned v[kTcsRound / 32][32];
-#pragma unroll
-                    for (int w = 0; w < kTcsRound / 32; ++w) PC_TC_LD32(v[w], tbase + (unsigned)(kTcsRound * rd) + 32u * w);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    if (rd == kTcsSpan / kTcsRound - 1) {
-                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive_plain(acc_empty + 8 * k);
-                    }
-#ifdef PC_TCS_DBG_LIGHT  // debug (timing only): the drain without the arithmetic
-#pragma unroll
-                    for (int w = 0; w < kTcsRound / 32; ++w) acc.x += __uint_as_float(v[w][w]);
-#else
+                // the fold of one round's values: eight (or sixteen) terms per two reciprocals, two chains
+                auto fold = [&](unsigned (&v)[kTcsRound / 32][32]) {
 #pragma unroll
                     for (int w = 0; w < kTcsRound / 32; ++w) {
 #pragma unroll
@@ -664,8 +655,60 @@ __global__ void __launch_bounds__(kTcsWarps * 32) pairs_tcs_kernel(const TcsArgs
                             else acc = __ffma2_rn(Nn, make_float2(rcp_approx(P.x), rcp_approx(P.y)), acc);
                         }
                     }
+                };
+#if PC_TCS_PIPE
+                // two buffers of kTcsRound columns: the next round's loads in flight while this one folds
+                // (released after the last round's loads, as below)
+                {
+                    constexpr int NR = kTcsSpan / kTcsRound;
+                    unsigned va[kTcsRound / 32][32], vb[kTcsRound / 32][32];
+#pragma unroll
+                    for (int w = 0; w < kTcsRound / 32; ++w) PC_TC_LD32(va[w], tbase + 32u * w);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int rd = 0; rd < NR; ++rd) {
+                        unsigned(&vc)[kTcsRound / 32][32] = (rd & 1) ? vb : va;
+                        unsigned(&vn)[kTcsRound / 32][32] = (rd & 1) ? va : vb;
+                        if (rd + 1 < NR) {
+#pragma unroll
+                            for (int w = 0; w < kTcsRound / 32; ++w)
+                                PC_TC_LD32(vn[w], tbase + (unsigned)(kTcsRound * (rd + 1)) + 32u * w);
+                        }
+                        fold(vc);
+                        if (rd + 1 < NR) {
+                            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                            for (int w = 0; w < kTcsRound / 32; ++w)
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) asm volatile("" : "+r"(vn[w][i]));  // (after the wait)
+                            if (rd + 1 == NR - 1) {
+                                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive_plain(acc_empty + 8 * k);
+                            }
+                        }
+                    }
+                }
+#else
+#pragma unroll 1
+                for (int rd = 0; rd < kTcsSpan / kTcsRound; ++rd) {
+                    unsigned v[kTcsRound / 32][32];
+#pragma unroll
+                    for (int w = 0; w < kTcsRound / 32; ++w) PC_TC_LD32(v[w], tbase + (unsigned)(kTcsRound * rd) + 32u * w);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (rd == kTcsSpan / kTcsRound - 1) {
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_plain(acc_empty + 8 * k);
+                    }
+#ifdef PC_TCS_DBG_LIGHT  // debug (timing only): the drain without the arithmetic
+#pragma unroll
+                    for (int w = 0; w < kTcsRound / 32; ++w) acc.x += __uint_as_float(v[w][w]);
+#else
+                    fold(v);
 #endif
                 }
+#endif
                 acc = __fadd2_rn(acc, acc2);
                 sum += (double)(acc.x + acc.y) * (double)kTcsS;
             }
