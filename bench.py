@@ -811,8 +811,8 @@ def run_ours(args):
                 "frac_of_pipelined_proto": per_clk_sm / 35.7,
                 "basis": "FMA 128 lane-ops/clk/SM / 2 per pair; MUFU 16/clk/SM / 0.25 per pair; TMEM loads alone "
                          "78.7 pairs/clk/SM and the same epilogue on a static operand 35.7 "
-                         "(scripts/tc_sum_proto.cu, B200); ncu of this kernel: FMA pipe 54 %, XU 54 %, "
-                         "tensor 25 %, issue 46 % (profiles/r2_ncu_tcs_kernel.txt)",
+                         "(scripts/tc_sum_proto.cu, B200); ncu of this kernel: FMA pipe 62 %, XU 62 %, "
+                         "tensor 30 %, issue 50 % (profiles/r2_ncu_tcs_kernel.txt)",
             },
             "ffma_kernel": ffma_part,
             "step_kernels_ms": {"pairs_tcs_kernel": tc_ms_avg, "pairs_kernel_sorted": ffma_ms_avg},
