@@ -1037,7 +1037,10 @@ int launch_tcs(const PairsArgs& p, TileSel ts, double* claims_tc, Slot* slots, l
 #ifndef PC_TCS_SMAX
 #define PC_TCS_SMAX 128  // (2^20: 32 / 64 / 128 / 256 units -> 58.1 / 57.6 / 57.5 / 57.5 ms)
 #endif
-    while (S < PC_TCS_SMAX && S * 2 * (long long)grid * 128 <= a.items) S *= 2;
+#ifndef PC_TCS_CPC
+#define PC_TCS_CPC 32  // claims per CTA the claim size keeps at least (8 tile parts at 2^20: 128 -> 8.67, 32 -> 8.56 ms)
+#endif
+    while (S < PC_TCS_SMAX && S * 2 * (long long)grid * PC_TCS_CPC <= a.items) S *= 2;
     a.S = S;
     a.nclaims = (a.items + S - 1) / S;
     *nslots = 0;
