@@ -177,8 +177,8 @@ int pc_pairs_host(const void* xyz_host, int32_t dtype, int64_t n, int32_t intera
                   pc_pairs_result* results);
 
 /* One part of a row range for multi-GPU work: the kernel's row tiles of
- * [lo, hi) dealt round-robin over nparts calls in blocks of three tiles
- * (blocks part, part + nparts, ...; three tiles are one origin group of the
+ * [lo, hi) dealt round-robin over nparts calls in blocks of four tiles
+ * (blocks part, part + nparts, ...; four tiles are one origin group of the
  * tensor-core sum), so every part holds the same mix of near and far work however the
  * points are ordered (with PC_TILE_SORTED, spatially sorted).  The nparts
  * results add up to the [lo, hi) result (counts exactly).  A part is not a

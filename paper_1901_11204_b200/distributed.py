@@ -10,7 +10,7 @@ ranks, both with no exchange but the final reduction:
   ``spi_parallel(workers=world).partials``.  Under the standard schedule rows
   own n-1-i pairs and the cuts r_g = n - n*sqrt(1 - g/G) equalise the work.
 * ``"tiles"`` -- the whole-range call's row tiles dealt round-robin in blocks
-  of three (``pc_pairs_part_*``): rank r runs blocks r, r+G, r+2G, ...  For fp32
+  of four (``pc_pairs_part_*``): rank r runs blocks r, r+G, r+2G, ...  For fp32
   spheres this is the path a single GPU takes (spatially sorted points,
   PC_TILE_SORTED: the inverse-square sum with tile-local Gram chunks, the
   contact count with box pruning) split G ways; on sorted points contiguous
